@@ -1,0 +1,203 @@
+/*
+ * anyq_b200.h — C-ABI of the B200-native any4 quantize + LUT-GEMM path.
+ *
+ * This is the drop-in boundary for the reference library `anyq`
+ * (/root/reference/proj). The reference has no FFI of its own: its boundary is
+ * the C++ headers proj/include/anyq/{core,learner,pack,quantize,qgemm}.hpp.
+ * Every entry point below replaces one of those functions (cited per entry)
+ * with the same argument meaning and the same error classes (returned as
+ * anyq_status, see core.hpp:27-74). All compute runs on the GPU; there is no
+ * CPU fallback. The library fails with ANYQ_ERR_CUDA when no device is usable.
+ *
+ * Two call styles:
+ *   - anyq_*      : host buffers in, host buffers out (value semantics, like
+ *                   the reference). H2D/D2H staging happens inside the call.
+ *   - anyq_dev_*  : device pointers + cudaStream_t (passed as void*), stream
+ *                   ordered, no host synchronisation; used for timed paths.
+ *
+ * Layout conventions follow the reference exactly: row-major fp32 matrices,
+ * packed codes little-end-first with rows padded to a byte boundary
+ * (pack.hpp:45-51), one LUT of 2^bits fp32 values per row (pack.hpp:27),
+ * group scales indexed by ScaleSet::group_of (scaling.hpp:36-45).
+ */
+#ifndef ANYQ_B200_H
+#define ANYQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; one per exception class of core.hpp:27-74. */
+typedef enum anyq_status {
+  ANYQ_OK = 0,
+  ANYQ_ERR_SHAPE = 1,       /* ShapeError */
+  ANYQ_ERR_CONFIG = 2,      /* ConfigError */
+  ANYQ_ERR_CODE_RANGE = 3,  /* CodeRangeError */
+  ANYQ_ERR_NONFINITE = 4,   /* NonFiniteError */
+  ANYQ_ERR_STATS = 5,       /* StatsError */
+  ANYQ_ERR_IO = 6,          /* IoError */
+  ANYQ_ERR_MAGIC = 7,       /* MagicError */
+  ANYQ_ERR_VERSION = 8,     /* VersionError */
+  ANYQ_ERR_TRUNCATED = 9,   /* TruncatedError */
+  ANYQ_ERR_INVARIANT = 10,  /* InvariantError */
+  ANYQ_ERR_INTERNAL = 11,   /* anyq::Error (internal assertion) */
+  ANYQ_ERR_CUDA = 12,       /* device / driver failure (no reference twin) */
+} anyq_status;
+
+/* Message of the last error raised on the calling thread ("" if none). */
+const char* anyq_last_error(void);
+
+/* Enums mirror core.hpp:78-96 and pack.hpp:17-19 value for value. */
+enum { ANYQ_CB_INT = 0, ANYQ_CB_FP4 = 1, ANYQ_CB_NF4 = 2, ANYQ_CB_ANY = 3 };
+enum {
+  ANYQ_G_TENSOR = 0,
+  ANYQ_G_ROW = 1,
+  ANYQ_G_COLUMN = 2,
+  ANYQ_G_GROUP = 3,
+  ANYQ_G_BLOCK = 4
+};
+enum { ANYQ_INIT_KMPP = 0, ANYQ_INIT_RANDOM = 1, ANYQ_INIT_GRID = 2, ANYQ_INIT_NF4 = 3 };
+enum { ANYQ_W_WEIGHTS = 0, ANYQ_W_ACTS = 1, ANYQ_W_FULL = 2 };
+enum { ANYQ_LAYOUT_ROWMAJOR = 0, ANYQ_LAYOUT_KTILED = 1 };
+enum { ANYQ_STORE_FP16 = 0, ANYQ_STORE_BF16 = 1, ANYQ_STORE_FP32 = 2 };
+
+/* QuantConfig + LearnerConfig (core.hpp:98-121), flattened. */
+typedef struct anyq_config {
+  int32_t bits;               /* 2,3,4,8 */
+  int32_t codebook;           /* ANYQ_CB_* */
+  int32_t granularity;        /* ANYQ_G_* */
+  int32_t group_size;
+  int32_t block_size;
+  int32_t symmetric;
+  int32_t int_range_shifted;
+  int32_t init;               /* ANYQ_INIT_* */
+  int32_t max_iters;
+  float rel_tol;
+  int32_t restarts;
+  int32_t weighting;          /* ANYQ_W_* */
+  int32_t check_invariants;
+  int32_t reserved;
+  uint64_t seed;
+} anyq_config;
+
+/* Defaults of core.hpp:98-121 (IntGrid, 4 bits, groupwise 128, kmeans++...). */
+void anyq_config_default(anyq_config* cfg);
+
+/* QuantizedTensor (pack.hpp:21-39) as flat host arrays. */
+typedef struct anyq_qtensor {
+  int64_t rows, cols;
+  anyq_config cfg;
+  int32_t layout;      /* ANYQ_LAYOUT_* */
+  int32_t tile_k;
+  int32_t lut_store;   /* ANYQ_STORE_* */
+  int32_t scale_store; /* ANYQ_STORE_* */
+  uint8_t* codes;      /* rows * packed_bytes_per_row(cols, bits) */
+  float* luts;         /* rows * 2^bits for ANYQ_CB_ANY, else NULL */
+  float* alphas;       /* num_groups */
+  float* betas;        /* num_groups */
+  int64_t num_groups;
+} anyq_qtensor;
+
+/* Sizes the caller must allocate for an anyq_qtensor of this shape/config. */
+int64_t anyq_packed_bytes_per_row(int64_t cols, int32_t bits); /* pack.hpp:45 */
+int64_t anyq_num_groups(const anyq_config* cfg, int64_t rows, int64_t cols);
+int64_t anyq_lut_entries(const anyq_config* cfg);
+
+/* ---------------------------------------------------------------------------
+ * Quantization (host buffers)
+ * ------------------------------------------------------------------------- */
+
+/* learner.hpp:74 quantize_any(w, cfg, exj, threads). exj may be NULL.
+ * `row_offset` is added to the local row index when keying the per-row RNG
+ * (rng_for_row(seed, row_offset + i)); pass 0 for reference semantics on a
+ * whole matrix, or the first global row when a matrix is split across GPUs.
+ * out must have codes/luts/alphas/betas allocated with the sizes above. */
+anyq_status anyq_quantize_any(const float* w, int64_t rows, int64_t cols,
+                              const anyq_config* cfg, const float* exj,
+                              int64_t row_offset, anyq_qtensor* out);
+
+/* quantize.hpp:17 quantize_fixed(w, cfg): RTN onto int/fp4/nf4 tables. */
+anyq_status anyq_quantize_fixed(const float* w, int64_t rows, int64_t cols,
+                                const anyq_config* cfg, anyq_qtensor* out);
+
+/* ---------------------------------------------------------------------------
+ * Packing / layout / dequant (host buffers, computed on device)
+ * ------------------------------------------------------------------------- */
+
+/* pack.hpp:50 pack_codes / pack.hpp:51 unpack_codes. */
+anyq_status anyq_pack_codes(const uint8_t* codes, int64_t rows, int64_t cols,
+                            int32_t bits, uint8_t* packed);
+anyq_status anyq_unpack_codes(const uint8_t* packed, int64_t rows, int64_t cols,
+                              int32_t bits, uint8_t* codes);
+
+/* pack.hpp:86-87 to_ktiled / from_ktiled on the packed codes of a tensor. */
+anyq_status anyq_ktile_codes(const uint8_t* packed, int64_t rows, int64_t cols,
+                             int32_t bits, int32_t tile_k, int32_t inverse,
+                             uint8_t* out);
+
+/* pack.hpp:68 narrowed(qt): LUT/scales rounded to their 16-bit stores and
+ * widened back, in place on the host arrays of qt. */
+anyq_status anyq_narrow_inplace(anyq_qtensor* qt);
+
+/* pack.hpp:98 dequantize(qt) -> rows x cols fp32. */
+anyq_status anyq_dequantize(const anyq_qtensor* qt, float* w_out);
+
+/* ---------------------------------------------------------------------------
+ * GEMM (host buffers)
+ * ------------------------------------------------------------------------- */
+
+/* qgemm.hpp:36 gemm_fused(x, qt, plan): y[m x rows] = x[m x cols] * W^T with
+ * W = dequant(qt). Reduction over k ascending in fp32 exactly as the
+ * reference, so the result is bit-identical to gemm_fused / gemm_reference.
+ * plan_layout/plan_tile_k reproduce GemmPlan's layout check (qgemm.cpp:75). */
+anyq_status anyq_gemm_fused(const float* x, int64_t m, const anyq_qtensor* qt,
+                            int32_t plan_layout, int32_t plan_tile_k, float* y);
+
+/* qgemm.hpp:28 gemm_dense(x, w). */
+anyq_status anyq_gemm_dense(const float* x, int64_t m, const float* w, int64_t n,
+                            int64_t k, float* y);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident path (timed). All pointers are device pointers; `stream`
+ * is a cudaStream_t. Calls are asynchronous and stream ordered.
+ * ------------------------------------------------------------------------- */
+
+/* Opaque prepacked weight tensor living in HBM (codes in the fragment-
+ * ordered tile layout, LUT + alpha/beta narrowed to fp16). */
+typedef struct anyq_dev_tensor anyq_dev_tensor;
+
+/* Build a device tensor from a host QuantizedTensor (narrowing the LUT and
+ * scales to fp16 exactly like narrowed(); pack.cpp:159-169). */
+anyq_status anyq_dev_tensor_create(const anyq_qtensor* qt, anyq_dev_tensor** out);
+void anyq_dev_tensor_destroy(anyq_dev_tensor* t);
+/* Bytes the GEMM must stream per call (codes + scales + LUT). */
+int64_t anyq_dev_tensor_weight_bytes(const anyq_dev_tensor* t);
+int64_t anyq_dev_tensor_rows(const anyq_dev_tensor* t);
+int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t);
+
+/* y[m x rows] (bf16) = x[m x cols] (bf16) * dequant(W)^T on the tensor-core
+ * LUT path (fp32 accumulation). m <= 64. Device pointers. */
+anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
+                               int64_t m, void* y_bf16, float* y_f32,
+                               void* stream);
+
+/* Device quantize: rows [row_offset, row_offset+rows) of a matrix, fp32 in,
+ * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device. */
+anyq_status anyq_dev_quantize_any(const float* w_dev, int64_t rows, int64_t cols,
+                                  const anyq_config* cfg, const float* exj_dev,
+                                  int64_t row_offset, uint8_t* codes_dev,
+                                  float* luts_dev, float* alphas_dev,
+                                  float* betas_dev, void* stream);
+
+/* Number of kernel launches issued by this library since load (for the
+ * bench's gpu_launches accounting). */
+uint64_t anyq_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ANYQ_B200_H */
