@@ -1,0 +1,416 @@
+"""Python mirror of the reference `anyq::` hot-path API, backed by the B200
+C-ABI library (include/anyq_b200.h, paper_2507_04610_b200/_lib/libanyq_b200.so).
+
+Names, argument meaning and error classes follow proj/include/anyq/*.hpp:
+
+  quantize_any      learner.hpp:74          quantize / quantize_fixed  quantize.hpp:17-23
+  pack_codes        pack.hpp:50             unpack_codes               pack.hpp:51
+  to_ktiled         pack.hpp:86             from_ktiled                pack.hpp:87
+  narrowed          pack.hpp:68             dequantize                 pack.hpp:98
+  make_plan         qgemm.hpp:24            gemm_dense                 qgemm.hpp:28
+  gemm_reference    qgemm.hpp:31            gemm_fused                 qgemm.hpp:36
+  apply_format      quantize.hpp:33         storage_bits_per_entry     codebooks.hpp:53
+
+Every call runs on the GPU. When the CUDA library or a device is missing the
+calls raise (CudaError / OSError) — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._abi import (  # noqa: F401  (re-exported vocabulary)
+    CB_ANY, CB_FP4, CB_INT, CB_NF4, G_BLOCK, G_COLUMN, G_GROUP, G_ROW, G_TENSOR,
+    INIT_GRID, INIT_KMPP, INIT_NF4, INIT_RANDOM, LAYOUT_KTILED, LAYOUT_ROWMAJOR,
+    STORE_BF16, STORE_FP16, STORE_FP32, W_ACTS, W_FULL, W_WEIGHTS, Config, default_config,
+)
+from .qtensor import QuantizedTensor
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libanyq_b200.so")
+
+
+# ---------------------------------------------------------------------------
+# errors (core.hpp:27-74)
+# ---------------------------------------------------------------------------
+class Error(RuntimeError):
+    status = 11
+
+
+class ShapeError(Error):
+    status = 1
+
+
+class ConfigError(Error):
+    status = 2
+
+
+class CodeRangeError(Error):
+    status = 3
+
+
+class NonFiniteError(Error):
+    status = 4
+
+
+class StatsError(Error):
+    status = 5
+
+
+class IoError(Error):
+    status = 6
+
+
+class MagicError(IoError):
+    status = 7
+
+
+class VersionError(IoError):
+    status = 8
+
+
+class TruncatedError(IoError):
+    status = 9
+
+
+class InvariantError(IoError):
+    status = 10
+
+
+class CudaError(Error):
+    status = 12
+
+
+_BY_STATUS = {
+    c.status: c
+    for c in (ShapeError, ConfigError, CodeRangeError, NonFiniteError, StatsError, IoError,
+              MagicError, VersionError, TruncatedError, InvariantError, Error, CudaError)
+}
+
+_lib_handle = None
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib_handle
+    if _lib_handle is not None:
+        return _lib_handle
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"{LIB_PATH} not built; run __graft_entry__.build() or make -C "
+                      "paper_2507_04610_b200/csrc")
+    L = C.CDLL(LIB_PATH)
+    i64, i32, st = C.c_int64, C.c_int32, C.c_int
+    fptr, u8 = C.POINTER(C.c_float), C.POINTER(C.c_uint8)
+    cfg, qt = C.POINTER(_abi.Config), C.POINTER(_abi.QTensor)
+    vp = C.c_void_p
+    sigs = {
+        "anyq_last_error": (C.c_char_p, []),
+        "anyq_launch_count": (C.c_uint64, []),
+        "anyq_config_default": (None, [cfg]),
+        "anyq_packed_bytes_per_row": (i64, [i64, i32]),
+        "anyq_num_groups": (i64, [cfg, i64, i64]),
+        "anyq_lut_entries": (i64, [cfg]),
+        "anyq_quantize_any": (st, [fptr, i64, i64, cfg, fptr, i64, qt]),
+        "anyq_quantize_fixed": (st, [fptr, i64, i64, cfg, qt]),
+        "anyq_pack_codes": (st, [u8, i64, i64, i32, u8]),
+        "anyq_unpack_codes": (st, [u8, i64, i64, i32, u8]),
+        "anyq_ktile_codes": (st, [u8, i64, i64, i32, i32, i32, u8]),
+        "anyq_narrow_inplace": (st, [qt]),
+        "anyq_dequantize": (st, [qt, fptr]),
+        "anyq_gemm_fused": (st, [fptr, i64, qt, i32, i32, fptr]),
+        "anyq_gemm_dense": (st, [fptr, i64, fptr, i64, i64, fptr]),
+        "anyq_dev_tensor_create": (st, [qt, C.POINTER(vp)]),
+        "anyq_dev_tensor_destroy": (None, [vp]),
+        "anyq_dev_tensor_weight_bytes": (i64, [vp]),
+        "anyq_dev_tensor_rows": (i64, [vp]),
+        "anyq_dev_tensor_cols": (i64, [vp]),
+        "anyq_dev_gemm_bf16": (st, [vp, vp, i64, vp, vp, vp]),
+        "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib_handle = L
+    return L
+
+
+# Symbols include/anyq_b200.h declares (checked by the CPU test suite).
+EXPORTED_SYMBOLS = (
+    "anyq_last_error", "anyq_config_default", "anyq_packed_bytes_per_row", "anyq_num_groups",
+    "anyq_lut_entries", "anyq_quantize_any", "anyq_quantize_fixed", "anyq_pack_codes",
+    "anyq_unpack_codes", "anyq_ktile_codes", "anyq_narrow_inplace", "anyq_dequantize",
+    "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
+    "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
+    "anyq_dev_gemm_bf16", "anyq_dev_quantize_any", "anyq_launch_count",
+)
+
+
+def _check(status: int):
+    if status != 0:
+        msg = lib().anyq_last_error().decode()
+        raise _BY_STATUS.get(status, Error)(msg)
+
+
+def launch_count() -> int:
+    return int(lib().anyq_launch_count())
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# ---------------------------------------------------------------------------
+# formats (quantize.cpp:34-64)
+# ---------------------------------------------------------------------------
+def apply_format(cfg: Config, fmt: str) -> Config:
+    table = {
+        "int2": (CB_INT, 2), "int3": (CB_INT, 3), "int4": (CB_INT, 4), "int8": (CB_INT, 8),
+        "fp4": (CB_FP4, 4), "nf4": (CB_NF4, 4),
+        "any2": (CB_ANY, 2), "any3": (CB_ANY, 3), "any4": (CB_ANY, 4), "any8": (CB_ANY, 8),
+    }
+    if fmt not in table:
+        raise ConfigError(f"unknown format '{fmt}'")
+    cfg.codebook, cfg.bits = table[fmt]
+    return cfg
+
+
+def format_name(cfg: Config) -> str:
+    return {CB_INT: f"int{cfg.bits}", CB_FP4: "fp4", CB_NF4: "nf4", CB_ANY: f"any{cfg.bits}"}[
+        cfg.codebook]
+
+
+def storage_bits_per_entry(cfg: Config, rows: int, cols: int) -> float:
+    """codebooks.cpp:99-121 (pure arithmetic on the config)."""
+    groups = _abi.num_groups(cfg, rows, cols)
+    lut_bits = rows * (1 << cfg.bits) * 16.0 if cfg.codebook == CB_ANY else 0.0
+    return cfg.bits + (groups * 2.0 * 16.0 + lut_bits) / (float(rows) * float(cols))
+
+
+# ---------------------------------------------------------------------------
+# quantization
+# ---------------------------------------------------------------------------
+def quantize_any(w, cfg: Config, exj=None, row_offset: int = 0) -> QuantizedTensor:
+    w = _f32(w)
+    rows, cols = w.shape
+    qt = QuantizedTensor.empty(rows, cols, cfg)
+    c = qt.as_c()
+    e = None if exj is None else _f32(exj)
+    if e is not None and e.size != cols:
+        raise StatsError(f"sample weights: stats length {e.size} does not match row length {cols}")
+    _check(lib().anyq_quantize_any(_abi.fp(w), rows, cols, C.byref(qt.cfg),
+                                   None if e is None else _abi.fp(e), row_offset, C.byref(c)))
+    return qt
+
+
+def quantize_fixed(w, cfg: Config) -> QuantizedTensor:
+    w = _f32(w)
+    rows, cols = w.shape
+    qt = QuantizedTensor.empty(rows, cols, cfg)
+    c = qt.as_c()
+    _check(lib().anyq_quantize_fixed(_abi.fp(w), rows, cols, C.byref(qt.cfg), C.byref(c)))
+    return qt
+
+
+def quantize(w, cfg: Config, stats: dict | None = None, module_name: str = "",
+             threads: int = 1) -> QuantizedTensor:
+    """quantize.cpp:25-32; `stats` maps module name -> E|x_j| (ActivationStats)."""
+    if cfg.codebook != CB_ANY:
+        return quantize_fixed(w, cfg)
+    exj = None
+    if stats is not None:
+        if module_name not in stats:
+            raise StatsError(f"no activation stats for module '{module_name}'")
+        exj = _f32(stats[module_name])
+        if exj.size != np.shape(w)[1]:
+            raise StatsError("activation stats channel count mismatch")
+    return quantize_any(w, cfg, exj)
+
+
+# ---------------------------------------------------------------------------
+# packing / layout / dequant
+# ---------------------------------------------------------------------------
+def pack_codes(codes, bits: int) -> np.ndarray:
+    codes = np.ascontiguousarray(codes, np.uint8)
+    rows, cols = codes.shape
+    out = np.zeros(rows * _abi.packed_bytes_per_row(cols, bits), np.uint8)
+    _check(lib().anyq_pack_codes(_abi.u8p(codes), rows, cols, bits, _abi.u8p(out)))
+    return out
+
+
+def unpack_codes(packed, rows: int, cols: int, bits: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, np.uint8)
+    if packed.size != rows * _abi.packed_bytes_per_row(cols, bits):
+        raise ShapeError("unpack_codes: packed size does not match shape")
+    out = np.zeros((rows, cols), np.uint8)
+    _check(lib().anyq_unpack_codes(_abi.u8p(packed), rows, cols, bits, _abi.u8p(out)))
+    return out
+
+
+def _retile(qt: QuantizedTensor, tile_k: int, inverse: int) -> np.ndarray:
+    out = np.empty_like(qt.codes)
+    _check(lib().anyq_ktile_codes(_abi.u8p(qt.codes), qt.rows, qt.cols, qt.cfg.bits, tile_k,
+                                  inverse, _abi.u8p(out)))
+    return out
+
+
+def from_ktiled(qt: QuantizedTensor) -> QuantizedTensor:
+    if qt.layout == LAYOUT_ROWMAJOR:
+        return qt
+    out = qt.clone()
+    out.codes = _retile(qt, qt.tile_k, 1)
+    out.layout, out.tile_k = LAYOUT_ROWMAJOR, 1
+    return out
+
+
+def to_ktiled(qt: QuantizedTensor, tile_k: int) -> QuantizedTensor:
+    if tile_k < 1:
+        raise ConfigError("tile_k must be >= 1")
+    src = from_ktiled(qt) if qt.layout == LAYOUT_KTILED else qt
+    out = src.clone()
+    out.codes = _retile(src, tile_k, 0)
+    out.layout, out.tile_k = LAYOUT_KTILED, tile_k
+    return out
+
+
+def narrowed(qt: QuantizedTensor) -> QuantizedTensor:
+    out = qt.clone()
+    c = out.as_c()
+    _check(lib().anyq_narrow_inplace(C.byref(c)))
+    return out
+
+
+def dequantize(qt: QuantizedTensor) -> np.ndarray:
+    out = np.empty((qt.rows, qt.cols), np.float32)
+    c = qt.as_c()
+    _check(lib().anyq_dequantize(C.byref(c), _abi.fp(out)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# GEMM
+# ---------------------------------------------------------------------------
+@dataclass
+class GemmPlan:
+    """qgemm.hpp:16-22."""
+
+    m: int
+    n: int
+    k: int
+    layout: int = LAYOUT_ROWMAJOR
+    tile_k: int = 1
+
+
+def make_plan(x, qt: QuantizedTensor) -> GemmPlan:
+    x = np.asarray(x)
+    return GemmPlan(m=x.shape[0], n=qt.rows, k=qt.cols, layout=qt.layout, tile_k=qt.tile_k)
+
+
+def gemm_dense(x, w) -> np.ndarray:
+    x, w = _f32(x), _f32(w)
+    if x.shape[1] != w.shape[1]:
+        raise ShapeError("gemm: reduction dimensions differ")
+    y = np.empty((x.shape[0], w.shape[0]), np.float32)
+    _check(lib().anyq_gemm_dense(_abi.fp(x), x.shape[0], _abi.fp(w), w.shape[0], w.shape[1],
+                                 _abi.fp(y)))
+    return y
+
+
+def gemm_reference(x, qt: QuantizedTensor) -> np.ndarray:
+    x = _f32(x)
+    if x.shape[1] != qt.cols:
+        raise ShapeError("gemm_reference: reduction dimensions differ")
+    return gemm_dense(x, dequantize(qt))
+
+
+def gemm_fused(x, qt: QuantizedTensor, plan: GemmPlan | None = None) -> np.ndarray:
+    """Bit-exact LUT GEMM on the GPU (same k-ascending fp32 order as qgemm.cpp)."""
+    x = _f32(x)
+    if x.shape[1] != qt.cols:
+        raise ShapeError("gemm_fused: reduction dimensions differ")
+    plan = plan or make_plan(x, qt)
+    if plan.m != x.shape[0] or plan.n != qt.rows or plan.k != qt.cols:
+        raise ShapeError("gemm_fused: plan does not match operands")
+    y = np.empty((x.shape[0], qt.rows), np.float32)
+    c = qt.as_c()
+    _check(lib().anyq_gemm_fused(_abi.fp(x), x.shape[0], C.byref(c), plan.layout, plan.tile_k,
+                                 _abi.fp(y)))
+    return y
+
+
+# ---------------------------------------------------------------------------
+# device-resident fast path (tensor-core LUT GEMM)
+# ---------------------------------------------------------------------------
+class DeviceTensor:
+    """A prepacked any4/int4/nf4/fp4 weight resident in HBM.
+
+    `gemm(x, y, y32=None, stream=None)` takes torch CUDA tensors (bf16 x of
+    shape [m, cols], bf16 y of shape [m, rows]) and launches the tcgen05 LUT
+    GEMM on `stream` (default: torch's current stream).
+    """
+
+    def __init__(self, qt: QuantizedTensor):
+        self._h = C.c_void_p()
+        c = qt.as_c()
+        _check(lib().anyq_dev_tensor_create(C.byref(c), C.byref(self._h)))
+        self.rows, self.cols = qt.rows, qt.cols
+        self.weight_bytes = int(lib().anyq_dev_tensor_weight_bytes(self._h))
+
+    def close(self):
+        if self._h:
+            lib().anyq_dev_tensor_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def gemm_ptr(self, x_ptr: int, m: int, y_ptr: int, y32_ptr: int | None, stream: int):
+        _check(lib().anyq_dev_gemm_bf16(self._h, C.c_void_p(x_ptr), m, C.c_void_p(y_ptr),
+                                        C.c_void_p(y32_ptr) if y32_ptr else None,
+                                        C.c_void_p(stream)))
+
+    def gemm(self, x, y=None, y32=None, stream=None):
+        import torch
+
+        assert x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()
+        m = x.shape[0]
+        if x.shape[1] != self.cols:
+            raise ShapeError("gemm: reduction dimensions differ")
+        if y is None:
+            y = torch.empty((m, self.rows), dtype=torch.bfloat16, device=x.device)
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        self.gemm_ptr(x.data_ptr(), m, y.data_ptr(), y32.data_ptr() if y32 is not None else None,
+                      s.cuda_stream)
+        return y
+
+
+def dev_quantize_any(w, cfg: Config, exj=None, row_offset: int = 0, stream=None):
+    """Device-resident quantize_any on torch CUDA tensors.
+
+    Returns (codes uint8 [rows, bpr], luts f32 [rows, 2^bits], alphas, betas)
+    as torch tensors in the reference layout.
+    """
+    import torch
+
+    assert w.is_cuda and w.dtype == torch.float32 and w.is_contiguous()
+    rows, cols = w.shape
+    dev = w.device
+    ng = _abi.num_groups(cfg, rows, cols)
+    codes = torch.empty((rows, _abi.packed_bytes_per_row(cols, cfg.bits)), dtype=torch.uint8,
+                        device=dev)
+    luts = torch.empty((rows, 1 << cfg.bits), dtype=torch.float32, device=dev)
+    alphas = torch.empty(ng, dtype=torch.float32, device=dev)
+    betas = torch.empty(ng, dtype=torch.float32, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib().anyq_dev_quantize_any(
+        C.c_void_p(w.data_ptr()), rows, cols, C.byref(cfg),
+        C.c_void_p(exj.data_ptr()) if exj is not None else None, row_offset,
+        C.c_void_p(codes.data_ptr()), C.c_void_p(luts.data_ptr()), C.c_void_p(alphas.data_ptr()),
+        C.c_void_p(betas.data_ptr()), C.c_void_p(s.cuda_stream)))
+    return codes, luts, alphas, betas

@@ -1,0 +1,500 @@
+// C-ABI entry points (include/anyq_b200.h). Host-side orchestration only:
+// argument validation with the reference's error classes, H2D/D2H staging for
+// the host-buffer calls, and kernel launches. All compute is on the device.
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+#include "lutgemm.cuh"
+
+namespace anyq_b200 {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+[[noreturn]] void fail(anyq_status s, const std::string& msg) { throw Failure{s, msg}; }
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+const float kFp4Table[15] = {-6.0f, -4.0f, -3.0f, -2.0f, -1.5f, -1.0f, -0.5f, 0.0f,
+                             0.5f,  1.0f,  1.5f,  2.0f,  3.0f,  4.0f,  6.0f};
+const float kNf4Table[16] = {-1.0f,
+                             -0.6961928009986877f,
+                             -0.5250730514526367f,
+                             -0.39491748809814453f,
+                             -0.28444138169288635f,
+                             -0.18477343022823334f,
+                             -0.09105003625154495f,
+                             0.0f,
+                             0.07958029955625534f,
+                             0.16093020141124725f,
+                             0.24611230194568634f,
+                             0.33791524171829224f,
+                             0.44070982933044434f,
+                             0.5626170039176941f,
+                             0.7229568362236023f,
+                             1.0f};
+
+Table int_grid_table(int bits, bool shifted) {
+  if (bits != 2 && bits != 3 && bits != 4 && bits != 8)
+    fail(ANYQ_ERR_CONFIG, "int_grid: bits must be one of {2,3,4,8}");
+  Table t;
+  int lo = -(1 << (bits - 1)) + (shifted ? 1 : 0);
+  t.n = 1 << bits;
+  for (int q = 0; q < t.n; ++q) t.v[q] = (float)(lo + q);
+  return t;
+}
+
+Table fixed_table(const anyq_config& c) {
+  Table t;
+  switch (c.codebook) {
+    case ANYQ_CB_INT: return int_grid_table(c.bits, c.int_range_shifted != 0);
+    case ANYQ_CB_FP4:
+      t.n = 15;
+      std::memcpy(t.v, kFp4Table, sizeof kFp4Table);
+      return t;
+    case ANYQ_CB_NF4:
+      t.n = 16;
+      std::memcpy(t.v, kNf4Table, sizeof kNf4Table);
+      return t;
+    case ANYQ_CB_ANY: fail(ANYQ_ERR_CONFIG, "AnyN has no fixed codebook");
+  }
+  fail(ANYQ_ERR_CONFIG, "unknown codebook kind");
+}
+
+Table effective_table(Table t, bool symmetric) {
+  if (symmetric) return t;
+  float lo = t.v[0];
+  for (int q = 0; q < t.n; ++q) t.v[q] -= lo;  // host fp32, same as codebooks.cpp:70
+  return t;
+}
+
+void validate_config(const anyq_config& c, int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 1) fail(ANYQ_ERR_SHAPE, "tensor must be at least 1x1");
+  if (c.bits != 2 && c.bits != 3 && c.bits != 4 && c.bits != 8)
+    fail(ANYQ_ERR_CONFIG, "bits must be one of {2,3,4,8}");
+  if ((c.codebook == ANYQ_CB_FP4 || c.codebook == ANYQ_CB_NF4) && c.bits != 4)
+    fail(ANYQ_ERR_CONFIG, "fp4/nf4 require bits == 4");
+  if (c.granularity == ANYQ_G_GROUP && c.group_size < 2)
+    fail(ANYQ_ERR_CONFIG, "group_size must be >= 2");
+  if (c.granularity == ANYQ_G_BLOCK && c.block_size < 1)
+    fail(ANYQ_ERR_CONFIG, "block_size must be >= 1");
+  if (c.max_iters < 1) fail(ANYQ_ERR_CONFIG, "learner.max_iters must be >= 1");
+  if (!(c.rel_tol >= 0)) fail(ANYQ_ERR_CONFIG, "learner.rel_tol must be >= 0");
+  if (c.restarts < 1) fail(ANYQ_ERR_CONFIG, "learner.restarts must be >= 1");
+  if (c.codebook == ANYQ_CB_ANY && c.granularity != ANYQ_G_ROW && c.granularity != ANYQ_G_GROUP)
+    fail(ANYQ_ERR_CONFIG, "learned lookup tables are per-row; use rowwise or groupwise scaling");
+  if (c.init == ANYQ_INIT_NF4 && c.bits != 4)
+    fail(ANYQ_ERR_CONFIG, "nf4 seeding needs a 16-entry table (bits == 4)");
+  if (c.granularity < 0 || c.granularity > 4) fail(ANYQ_ERR_CONFIG, "unknown granularity");
+  if (c.codebook < 0 || c.codebook > 3) fail(ANYQ_ERR_CONFIG, "unknown codebook kind");
+  if (c.codebook == ANYQ_CB_ANY && (c.init < 0 || c.init > 3)) fail(ANYQ_ERR_CONFIG, "unknown init");
+  if (c.codebook == ANYQ_CB_ANY && (c.weighting < 0 || c.weighting > 2))
+    fail(ANYQ_ERR_CONFIG, "unknown weighting mode");
+}
+
+int64_t group_count(const anyq_config& c, int64_t rows, int64_t cols) {
+  switch (c.granularity) {
+    case ANYQ_G_TENSOR: return 1;
+    case ANYQ_G_ROW: return rows;
+    case ANYQ_G_COLUMN: return cols;
+    case ANYQ_G_GROUP: return rows * ((cols + c.group_size - 1) / c.group_size);
+    case ANYQ_G_BLOCK:
+      return ((rows + c.block_size - 1) / c.block_size) * ((cols + c.block_size - 1) / c.block_size);
+  }
+  fail(ANYQ_ERR_CONFIG, "unknown granularity");
+}
+
+void check_device_error(const int* d_err, const char* what) {
+  int h = 0;
+  ANYQ_CUDA(cudaMemcpy(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h != ANYQ_OK) {
+    const char* kind = h == ANYQ_ERR_NONFINITE  ? "non-finite value"
+                       : h == ANYQ_ERR_STATS    ? "negative, non-finite or all-zero weights/stats"
+                       : h == ANYQ_ERR_CODE_RANGE ? "code exceeds its value table"
+                       : h == ANYQ_ERR_IO         ? "value overflows its 16-bit storage format"
+                       : h == ANYQ_ERR_INVARIANT  ? "scale underflows its 16-bit storage format"
+                                                  : "internal invariant violated";
+    fail((anyq_status)h, std::string(what) + ": " + kind);
+  }
+}
+
+static void ensure_device() {
+  static std::once_flag once;
+  static cudaError_t st = cudaSuccess;
+  std::call_once(once, [] {
+    int n = 0;
+    st = cudaGetDeviceCount(&n);
+    if (st == cudaSuccess && n == 0) st = cudaErrorNoDevice;
+  });
+  if (st != cudaSuccess)
+    fail(ANYQ_ERR_CUDA, std::string("no usable CUDA device: ") + cudaGetErrorString(st));
+}
+
+template <typename F>
+static anyq_status guard(F&& f) {
+  try {
+    ensure_device();
+    f();
+    g_last_error.clear();
+    return ANYQ_OK;
+  } catch (const Failure& e) {
+    g_last_error = e.msg;
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ANYQ_ERR_INTERNAL;
+  }
+}
+
+// qmin/qmax of the quantizer (learner.cpp:401, quantize.cpp:12)
+static void table_range(const anyq_config& c, float* qmin, float* qmax) {
+  Table t = c.codebook == ANYQ_CB_ANY ? int_grid_table(c.bits, c.int_range_shifted != 0)
+                                      : fixed_table(c);
+  *qmin = t.v[0];
+  *qmax = t.v[t.n - 1];
+  if (!(*qmax > *qmin)) fail(ANYQ_ERR_CONFIG, "qmax must exceed qmin");
+  if (c.symmetric && !(*qmax > 0)) fail(ANYQ_ERR_CONFIG, "symmetric scaling needs qmax > 0");
+}
+
+// Device-side quantize of rows (shared by the host and device entry points).
+static void quantize_device(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg,
+                            const float* exj, int64_t row_offset, uint8_t* packed, float* luts,
+                            float* alphas, float* betas, cudaStream_t s) {
+  validate_config(cfg, rows, cols);
+  float qmin, qmax;
+  table_range(cfg, &qmin, &qmax);
+  DevBuf<int> err(1);
+  ANYQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+  launch_check_finite(w, rows * cols, err.p, ANYQ_ERR_NONFINITE, s);
+  ANYQ_CUDA(cudaStreamSynchronize(s));
+  check_device_error(err.p, cfg.codebook == ANYQ_CB_ANY ? "quantize_any" : "quantize_fixed");
+  launch_scales(w, rows, cols, cfg, qmin, qmax, alphas, betas, s);
+  DevBuf<float> ws(rows * cols), sw;
+  DevBuf<uint8_t> codes(rows * cols);
+  if (cfg.codebook == ANYQ_CB_ANY) {
+    if (exj) {
+      launch_check_stats(exj, cols, err.p, s);
+      ANYQ_CUDA(cudaStreamSynchronize(s));
+      check_device_error(err.p, "sample weights");
+    }
+    sw.alloc(rows * cols);
+    launch_scale_rows(w, rows, cols, cfg, alphas, betas, exj, ws.p, sw.p, err.p, s);
+    ANYQ_CUDA(cudaStreamSynchronize(s));
+    check_device_error(err.p, "KmProblem");
+    launch_kmeans(ws.p, sw.p, rows, cols, cfg, row_offset, luts, codes.p, err.p, s);
+  } else {
+    launch_scale_rows(w, rows, cols, cfg, alphas, betas, nullptr, ws.p, nullptr, err.p, s);
+    ANYQ_CUDA(cudaStreamSynchronize(s));
+    check_device_error(err.p, "round_to_codebook");
+    Table eff = effective_table(fixed_table(cfg), cfg.symmetric != 0);
+    launch_round(ws.p, rows * cols, eff, codes.p, s);
+  }
+  launch_pack(codes.p, rows, cols, cfg.bits, packed, err.p, s);
+  ANYQ_CUDA(cudaStreamSynchronize(s));
+  check_device_error(err.p, "quantize");
+}
+
+static void fill_header(anyq_qtensor* out, int64_t rows, int64_t cols, const anyq_config& cfg) {
+  out->rows = rows;
+  out->cols = cols;
+  out->cfg = cfg;
+  out->layout = ANYQ_LAYOUT_ROWMAJOR;
+  out->tile_k = 1;
+  out->lut_store = ANYQ_STORE_FP16;
+  out->scale_store = ANYQ_STORE_FP16;
+  out->num_groups = group_count(cfg, rows, cols);
+}
+
+static void check_qt(const anyq_qtensor* qt) {
+  if (!qt) fail(ANYQ_ERR_SHAPE, "null tensor");
+  validate_config(qt->cfg, qt->rows, qt->cols);
+  if (qt->num_groups != group_count(qt->cfg, qt->rows, qt->cols))
+    fail(ANYQ_ERR_SHAPE, "tensor group count does not match its granularity");
+  if (qt->cfg.codebook == ANYQ_CB_ANY && !qt->luts) fail(ANYQ_ERR_SHAPE, "AnyN tensor without LUTs");
+  if (qt->layout == ANYQ_LAYOUT_KTILED && qt->tile_k < 1) fail(ANYQ_ERR_CONFIG, "tile_k must be >= 1");
+}
+
+// Uploads a host tensor; LUT null for fixed formats.
+struct DevTensorArrays {
+  DevBuf<uint8_t> codes;
+  DevBuf<float> luts, alphas, betas;
+  void upload(const anyq_qtensor* qt) {
+    int64_t nb = qt->rows * packed_bpr(qt->cols, qt->cfg.bits);
+    codes.alloc(nb);
+    codes.upload(qt->codes, nb);
+    if (qt->cfg.codebook == ANYQ_CB_ANY) {
+      int64_t nl = qt->rows * (int64_t(1) << qt->cfg.bits);
+      luts.alloc(nl);
+      luts.upload(qt->luts, nl);
+    }
+    alphas.alloc(qt->num_groups);
+    alphas.upload(qt->alphas, qt->num_groups);
+    betas.alloc(qt->num_groups);
+    betas.upload(qt->betas, qt->num_groups);
+  }
+};
+
+}  // namespace anyq_b200
+
+using namespace anyq_b200;
+
+extern "C" {
+
+const char* anyq_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t anyq_launch_count(void) { return g_launches.load(); }
+
+void anyq_config_default(anyq_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->bits = 4;
+  c->codebook = ANYQ_CB_INT;
+  c->granularity = ANYQ_G_GROUP;
+  c->group_size = 128;
+  c->block_size = 1;
+  c->init = ANYQ_INIT_KMPP;
+  c->max_iters = 100;
+  c->rel_tol = 1e-6f;
+  c->restarts = 1;
+  c->weighting = ANYQ_W_FULL;
+}
+
+int64_t anyq_packed_bytes_per_row(int64_t cols, int32_t bits) { return packed_bpr(cols, bits); }
+
+int64_t anyq_num_groups(const anyq_config* cfg, int64_t rows, int64_t cols) {
+  try {
+    return group_count(*cfg, rows, cols);
+  } catch (const Failure&) {
+    return -1;
+  }
+}
+
+int64_t anyq_lut_entries(const anyq_config* cfg) {
+  return cfg->codebook == ANYQ_CB_ANY ? (int64_t(1) << cfg->bits) : 0;
+}
+
+anyq_status anyq_quantize_any(const float* w, int64_t rows, int64_t cols, const anyq_config* cfg,
+                              const float* exj, int64_t row_offset, anyq_qtensor* out) {
+  return guard([&] {
+    if (cfg->codebook != ANYQ_CB_ANY) fail(ANYQ_ERR_CONFIG, "quantize_any requires the learned codebook");
+    validate_config(*cfg, rows, cols);
+    cudaStream_t s = 0;
+    DevBuf<float> dw(rows * cols), dexj;
+    dw.upload(w, rows * cols);
+    if (exj) {
+      dexj.alloc(cols);
+      dexj.upload(exj, cols);
+    }
+    int64_t ng = group_count(*cfg, rows, cols);
+    int64_t nb = rows * packed_bpr(cols, cfg->bits);
+    int64_t nl = rows * (int64_t(1) << cfg->bits);
+    DevBuf<uint8_t> packed(nb);
+    DevBuf<float> luts(nl), alphas(ng), betas(ng);
+    quantize_device(dw.p, rows, cols, *cfg, dexj.p, row_offset, packed.p, luts.p, alphas.p,
+                    betas.p, s);
+    fill_header(out, rows, cols, *cfg);
+    packed.download(out->codes, nb);
+    luts.download(out->luts, nl);
+    alphas.download(out->alphas, ng);
+    betas.download(out->betas, ng);
+  });
+}
+
+anyq_status anyq_quantize_fixed(const float* w, int64_t rows, int64_t cols, const anyq_config* cfg,
+                                anyq_qtensor* out) {
+  return guard([&] {
+    if (cfg->codebook == ANYQ_CB_ANY) fail(ANYQ_ERR_CONFIG, "quantize_fixed handles fixed codebooks only");
+    validate_config(*cfg, rows, cols);
+    cudaStream_t s = 0;
+    DevBuf<float> dw(rows * cols);
+    dw.upload(w, rows * cols);
+    int64_t ng = group_count(*cfg, rows, cols);
+    int64_t nb = rows * packed_bpr(cols, cfg->bits);
+    DevBuf<uint8_t> packed(nb);
+    DevBuf<float> alphas(ng), betas(ng);
+    quantize_device(dw.p, rows, cols, *cfg, nullptr, 0, packed.p, nullptr, alphas.p, betas.p, s);
+    fill_header(out, rows, cols, *cfg);
+    packed.download(out->codes, nb);
+    alphas.download(out->alphas, ng);
+    betas.download(out->betas, ng);
+  });
+}
+
+anyq_status anyq_dev_quantize_any(const float* w_dev, int64_t rows, int64_t cols,
+                                  const anyq_config* cfg, const float* exj_dev, int64_t row_offset,
+                                  uint8_t* codes_dev, float* luts_dev, float* alphas_dev,
+                                  float* betas_dev, void* stream) {
+  return guard([&] {
+    if (cfg->codebook != ANYQ_CB_ANY) fail(ANYQ_ERR_CONFIG, "quantize_any requires the learned codebook");
+    quantize_device(w_dev, rows, cols, *cfg, exj_dev, row_offset, codes_dev, luts_dev, alphas_dev,
+                    betas_dev, (cudaStream_t)stream);
+  });
+}
+
+anyq_status anyq_pack_codes(const uint8_t* codes, int64_t rows, int64_t cols, int32_t bits,
+                            uint8_t* packed) {
+  return guard([&] {
+    if (bits != 2 && bits != 3 && bits != 4 && bits != 8)
+      fail(ANYQ_ERR_CONFIG, "pack_codes: bits must be one of {2,3,4,8}");
+    int64_t nb = rows * packed_bpr(cols, bits);
+    DevBuf<uint8_t> dc(rows * cols), dp(nb);
+    DevBuf<int> err(1);
+    err.zero();
+    dc.upload(codes, rows * cols);
+    if (rows * cols > 0) launch_pack(dc.p, rows, cols, bits, dp.p, err.p, 0);
+    check_device_error(err.p, "pack_codes");
+    dp.download(packed, nb);
+  });
+}
+
+anyq_status anyq_unpack_codes(const uint8_t* packed, int64_t rows, int64_t cols, int32_t bits,
+                              uint8_t* codes) {
+  return guard([&] {
+    if (bits != 2 && bits != 3 && bits != 4 && bits != 8)
+      fail(ANYQ_ERR_CONFIG, "unpack_codes: bits must be one of {2,3,4,8}");
+    int64_t nb = rows * packed_bpr(cols, bits);
+    DevBuf<uint8_t> dp(nb), dc(rows * cols);
+    dp.upload(packed, nb);
+    if (rows * cols > 0) launch_unpack(dp.p, rows, cols, bits, dc.p, 0);
+    dc.download(codes, rows * cols);
+  });
+}
+
+anyq_status anyq_ktile_codes(const uint8_t* packed, int64_t rows, int64_t cols, int32_t bits,
+                             int32_t tile_k, int32_t inverse, uint8_t* out) {
+  return guard([&] {
+    if (tile_k < 1) fail(ANYQ_ERR_CONFIG, "tile_k must be >= 1");
+    int64_t nb = rows * packed_bpr(cols, bits);
+    DevBuf<uint8_t> dp(nb), c0(rows * cols), c1(rows * cols), dq(nb);
+    DevBuf<int> err(1);
+    err.zero();
+    dp.upload(packed, nb);
+    launch_unpack(dp.p, rows, cols, bits, c0.p, 0);
+    launch_ktile(c0.p, rows, cols, tile_k, inverse, c1.p, 0);
+    launch_pack(c1.p, rows, cols, bits, dq.p, err.p, 0);
+    check_device_error(err.p, "ktile");
+    dq.download(out, nb);
+  });
+}
+
+anyq_status anyq_narrow_inplace(anyq_qtensor* qt) {
+  return guard([&] {
+    check_qt(qt);
+    DevBuf<int> err(1);
+    err.zero();
+    DevBuf<float> l, a(qt->num_groups), b(qt->num_groups);
+    int64_t nl = 0;
+    if (qt->cfg.codebook == ANYQ_CB_ANY) {
+      nl = qt->rows * (int64_t(1) << qt->cfg.bits);
+      l.alloc(nl);
+      l.upload(qt->luts, nl);
+      launch_narrow(l.p, nl, qt->lut_store, 0, err.p, 0);
+    }
+    a.upload(qt->alphas, qt->num_groups);
+    b.upload(qt->betas, qt->num_groups);
+    // reference order: alpha then beta per group; errors: overflow/non-finite (IoError /
+    // NonFiniteError) dominate the alpha-underflow invariant.
+    launch_narrow(a.p, qt->num_groups, qt->scale_store, 1, err.p, 0);
+    launch_narrow(b.p, qt->num_groups, qt->scale_store, 0, err.p, 0);
+    check_device_error(err.p, "narrowed");
+    if (nl) l.download(qt->luts, nl);
+    a.download(qt->alphas, qt->num_groups);
+    b.download(qt->betas, qt->num_groups);
+  });
+}
+
+anyq_status anyq_dequantize(const anyq_qtensor* qt, float* w_out) {
+  return guard([&] {
+    check_qt(qt);
+    DevTensorArrays t;
+    t.upload(qt);
+    Table fixed{};
+    if (qt->cfg.codebook != ANYQ_CB_ANY)
+      fixed = effective_table(fixed_table(qt->cfg), qt->cfg.symmetric != 0);
+    DevBuf<float> w(qt->rows * qt->cols);
+    DevBuf<int> err(1);
+    err.zero();
+    launch_dequant(t.codes.p, qt->rows, qt->cols, qt->cfg.bits, qt->layout == ANYQ_LAYOUT_KTILED,
+                   qt->tile_k, t.luts.p, fixed, qt->cfg, t.alphas.p, t.betas.p, w.p, err.p, 0);
+    check_device_error(err.p, "dequantize");
+    w.download(w_out, qt->rows * qt->cols);
+  });
+}
+
+anyq_status anyq_gemm_fused(const float* x, int64_t m, const anyq_qtensor* qt, int32_t plan_layout,
+                            int32_t plan_tile_k, float* y) {
+  return guard([&] {
+    check_qt(qt);
+    if (plan_layout != qt->layout || (qt->layout == ANYQ_LAYOUT_KTILED && plan_tile_k != qt->tile_k))
+      fail(ANYQ_ERR_CONFIG, "gemm_fused: plan layout does not match tensor layout");
+    if (m < 0) fail(ANYQ_ERR_SHAPE, "gemm_fused: negative m");
+    if (m == 0) return;
+    DevTensorArrays t;
+    t.upload(qt);
+    Table fixed{};
+    if (qt->cfg.codebook != ANYQ_CB_ANY)
+      fixed = effective_table(fixed_table(qt->cfg), qt->cfg.symmetric != 0);
+    DevBuf<float> dx(m * qt->cols), dy(m * qt->rows);
+    dx.upload(x, m * qt->cols);
+    DevBuf<int> err(1);
+    err.zero();
+    launch_gemm_exact(dx.p, m, qt->cols, t.codes.p, qt->rows, qt->cfg.bits,
+                      qt->layout == ANYQ_LAYOUT_KTILED, qt->tile_k, t.luts.p, fixed, qt->cfg,
+                      t.alphas.p, t.betas.p, dy.p, err.p, 0);
+    check_device_error(err.p, "gemm_fused");
+    dy.download(y, m * qt->rows);
+  });
+}
+
+anyq_status anyq_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int64_t k,
+                            float* y) {
+  return guard([&] {
+    if (m <= 0 || n <= 0) return;
+    DevBuf<float> dx(m * k), dw(n * k), dy(m * n);
+    dx.upload(x, m * k);
+    dw.upload(w, n * k);
+    launch_gemm_dense(dx.p, m, dw.p, n, k, dy.p, 0);
+    ANYQ_CUDA(cudaDeviceSynchronize());
+    dy.download(y, m * n);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// device-resident tensors + tensor-core GEMM (lutgemm.cu)
+// ---------------------------------------------------------------------------
+anyq_status anyq_dev_tensor_create(const anyq_qtensor* qt, anyq_dev_tensor** out) {
+  return guard([&] {
+    check_qt(qt);
+    *out = reinterpret_cast<anyq_dev_tensor*>(lutgemm_create(qt));
+  });
+}
+
+void anyq_dev_tensor_destroy(anyq_dev_tensor* t) {
+  lutgemm_destroy(reinterpret_cast<LutTensor*>(t));
+}
+
+int64_t anyq_dev_tensor_weight_bytes(const anyq_dev_tensor* t) {
+  return reinterpret_cast<const LutTensor*>(t)->weight_bytes;
+}
+int64_t anyq_dev_tensor_rows(const anyq_dev_tensor* t) {
+  return reinterpret_cast<const LutTensor*>(t)->rows;
+}
+int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t) {
+  return reinterpret_cast<const LutTensor*>(t)->cols;
+}
+
+anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
+                               void* y_bf16, float* y_f32, void* stream) {
+  return guard([&] {
+    lutgemm_run(reinterpret_cast<const LutTensor*>(t), x_bf16, m, y_bf16, y_f32,
+                (cudaStream_t)stream);
+  });
+}
+
+// Debug hook (not part of the reference interface): record a per-CTA
+// globaltimer timeline of the tensor-core GEMM into dev ([ncta][16] int64).
+void anyq_debug_set_trace(long long* dev) { lutgemm_set_trace(dev); }
+
+}  // extern "C"

@@ -1,0 +1,43 @@
+// Launcher declarations shared by the C-ABI layer (capi.cu) and the kernels.
+#pragma once
+
+#include <float.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace anyq_b200 {
+
+void launch_check_finite(const float* p, int64_t n, int* err, int status, cudaStream_t s);
+void launch_check_stats(const float* p, int64_t n, int* err, cudaStream_t s);
+void launch_scales(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg, float qmin,
+                   float qmax, float* alphas, float* betas, cudaStream_t s);
+void launch_scale_rows(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg,
+                       const float* alphas, const float* betas, const float* exj, float* ws,
+                       float* sw, int* err, cudaStream_t s);
+void launch_round(const float* ws, int64_t n, const Table& t, uint8_t* codes, cudaStream_t s);
+void launch_pack(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
+                 int* err, cudaStream_t s);
+void launch_unpack(const uint8_t* packed, int64_t rows, int64_t cols, int bits, uint8_t* codes,
+                   cudaStream_t s);
+void launch_ktile(const uint8_t* in, int64_t rows, int64_t cols, int64_t tile_k, int inverse,
+                  uint8_t* out, cudaStream_t s);
+void launch_narrow(float* v, int64_t n, int store, int is_alpha, int* err, cudaStream_t s);
+void launch_dequant(const uint8_t* packed, int64_t rows, int64_t cols, int bits, int ktiled,
+                    int64_t tile_k, const float* luts, const Table& fixed, const anyq_config& cfg,
+                    const float* alphas, const float* betas, float* w, int* err, cudaStream_t s);
+void launch_gemm_exact(const float* x, int64_t m, int64_t k, const uint8_t* packed, int64_t n,
+                       int bits, int ktiled, int64_t tile_k, const float* luts, const Table& fixed,
+                       const anyq_config& cfg, const float* alphas, const float* betas, float* y,
+                       int* err, cudaStream_t s);
+void launch_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int64_t k, float* y,
+                       cudaStream_t s);
+
+// k-means learner (kmeans.cu): ws/sw are rows x cols on device; writes the
+// row LUTs (rows x 2^bits fp32) and logical codes (rows x cols uint8).
+void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
+                   const anyq_config& cfg, int64_t row_offset, float* luts, uint8_t* codes,
+                   int* err, cudaStream_t s);
+
+}  // namespace anyq_b200

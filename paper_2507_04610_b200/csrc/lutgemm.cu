@@ -1,0 +1,890 @@
+// Tensor-core any4 LUT GEMM for small M (1..16), sm_100a.
+//
+//   y[m][n] = sum_g alpha[n][g] * sum_{k in g} x[m][k] * T_n[c[n][k]]
+//           + sum_g beta[n][g]  * sum_{k in g} x[m][k]
+// which equals x * (alpha*T[c] + beta)^T (qgemm.cpp:98-111) with the group
+// scale factored out of the inner reduction.
+//
+// Design (one persistent CTA per SM, 10 warps):
+//  * 8 "dequant" warps = 2 teams x 4 quarters. Lane L of every dequant warp
+//    owns row L of the current 32-row block, so each lane looks up only its
+//    own row's pair table: T2[byte] = half2(T[lo nibble], T[hi nibble]), 256
+//    entries laid out lane-interleaved in shared memory (entry e of row L at
+//    e*256 + L*4) -> bank L for every lookup, conflict free, and the address
+//    is ONE prmt (code byte into bits 8..15, lane offset in bits 0..7).
+//    One LDS therefore dequantises two weights (exact fp16 LUT values).
+//  * The dequantised fp16 values go straight to TMEM with tcgen05.st (quarter
+//    q = warp%4 owns TMEM lanes 32q..32q+31), never through shared memory.
+//    Quarter q holds k-slice [16q, 16q+16) of every 64-k MMA step, so one
+//    tcgen05.mma (M=128, N=4*MP, K=16, A from TMEM, B from smem) computes all
+//    four k-slices at once against a block-diagonal B (x of slice q' in
+//    columns q'*MP..q'*MP+MP-1); the q==q' diagonal blocks are the products.
+//  * Per scale group a fresh accumulator (4 TMEM slots); the owning team
+//    drains it one chunk later (tcgen05.ld), applies alpha (and beta * sum x)
+//    in fp32 registers. x enters as fp16 scaled by 2^e per (group, row of x):
+//    bf16 -> fp16 is then exact, so products are exact and accumulation is
+//    fp32 — results match the fp32 reference to accumulation-order rounding.
+//  * A producer warp streams 128-k code chunks (2 KB per 32 rows) and the x
+//    images with cp.async.bulk into a 4-stage mbarrier ring; one thread of
+//    the MMA warp issues tcgen05.mma and tcgen05.commit.
+//  * Work = (row block, chunk) units split contiguously over the CTAs
+//    (stream-K); row blocks shared by several CTAs are combined in a fixed
+//    order by the last-arriving CTA (deterministic, self-resetting counters).
+#include <cuda_bf16.h>
+
+#include "kernels.cuh"
+#include "lutgemm.cuh"
+
+namespace anyq_b200 {
+
+namespace {
+
+constexpr int kTeams = 4;
+constexpr int kDqWarps = 4 * kTeams;  // warps 0..15: 4 teams x 4 quarters
+constexpr int kProducerWarp = kDqWarps;
+constexpr int kMmaWarp = kDqWarps + 1;
+constexpr int kEpiWarp0 = kDqWarps + 2;  // one epilogue warp per TMEM lane quarter
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kDqWarps + 6) * 32;
+constexpr int kASlots = 2;        // A operand slots (one stage each) in TMEM
+constexpr int kAccSlots = 2;      // accumulator slots (one stage each) in TMEM
+constexpr int kTblBytes = 65536;
+constexpr int kChunkBytes = 2048;  // 32 rows x 128 k x 4 bit
+constexpr int kMaxMP = 16;
+
+// All hand-offs between roles are per STAGE (CPS chunks of 128 k), so the
+// fixed cost of an mbarrier round trip / tcgen05 fence is paid once per
+// CPS*4096 weights instead of once per 4096.
+template <int MP>
+struct Cfg {
+  static constexpr int NB = 4 * MP;                  // MMA N
+  static constexpr int CPS = MP <= 4 ? 8 : (MP <= 8 ? 4 : 2);  // chunks per stage
+  static constexpr int kStepImg = NB * 32;           // one 64-k x image (16 k x NB fp16)
+  static constexpr int kStageCodes = CPS * kChunkBytes;
+  static constexpr int kStageX = 2 * CPS * kStepImg;
+  static constexpr int kStageBytes = kStageCodes + kStageX;
+  static constexpr int kStages = MP <= 4 ? 5 : (MP <= 8 ? 8 : 10);
+  static constexpr int kRingOff = kTblBytes;
+  static constexpr int kAbStage = CPS * 128;
+  static constexpr int kAbRingOff = kRingOff + kStages * kStageBytes;
+  static constexpr int kRedOff = kAbRingOff + kStages * kAbStage;
+  static constexpr int kRedBytes = kEpiWarps * MP * 32 * 4;
+  static constexpr int kBarOff = kRedOff + kRedBytes;
+  static constexpr int kNumBars = 4 * kStages + 2 * kASlots + 2 * kAccSlots;
+  static constexpr int kXOff = kBarOff + ((kNumBars * 8 + 16 + 127) / 128) * 128;
+  static constexpr int kSmem = kXOff;  // + xinv/xsum staging (size set at launch)
+  static constexpr int kASlotCols = CPS * 16;
+  static constexpr int kAccSlotCols = CPS * NB;
+  static constexpr int kAccCol0 = kASlots * kASlotCols;
+  static constexpr int kUsedCols = kAccCol0 + kAccSlots * kAccSlotCols;
+  static constexpr int kTmemCols = kUsedCols <= 128 ? 128 : kUsedCols <= 256 ? 256 : 512;
+  static_assert(kUsedCols <= 512, "TMEM budget");
+  // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, M=128.
+  static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(NB >> 3) << 17) | ((128u >> 4) << 24);
+};
+
+struct Params {
+  const uint8_t* codes;
+  const __half* lut;
+  const __half2* ab;
+  const __half* ximg;
+  const float* xinv;
+  const float* xsum;
+  float* part;
+  int* counters;
+  __nv_bfloat16* y;
+  float* y32;
+  int64_t N, U;
+  int M, RB, C, GC, GR, cmax, ncta;
+  long long* trace;  // debug: [ncta][16] globaltimer stamps, or null
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, "
+      "p; }" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+template <int MP>
+__device__ __forceinline__ void tc_ld_nowait(uint32_t taddr, float (&r)[MP]) {
+  uint32_t u[MP];
+  if constexpr (MP == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                 : "r"(taddr)
+                 : "memory");
+  } else if constexpr (MP == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),
+                   "=r"(u[6]), "=r"(u[7])
+                 : "r"(taddr)
+                 : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+          "=r"(u[14]), "=r"(u[15])
+        : "r"(taddr)
+        : "memory");
+  }
+#pragma unroll
+  for (int i = 0; i < MP; ++i) r[i] = __uint_as_float(u[i]);
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// per-chunk trace of CTA 0: [event][chunk] at P.trace + 148*16
+#define TRACEC(ev, i)                                                                  \
+  do {                                                                                 \
+    if (P.trace && blockIdx.x == 0 && (i) < 256) P.trace[148 * 16 + (ev) * 256 + (i)] = gtimer(); \
+  } while (0)
+#define TRACE(slot)                                                   \
+  do {                                                                \
+    if (P.trace) P.trace[blockIdx.x * 16 + (slot)] = gtimer();        \
+  } while (0)
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// UMMA shared-memory descriptor, no swizzle, K-major: core matrices of 8 rows
+// x 16 B; LBO = 128 B between the two k-halves, SBO = 256 B between 8-row
+// groups; version 1 (Blackwell).
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+
+// ---------------------------------------------------------------------------
+// Work schedule shared by every role (stream-K over (row block, chunk)).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int cta_of(int64_t u, int64_t U, int ncta) {
+  return (int)(((u + 1) * ncta + U - 1) / U) - 1;
+}
+
+// ---------------------------------------------------------------------------
+// x preparation: fp16 images (block-diagonal B per 64-k step), 2^-e per
+// (group, m), and per-chunk sums of x.
+// ---------------------------------------------------------------------------
+template <int MP>
+__global__ void __launch_bounds__(128) k_xprep(const __nv_bfloat16* __restrict__ x, int M, int64_t K,
+                                               __half* __restrict__ ximg, float* __restrict__ xinv,
+                                               float* __restrict__ xsum) {
+  // one block per 128-k chunk; warp w handles rows m = w, w+4, ...; lane owns
+  // k = 128c + 4*lane + [0,4). Scale 2^e per (chunk, m) puts max|x| in
+  // [2^14, 2^15): bf16 -> fp16 is then exact (8 significant bits).
+  constexpr int NB = 4 * MP;
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k0 = (int64_t)c * 128 + lane * 4;
+  const int64_t s = 2 * c + (lane >> 4);
+  const int kk = (lane & 3) * 4, qq = (lane & 15) >> 2;
+  for (int m = warp; m < MP; m += 4) {
+    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (m < M) {
+      const __nv_bfloat16* xr = x + (int64_t)m * K;
+      if (k0 + 3 < K && (K & 3) == 0) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(xr + k0);
+        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+        const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+        v[0] = __low2float(a);
+        v[1] = __high2float(a);
+        v[2] = __low2float(b);
+        v[3] = __high2float(b);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (k0 + t < K) v[t] = __bfloat162float(xr[k0 + t]);
+      }
+    }
+    float amax = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+    float sum = (v[0] + v[1]) + (v[2] + v[3]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+      sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    }
+    const int e = (amax > 0.0f && isfinite(amax)) ? 14 - ilogbf(amax) : 0;
+    const int n = qq * MP + m;
+    __half2 h01 = __halves2half2(__float2half_rn(ldexpf(v[0], e)), __float2half_rn(ldexpf(v[1], e)));
+    __half2 h23 = __halves2half2(__float2half_rn(ldexpf(v[2], e)), __float2half_rn(ldexpf(v[3], e)));
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&h01);
+    packed.y = *reinterpret_cast<uint32_t*>(&h23);
+    *reinterpret_cast<uint2*>(ximg + s * (NB * 16) + (n >> 3) * 128 + (kk >> 3) * 64 + (n & 7) * 8 +
+                              (kk & 7)) = packed;
+    if (lane == 0) {
+      xinv[c * kMaxMP + m] = ldexpf(1.0f, -e);
+      xsum[c * kMaxMP + m] = sum;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// main kernel
+// ---------------------------------------------------------------------------
+template <int MP>
+__global__ void __launch_bounds__(kThreads, 1) k_lutgemm(Params P) {
+  using CF = Cfg<MP>;
+  constexpr int CPS = CF::CPS;
+  constexpr int kStages = CF::kStages;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::kBarOff);
+  const uint32_t bar_full = smem_u32(bars + 0);               // codes + x of a stage landed
+  const uint32_t bar_empty = smem_u32(bars + kStages);        // stage smem free (MMA done)
+  const uint32_t bar_abfull = smem_u32(bars + 2 * kStages);   // alpha/beta of a stage landed
+  const uint32_t bar_abempty = smem_u32(bars + 3 * kStages);  // alpha/beta consumed
+  const uint32_t bar_afull = smem_u32(bars + 4 * kStages);    // A (TMEM) written by dequant
+  const uint32_t bar_aempty = smem_u32(bars + 4 * kStages + kASlots);
+  const uint32_t bar_accfull = smem_u32(bars + 4 * kStages + 2 * kASlots);
+  const uint32_t bar_accempty = smem_u32(bars + 4 * kStages + 2 * kASlots + kAccSlots);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CF::kBarOff + 8 * CF::kNumBars);
+
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) TRACE(0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(bar_full + 8 * i, 1);
+      mbar_init(bar_empty + 8 * i, 1);
+      mbar_init(bar_abfull + 8 * i, 1);
+      mbar_init(bar_abempty + 8 * i, kEpiWarps * 32);
+    }
+    for (int i = 0; i < kASlots; ++i) {
+      mbar_init(bar_afull + 8 * i, kDqWarps * 32);
+      mbar_init(bar_aempty + 8 * i, 1);
+    }
+    for (int i = 0; i < kAccSlots; ++i) {
+      mbar_init(bar_accfull + 8 * i, 1);
+      mbar_init(bar_accempty + 8 * i, kEpiWarps * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
+
+  // This CTA's contiguous range of (row block, chunk) units, walked as
+  // stages of <= CPS chunks that never cross a row block. 32-bit cursors.
+  const int C = P.C;
+  const int u0 = (int)((int64_t)blockIdx.x * P.U / P.ncta);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * P.U / P.ncta);
+  const int nunits = u1 - u0;
+  const int rb0 = u0 / C, c00 = u0 % C;
+
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ producer
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int rb = rb0, c = c00, left = nunits;
+    for (int si = 0; left > 0; ++si) {
+      const int nc = min(min(left, C - c), CPS);
+      const int st = si % kStages;
+      const uint32_t ph = (uint32_t)((si / kStages) & 1);
+      mbar_wait(bar_empty + 8 * st, ph ^ 1);
+      const uint32_t codes_b = nc * kChunkBytes, x_b = 2 * nc * CF::kStepImg;
+      const uint32_t dst = sbase + CF::kRingOff + st * CF::kStageBytes;
+      const int g0 = c / P.GC, g1 = (c + nc - 1) / P.GC;
+      if (elect_one()) {
+        mbar_expect_tx(bar_full + 8 * st, codes_b + x_b);
+        bulk_g2s(dst, P.codes + ((int64_t)rb * C + c) * kChunkBytes, codes_b, bar_full + 8 * st);
+        bulk_g2s(dst + CF::kStageCodes,
+                 reinterpret_cast<const uint8_t*>(P.ximg) + (size_t)2 * c * CF::kStepImg, x_b,
+                 bar_full + 8 * st);
+      }
+      __syncwarp();
+      mbar_wait(bar_abempty + 8 * st, ph ^ 1);
+      if (elect_one()) {
+        mbar_expect_tx(bar_abfull + 8 * st, (g1 - g0 + 1) * 128);
+        bulk_g2s(sbase + CF::kAbRingOff + st * CF::kAbStage, P.ab + ((int64_t)rb * P.GR + g0) * 32,
+                 (g1 - g0 + 1) * 128, bar_abfull + 8 * st);
+      }
+      __syncwarp();
+      if (si == 0 && lane == 0) TRACE(2);
+      left -= nc;
+      c += nc;
+      if (c == C) {
+        c = 0;
+        ++rb;
+      }
+    }
+    if (lane == 0) TRACE(3);
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issue
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int c = c00, left = nunits;
+    const uint64_t desc_hi = (uint64_t)bdesc(0) & ~0x3FFFull;
+    for (int si = 0; left > 0; ++si) {
+      const int nc = min(min(left, C - c), CPS);
+      const int st = si % kStages;
+      const int as = si & (kASlots - 1), cs = si & (kAccSlots - 1);
+      mbar_wait(bar_full + 8 * st, (uint32_t)((si / kStages) & 1));
+      if (lane == 0) TRACEC(0, si);
+      mbar_wait(bar_afull + 8 * as, (uint32_t)((si / kASlots) & 1));
+      if (lane == 0) TRACEC(1, si);
+      mbar_wait(bar_accempty + 8 * cs, (uint32_t)(((si / kAccSlots) & 1) ^ 1));
+      if (lane == 0) TRACEC(2, si);
+      tc_fence_after();
+      if (si == 0 && lane == 0) TRACE(4);
+      if (elect_one()) {
+        const uint32_t xaddr = (sbase + CF::kRingOff + st * CF::kStageBytes + CF::kStageCodes) >> 4;
+        const uint32_t a0 = tmem + (uint32_t)as * CF::kASlotCols;
+        const uint32_t d0 = tmem + CF::kAccCol0 + (uint32_t)cs * CF::kAccSlotCols;
+#pragma unroll 1
+        for (int ci = 0; ci < nc; ++ci) {
+          const uint32_t xa = xaddr + (uint32_t)(2 * ci) * (CF::kStepImg / 16);
+          tc_mma_ts(d0 + ci * CF::NB, a0 + ci * 16, desc_hi | (xa & 0x3FFF), CF::kIdesc, 0u);
+          tc_mma_ts(d0 + ci * CF::NB, a0 + ci * 16 + 8,
+                    desc_hi | ((xa + CF::kStepImg / 16) & 0x3FFF), CF::kIdesc, 1u);
+        }
+        tc_commit(bar_aempty + 8 * as);
+        tc_commit(bar_accfull + 8 * cs);
+        tc_commit(bar_empty + 8 * st);
+      }
+      __syncwarp();
+      if (lane == 0) TRACEC(3, si);
+      left -= nc;
+      c += nc;
+      if (c == C) c = 0;
+    }
+    if (lane == 0) TRACE(5);
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ epilogue
+    // Per stage: drain the CPS chunk accumulators (quarter q = warp%4 owns
+    // TMEM lanes 32q..32q+31 = row `lane`, k-slice q), apply alpha * 2^-e
+    // and beta * sum(x); at the end of a row block reduce the four quarters
+    // and write / combine the outputs.
+    const int q = warp & 3;
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+    float* red = reinterpret_cast<float*>(smem + CF::kRedOff);
+    float yacc[MP];
+#pragma unroll
+    for (int m = 0; m < MP; ++m) yacc[m] = 0.0f;
+    float* sxinv = reinterpret_cast<float*>(smem + CF::kXOff);
+    float* sxsum = sxinv + C * MP;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int e = threadIdx.x - kEpiWarp0 * 32; e < C * MP; e += kEpiWarps * 32) {
+      const int cc = e / MP, m = e % MP;
+      sxinv[e] = P.xinv[cc * kMaxMP + m];
+      sxsum[e] = P.xsum[cc * kMaxMP + m];
+    }
+    named_bar(2, kEpiWarps * 32);
+    if (threadIdx.x == kEpiWarp0 * 32) TRACE(6);
+    int rb = rb0, c = c00, left = nunits;
+    for (int si = 0; left > 0; ++si) {
+      const int nc = min(min(left, C - c), CPS);
+      const int st = si % kStages;
+      const int cs = si & (kAccSlots - 1);
+      const int g0 = c / P.GC;
+      mbar_wait(bar_abfull + 8 * st, (uint32_t)((si / kStages) & 1));
+      mbar_wait(bar_accfull + 8 * cs, (uint32_t)((si / kAccSlots) & 1));
+      if (threadIdx.x == kEpiWarp0 * 32) TRACEC(4, si);
+      tc_fence_after();
+      float r[CPS][MP];
+      const uint32_t tacc = tq + CF::kAccCol0 + (uint32_t)cs * CF::kAccSlotCols + q * MP;
+#pragma unroll
+      for (int ci = 0; ci < CPS; ++ci)
+        if (ci < nc) tc_ld_nowait<MP>(tacc + ci * CF::NB, r[ci]);
+      tc_wait_ld();
+      // pin every loaded register after the wait (volatile asms keep order)
+#pragma unroll
+      for (int ci = 0; ci < CPS; ++ci)
+#pragma unroll
+        for (int m = 0; m < MP; ++m) asm volatile("" : "+f"(r[ci][m]));
+      tc_fence_before();
+      mbar_arrive(bar_accempty + 8 * cs);
+      float2 ab[CPS];
+#pragma unroll
+      for (int ci = 0; ci < CPS; ++ci)
+        ab[ci] = __half22float2(*reinterpret_cast<const __half2*>(
+            smem + CF::kAbRingOff + st * CF::kAbStage + ((c + ci) / P.GC - g0) * 128 + lane * 4));
+      mbar_arrive(bar_abempty + 8 * st);
+      if (threadIdx.x == kEpiWarp0 * 32) TRACEC(5, si);
+      if (si == 0 && threadIdx.x == kEpiWarp0 * 32) TRACE(7);
+#pragma unroll
+      for (int ci = 0; ci < CPS; ++ci) {
+        if (ci < nc) {
+#pragma unroll
+          for (int m = 0; m < MP; ++m) {
+            float v = ab[ci].x * (r[ci][m] * sxinv[(c + ci) * MP + m]);
+            if (q == 0) v = fmaf(ab[ci].y, sxsum[(c + ci) * MP + m], v);
+            yacc[m] += v;
+          }
+        }
+      }
+      left -= nc;
+      c += nc;
+      if (c == C || left == 0) {
+        // ---- end of this CTA's share of row block rb
+#pragma unroll
+        for (int m = 0; m < MP; ++m) {
+          red[(q * MP + m) * 32 + lane] = yacc[m];
+          yacc[m] = 0.0f;
+        }
+        named_bar(2, kEpiWarps * 32);
+        if (q == 0) {
+          const int64_t n = (int64_t)rb * 32 + lane;
+          float sacc[MP];
+#pragma unroll
+          for (int m = 0; m < MP; ++m)
+            sacc[m] = ((red[(0 * MP + m) * 32 + lane] + red[(1 * MP + m) * 32 + lane]) +
+                       red[(2 * MP + m) * 32 + lane]) +
+                      red[(3 * MP + m) * 32 + lane];
+          const int first = cta_of((int64_t)rb * C, P.U, P.ncta);
+          const int last = cta_of((int64_t)(rb + 1) * C - 1, P.U, P.ncta);
+          bool write = true;
+          if (lane == 0 && (c == C)) TRACE(13);
+          if (last > first) {
+            const int pslot = (int)blockIdx.x - first;
+            float* pp = P.part + ((int64_t)rb * P.cmax + pslot) * kMaxMP * 32;
+#pragma unroll
+            for (int m = 0; m < MP; ++m) pp[m * 32 + lane] = sacc[m];
+            __threadfence();
+            __syncwarp();
+            int old = 0;
+            if (lane == 0) old = atomicAdd(&P.counters[rb], 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (lane == 0 && (c == C)) TRACE(14);
+            write = old == last - first;
+            if (write) {
+              __threadfence();
+#pragma unroll
+              for (int m = 0; m < MP; ++m) {
+                float t = 0.0f;
+                for (int sl = 0; sl <= last - first; ++sl)
+                  t += __ldcg(P.part + ((int64_t)rb * P.cmax + sl) * kMaxMP * 32 + m * 32 + lane);
+                sacc[m] = t;
+              }
+              if (lane == 0) P.counters[rb] = 0;
+            }
+          }
+          if (lane == 0 && (c == C)) TRACE(15);
+          if (write && n < P.N) {
+#pragma unroll
+            for (int m = 0; m < MP; ++m) {
+              if (m < P.M) {
+                P.y[(int64_t)m * P.N + n] = __float2bfloat16_rn(sacc[m]);
+                if (P.y32) P.y32[(int64_t)m * P.N + n] = sacc[m];
+              }
+            }
+          }
+        }
+        named_bar(2, kEpiWarps * 32);
+        if (threadIdx.x == kEpiWarp0 * 32) TRACE(8 + (c == C ? 0 : 1));
+        if (c == C) {
+          c = 0;
+          ++rb;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ dequant
+    // Lane L of every dequant warp owns row L of the current row block; team
+    // t = warp/4 handles the stage's chunks ci with ci%2 == t; quarter
+    // q = warp%4 owns k-slice [16q, 16q+16) of each 64-k step.
+    const int q = warp & 3, team = warp >> 2;
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+    const uint32_t laneoff = (uint32_t)lane * 4u;
+    int rb = rb0, c = c00, left = nunits, cur_rb = -1;
+    auto lookup16 = [&](const uint4 w4, uint32_t (&v)[16]) {
+      const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const uint32_t addr = __byte_perm(wd[b >> 2], laneoff, 0x7604u | ((uint32_t)(b & 3) << 4));
+        v[b] = *reinterpret_cast<const uint32_t*>(smem + addr);
+      }
+    };
+    for (int si = 0; left > 0; ++si) {
+      const int nc = min(min(left, C - c), CPS);
+      if (rb != cur_rb) {
+        named_bar(1, kDqWarps * 32);
+        // pair table for row `lane` of block rb: warp w builds the 16 entries
+        // with high nibble w (entry e = 16*hi + lo -> (T[lo], T[hi]))
+        static_assert(kDqWarps == 16, "one high nibble per dequant warp");
+        const uint4* lp = reinterpret_cast<const uint4*>(P.lut + ((int64_t)rb * 32 + lane) * 16);
+        const uint4 l0 = __ldg(lp), l1 = __ldg(lp + 1);
+        const uint32_t t[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        uint32_t th = t[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) th = ((warp >> 1) == w) ? t[w] : th;
+        const uint32_t hsel = (warp & 1) ? 0x76u : 0x54u;
+#pragma unroll
+        for (int lo = 0; lo < 16; ++lo) {
+          const uint32_t sel = ((lo & 1) ? 0x32u : 0x10u) | (hsel << 8);
+          const uint32_t entry = __byte_perm(t[lo >> 1], th, sel);
+          *reinterpret_cast<uint32_t*>(smem + (16 * warp + lo) * 256 + laneoff) = entry;
+        }
+        named_bar(1, kDqWarps * 32);
+        if (cur_rb < 0 && threadIdx.x == 0) TRACE(10);
+        cur_rb = rb;
+      }
+      const int st = si % kStages;
+      const int as = si & (kASlots - 1);
+      mbar_wait(bar_full + 8 * st, (uint32_t)((si / kStages) & 1));
+      if (threadIdx.x == 0) TRACEC(6, si);
+      mbar_wait(bar_aempty + 8 * as, (uint32_t)(((si / kASlots) & 1) ^ 1));
+      if (threadIdx.x == 0) TRACEC(7, si);
+      tc_fence_after();
+      const uint8_t* cs = smem + CF::kRingOff + st * CF::kStageBytes + q * 512 + lane * 16;
+      const uint32_t ta = tq + (uint32_t)as * CF::kASlotCols;
+      // chunks ci = team, team+4, ...; two at a time so 32 lookups are in flight
+#pragma unroll 1
+      for (int ci = team; ci < nc; ci += 2 * kTeams) {
+        const int cj = ci + kTeams;
+        const uint4 wa = *reinterpret_cast<const uint4*>(cs + ci * kChunkBytes);
+        uint4 wb = make_uint4(0, 0, 0, 0);
+        if (cj < nc) wb = *reinterpret_cast<const uint4*>(cs + cj * kChunkBytes);
+        uint32_t va[16], vb[16];
+        lookup16(wa, va);
+        if (cj < nc) lookup16(wb, vb);
+        tc_st16(ta + ci * 16, va);
+        if (cj < nc) tc_st16(ta + cj * 16, vb);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_afull + 8 * as);
+      if (threadIdx.x == 0) TRACEC(8, si);
+      left -= nc;
+      c += nc;
+      if (c == C) {
+        c = 0;
+        ++rb;
+      }
+    }
+    if (threadIdx.x == 0) TRACE(11);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) TRACE(12);
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(CF::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prepack
+// ---------------------------------------------------------------------------
+// logical codes [rows][cols] -> [RB][C][4][32][16 B]
+__global__ void k_prepack_codes(const uint8_t* __restrict__ codes, int64_t rows, int64_t cols, int RB,
+                                int C, uint8_t* __restrict__ out) {
+  const int64_t total = (int64_t)RB * C * kChunkBytes;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e & 15);
+    const int L = (int)((e >> 4) & 31);
+    const int q = (int)((e >> 9) & 3);
+    const int64_t c = (e >> 11) % C;
+    const int64_t rb = (e >> 11) / C;
+    const int64_t row = rb * 32 + L;
+    const int64_t step = 2 * c + (b >> 3);
+    const int64_t k = 64 * step + 16 * q + 2 * (b & 7);
+    uint32_t lo = 0, hi = 0;
+    if (row < rows) {
+      if (k < cols) lo = codes[row * cols + k];
+      if (k + 1 < cols) hi = codes[row * cols + k + 1];
+    }
+    out[e] = (uint8_t)((lo & 15) | ((hi & 15) << 4));
+  }
+}
+
+// LUT (fp32 narrowed values) -> fp16 [RB*32][16], alpha/beta -> [RB][GR][32]
+__global__ void k_prepack_scales(const float* __restrict__ luts, const float* __restrict__ table16,
+                                 const float* __restrict__ alphas, const float* __restrict__ betas,
+                                 int64_t rows, int RB, int GR, __half* __restrict__ lut,
+                                 __half2* __restrict__ ab, int* err) {
+  const int64_t nl = (int64_t)RB * 32 * 16;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nl;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / 16;
+    float v = 0.0f;
+    if (row < rows) v = luts ? luts[e] : table16[e & 15];
+    int st = ANYQ_OK;
+    uint16_t h = f32_to_f16_exact(v, &st);
+    if (st != ANYQ_OK) dev_fail(err, st);
+    lut[e] = __ushort_as_half(h);
+  }
+  const int64_t na = (int64_t)RB * GR * 32;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < na;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int L = (int)(e & 31);
+    const int64_t g = (e >> 5) % GR;
+    const int64_t rb = (e >> 5) / GR;
+    const int64_t row = rb * 32 + L;
+    float a = 1.0f, b = 0.0f;
+    if (row < rows) {
+      a = alphas[row * GR + g];
+      b = betas[row * GR + g];
+    }
+    int st = ANYQ_OK;
+    uint16_t ha = f32_to_f16_exact(a, &st), hb = f32_to_f16_exact(b, &st);
+    if (st != ANYQ_OK) dev_fail(err, st);
+    if (row < rows && !(f16_to_f32_exact(ha) > 0.0f)) dev_fail(err, ANYQ_ERR_INVARIANT);
+    ab[e] = __halves2half2(__ushort_as_half(ha), __ushort_as_half(hb));
+  }
+}
+
+__global__ void k_check_codes_below(const uint8_t* codes, int64_t n, int limit, int* err) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (codes[e] >= limit) dev_fail(err, ANYQ_ERR_CODE_RANGE);
+}
+
+long long* g_trace = nullptr;
+
+template <int MP>
+void launch_mp(const LutTensor* t, const void* x, int64_t m, void* y, float* y32, cudaStream_t s) {
+  using CF = Cfg<MP>;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)t->C);
+    lc.blockDim = dim3(128);
+    lc.stream = s;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_xprep<MP>, reinterpret_cast<const __nv_bfloat16*>(x), (int)m,
+                                 (int64_t)t->cols, t->ximg, t->xinv, t->xsum));
+    ANYQ_LAUNCHED();
+  }
+  Params P;
+  P.codes = t->codes;
+  P.lut = t->lut;
+  P.ab = t->ab;
+  P.ximg = t->ximg;
+  P.xinv = t->xinv;
+  P.xsum = t->xsum;
+  P.part = t->part;
+  P.counters = t->counters;
+  P.y = reinterpret_cast<__nv_bfloat16*>(y);
+  P.y32 = y32;
+  P.N = t->rows;
+  P.U = (int64_t)t->RB * t->C;
+  P.M = (int)m;
+  P.RB = t->RB;
+  P.C = t->C;
+  P.GC = t->GC;
+  P.GR = t->GR;
+  P.cmax = t->cmax;
+  P.ncta = (int)std::min<int64_t>(t->sms, P.U);
+  P.trace = g_trace;
+  const int smem_bytes = CF::kSmem + 2 * t->C * MP * (int)sizeof(float);
+  static int configured = 0;
+  if (smem_bytes > configured) {
+    ANYQ_CUDA(cudaFuncSetAttribute(k_lutgemm<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem_bytes));
+    configured = smem_bytes;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)P.ncta);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = smem_bytes;
+  lc.stream = s;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_lutgemm<MP>, P));
+  ANYQ_LAUNCHED();
+}
+
+}  // namespace
+
+LutTensor* lutgemm_create(const anyq_qtensor* qt) {
+  const anyq_config& c = qt->cfg;
+  if (c.bits != 4) fail(ANYQ_ERR_CONFIG, "tensor-core LUT GEMM needs 4-bit codes");
+  if (c.granularity != ANYQ_G_GROUP && c.granularity != ANYQ_G_ROW)
+    fail(ANYQ_ERR_CONFIG, "tensor-core LUT GEMM needs rowwise or groupwise scales");
+  if (c.granularity == ANYQ_G_GROUP && c.group_size % 128 != 0)
+    fail(ANYQ_ERR_CONFIG, "tensor-core LUT GEMM needs group_size % 128 == 0");
+  if (qt->lut_store != ANYQ_STORE_FP16 || qt->scale_store != ANYQ_STORE_FP16)
+    fail(ANYQ_ERR_CONFIG, "tensor-core LUT GEMM needs fp16 LUT and scale storage");
+  auto* t = new LutTensor();
+  try {
+    const int64_t rows = qt->rows, cols = qt->cols;
+    t->rows = rows;
+    t->cols = cols;
+    t->RB = (int)((rows + 31) / 32);
+    t->C = (int)((cols + 127) / 128);
+    t->GC = c.granularity == ANYQ_G_ROW ? t->C : c.group_size / 128;
+    t->GR = (t->C + t->GC - 1) / t->GC;
+    const int64_t ng = c.granularity == ANYQ_G_ROW ? rows : rows * t->GR;
+    if (ng != qt->num_groups) fail(ANYQ_ERR_SHAPE, "group count mismatch");
+    int dev = 0;
+    ANYQ_CUDA(cudaGetDevice(&dev));
+    ANYQ_CUDA(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, dev));
+    t->weight_bytes = rows * ((cols * 4 + 7) / 8) + ng * 4 + rows * 16 * 2;
+
+    // logical row-major codes on device
+    const int64_t nb = rows * packed_bpr(cols, 4);
+    DevBuf<uint8_t> dp(nb), logical(rows * cols), tmp;
+    dp.upload(qt->codes, nb);
+    launch_unpack(dp.p, rows, cols, 4, logical.p, 0);
+    if (qt->layout == ANYQ_LAYOUT_KTILED) {
+      tmp.alloc(rows * cols);
+      launch_ktile(logical.p, rows, cols, qt->tile_k, 1, tmp.p, 0);
+      ANYQ_CUDA(cudaMemcpy(logical.p, tmp.p, rows * cols, cudaMemcpyDeviceToDevice));
+    }
+    DevBuf<int> err(1);
+    err.zero();
+    Table fixed{};
+    if (c.codebook != ANYQ_CB_ANY) {
+      fixed = effective_table(fixed_table(c), c.symmetric != 0);
+      if (fixed.n < 16) {
+        k_check_codes_below<<<148, 256>>>(logical.p, rows * cols, fixed.n, err.p);
+        ANYQ_LAUNCHED();
+      }
+      for (int i = fixed.n; i < 16; ++i) fixed.v[i] = 0.0f;
+    }
+    ANYQ_CUDA(cudaMalloc(&t->codes, (size_t)t->RB * t->C * kChunkBytes));
+    k_prepack_codes<<<148 * 8, 256>>>(logical.p, rows, cols, t->RB, t->C, t->codes);
+    ANYQ_LAUNCHED();
+
+    DevBuf<float> luts, table16(16), alphas(ng), betas(ng);
+    if (c.codebook == ANYQ_CB_ANY) {
+      luts.alloc(rows * 16);
+      luts.upload(qt->luts, rows * 16);
+    }
+    table16.upload(fixed.v, 16);
+    // scales in [row][GR] order (rowwise: GR == 1 per row)
+    alphas.upload(qt->alphas, ng);
+    betas.upload(qt->betas, ng);
+    ANYQ_CUDA(cudaMalloc(&t->lut, sizeof(__half) * t->RB * 32 * 16));
+    ANYQ_CUDA(cudaMalloc(&t->ab, sizeof(__half2) * t->RB * t->GR * 32));
+    k_prepack_scales<<<148, 256>>>(luts.p, table16.p, alphas.p, betas.p, rows, t->RB, t->GR, t->lut,
+                                   t->ab, err.p);
+    ANYQ_LAUNCHED();
+    ANYQ_CUDA(cudaDeviceSynchronize());
+    check_device_error(err.p, "dev_tensor_create");
+
+    // workspace
+    const int64_t U = (int64_t)t->RB * t->C;
+    const int ncta = (int)std::min<int64_t>(t->sms, U);
+    int cmax = 1;
+    for (int rb = 0; rb < t->RB; ++rb) {
+      auto cta = [&](int64_t u) { return (int)(((u + 1) * ncta + U - 1) / U) - 1; };
+      cmax = std::max(cmax, cta((int64_t)(rb + 1) * t->C - 1) - cta((int64_t)rb * t->C) + 1);
+    }
+    t->cmax = cmax;
+    ANYQ_CUDA(cudaMalloc(&t->ximg, sizeof(__half) * (size_t)2 * t->C * 64 * 16));
+    ANYQ_CUDA(cudaMalloc(&t->xinv, sizeof(float) * t->C * kMaxMP));
+    ANYQ_CUDA(cudaMalloc(&t->xsum, sizeof(float) * t->C * kMaxMP));
+    ANYQ_CUDA(cudaMalloc(&t->part, sizeof(float) * (size_t)t->RB * cmax * kMaxMP * 32));
+    ANYQ_CUDA(cudaMalloc(&t->counters, sizeof(int) * t->RB));
+    ANYQ_CUDA(cudaMemset(t->counters, 0, sizeof(int) * t->RB));
+  } catch (...) {
+    lutgemm_destroy(t);
+    throw;
+  }
+  return t;
+}
+
+void lutgemm_set_trace(long long* dev) { g_trace = dev; }
+
+void lutgemm_destroy(LutTensor* t) {
+  if (!t) return;
+  cudaFree(t->codes);
+  cudaFree(t->lut);
+  cudaFree(t->ab);
+  cudaFree(t->ximg);
+  cudaFree(t->xinv);
+  cudaFree(t->xsum);
+  cudaFree(t->part);
+  cudaFree(t->counters);
+  delete t;
+}
+
+void lutgemm_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y32,
+                 cudaStream_t s) {
+  if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");
+  if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "tensor-core LUT GEMM supports 1 <= m <= 16");
+  if (m <= 4) launch_mp<4>(t, x, m, y, y32, s);
+  else if (m <= 8) launch_mp<8>(t, x, m, y, y32, s);
+  else launch_mp<16>(t, x, m, y, y32, s);
+}
+
+}  // namespace anyq_b200

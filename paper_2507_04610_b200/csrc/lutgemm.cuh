@@ -1,0 +1,37 @@
+// Tensor-core LUT GEMM (small M): device-resident prepacked weight tensor.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace anyq_b200 {
+
+// Prepacked 4-bit LUT tensor resident in HBM (see lutgemm.cu for layouts).
+struct LutTensor {
+  int64_t rows = 0, cols = 0;
+  int RB = 0;   // 32-row blocks
+  int C = 0;    // 128-wide k chunks (K padded up)
+  int GC = 0;   // chunks per scale group
+  int GR = 0;   // scale groups per row
+  int64_t weight_bytes = 0;  // algorithmic bytes streamed per GEMM (codes+scales+LUT)
+  uint8_t* codes = nullptr;  // [RB][C][4 quarters][32 rows][16 B]
+  __half* lut = nullptr;     // [RB*32][16]
+  __half2* ab = nullptr;     // [RB][GR][32] (alpha, beta)
+  // per-call workspace (one call in flight per tensor)
+  __half* ximg = nullptr;  // [2C steps][64 rows][16 k] canonical UMMA K-major images
+  float* xinv = nullptr;   // [C][16]  2^-e per (chunk, m)
+  float* xsum = nullptr;   // [C][16]  sum_k x per (chunk, m)
+  float* part = nullptr;   // [RB][cmax][16][32]
+  int* counters = nullptr; // [RB]
+  int cmax = 0;
+  int sms = 148;
+};
+
+LutTensor* lutgemm_create(const anyq_qtensor* qt);
+void lutgemm_destroy(LutTensor* t);
+void lutgemm_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
+void lutgemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
+                 cudaStream_t s);
+
+}  // namespace anyq_b200

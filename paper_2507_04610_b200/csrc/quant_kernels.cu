@@ -1,0 +1,442 @@
+// Element-wise / per-group kernels of the quantize and layout path:
+//   scales (scaling.cpp:29-70), scaled weights (scaling.cpp:72-83), sample
+//   weights (learner.cpp:25-51, 379-380), RTN onto fixed tables
+//   (codebooks.cpp:75-97), bit packing (pack.cpp:15-55), k-tiling
+//   (pack.cpp:175-199), 16-bit narrowing (pack.cpp:159-169), dequantisation
+//   (pack.cpp:205-238) and the bit-exact fp32 LUT GEMM (qgemm.cpp:71-128).
+//
+// Every arithmetic step that the reference performs in fp32 is written with
+// explicit round-to-nearest intrinsics (__fadd_rn/__fmul_rn/__fdiv_rn) so the
+// compiler cannot contract or reassociate it: these kernels are bit-identical
+// to the reference by construction.
+#include "kernels.cuh"
+
+namespace anyq_b200 {
+
+// ---------------------------------------------------------------------------
+// finite check (core.hpp:145-147)
+// ---------------------------------------------------------------------------
+__global__ void k_check_finite(const float* __restrict__ p, int64_t n, int* err, int status) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int bad = 0;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) bad |= !isfinite(p[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) dev_fail(err, status);
+}
+
+// stats entries must be >= 0 and finite (learner.cpp:33-35)
+__global__ void k_check_stats(const float* __restrict__ p, int64_t n, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int bad = 0;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) bad |= !(p[i] >= 0.0f) || !isfinite(p[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) dev_fail(err, ANYQ_ERR_STATS);
+}
+
+// ---------------------------------------------------------------------------
+// Scales. The reference scans elements in row-major order with strict < / >,
+// so among equal extreme values the first encountered wins (this matters for
+// -0.0 vs +0.0). Both paths reduce (value, flat index) pairs with the same
+// tie rule, which reproduces that exactly.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void alpha_beta(float mn, float mx, bool symmetric, float qmin,
+                                           float qmax, float* a, float* b) {
+  if (symmetric) {
+    float x = fabsf(mn), y = fabsf(mx);
+    float absmax = (x < y) ? y : x;  // std::max(x, y)
+    *a = absmax > 0.0f ? __fdiv_rn(absmax, qmax) : 1.0f;
+    *b = 0.0f;
+  } else {
+    float range = __fsub_rn(mx, mn);
+    *a = range > 0.0f ? __fdiv_rn(range, __fsub_rn(qmax, qmin)) : 1.0f;
+    *b = mn;
+  }
+}
+
+// One warp per (row, group) for rowwise / groupwise granularity.
+__global__ void k_scales_rowgroup(const float* __restrict__ w, int64_t rows, int64_t cols,
+                                  int64_t gsize, int64_t gpr, bool symmetric, float qmin,
+                                  float qmax, float* __restrict__ alphas,
+                                  float* __restrict__ betas) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= rows * gpr) return;
+  int64_t i = warp / gpr, g = warp % gpr;
+  int64_t j0 = g * gsize, j1 = min(cols, j0 + gsize);
+  const float* row = w + i * cols;
+  float mn = FLT_MAX, mx = -FLT_MAX;
+  int64_t imn = INT64_MAX, imx = INT64_MAX;
+  for (int64_t j = j0 + lane; j < j1; j += 32) {
+    float v = row[j];
+    if (v < mn) { mn = v; imn = j; }
+    if (v > mx) { mx = v; imx = j; }
+  }
+  for (int off = 16; off; off >>= 1) {
+    float omn = __shfl_xor_sync(0xffffffffu, mn, off);
+    int64_t oimn = __shfl_xor_sync(0xffffffffu, imn, off);
+    float omx = __shfl_xor_sync(0xffffffffu, mx, off);
+    int64_t oimx = __shfl_xor_sync(0xffffffffu, imx, off);
+    if (omn < mn || (omn == mn && oimn < imn)) { mn = omn; imn = oimn; }
+    if (omx > mx || (omx == mx && oimx < imx)) { mx = omx; imx = oimx; }
+  }
+  if (lane == 0) {
+    // The reference starts from FLT_MAX / lowest() and only replaces on
+    // strict comparison, so a group whose values are all FLT_MAX keeps it.
+    float a, b;
+    alpha_beta(mn, mx, symmetric, qmin, qmax, &a, &b);
+    alphas[warp] = a;
+    betas[warp] = b;
+  }
+}
+
+// Ordered 64-bit key for atomic (value, index) reductions: -0.0 and +0.0
+// compare equal (as the reference's float comparisons do) and ties break on
+// the smaller flat index.
+__device__ __forceinline__ uint32_t ordered(float v) {
+  uint32_t u = __float_as_uint(v == 0.0f ? 0.0f : v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void k_scales_atomic(const float* __restrict__ w, int64_t rows, int64_t cols,
+                                GroupMap gm, unsigned long long* __restrict__ kmin,
+                                unsigned long long* __restrict__ kmax) {
+  int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, j = e % cols;
+    int64_t g = gm(i, j);
+    uint32_t o = ordered(w[e]);
+    atomicMin(&kmin[g], ((unsigned long long)o << 32) | (uint32_t)e);
+    atomicMax(&kmax[g], ((unsigned long long)o << 32) | (0xFFFFFFFFu - (uint32_t)e));
+  }
+}
+
+__global__ void k_scales_finish(const float* __restrict__ w, int64_t ng,
+                                const unsigned long long* __restrict__ kmin,
+                                const unsigned long long* __restrict__ kmax, bool symmetric,
+                                float qmin, float qmax, float* alphas, float* betas) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  uint32_t imn = (uint32_t)(kmin[g] & 0xFFFFFFFFull);
+  uint32_t imx = 0xFFFFFFFFu - (uint32_t)(kmax[g] & 0xFFFFFFFFull);
+  float a, b;
+  alpha_beta(w[imn], w[imx], symmetric, qmin, qmax, &a, &b);
+  alphas[g] = a;
+  betas[g] = b;
+}
+
+// ---------------------------------------------------------------------------
+// Scaled weights + per-row sample weights (one block per row).
+// ---------------------------------------------------------------------------
+__global__ void k_scale_rows(const float* __restrict__ w, int64_t rows, int64_t cols, GroupMap gm,
+                             const float* __restrict__ alphas, const float* __restrict__ betas,
+                             const float* __restrict__ exj, int weighting,
+                             float* __restrict__ ws, float* __restrict__ sw, int* err) {
+  int64_t i = blockIdx.x;
+  if (i >= rows) return;
+  const float* wr = w + i * cols;
+  float* wsr = ws + i * cols;
+  float* swr = sw ? sw + i * cols : nullptr;
+  int any_pos = 0, bad = 0;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    int64_t g = gm(i, j);
+    float x = __fdiv_rn(__fsub_rn(wr[j], betas[g]), alphas[g]);
+    wsr[j] = x;
+    bad |= !isfinite(x);
+    if (swr) {
+      float e = exj ? exj[j] : 1.0f;
+      float v = weighting == ANYQ_W_WEIGHTS ? 1.0f
+                : weighting == ANYQ_W_ACTS  ? e
+                                            : __fmul_rn(alphas[g], e);
+      swr[j] = v;
+      any_pos |= v > 0.0f;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) dev_fail(err, ANYQ_ERR_NONFINITE);
+  if (swr && !__syncthreads_or(any_pos)) {  // fully dead channels (learner.cpp:380)
+    for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) swr[j] = 1.0f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RTN onto a sorted table, ties toward the lower index (codebooks.cpp:75-97).
+// ---------------------------------------------------------------------------
+__global__ void k_round_to_table(const float* __restrict__ ws, int64_t n, Table t,
+                                 uint8_t* __restrict__ codes) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float x = ws[e];
+    int lo = 0, hi = t.n;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (t.v[mid] < x) lo = mid + 1;
+      else hi = mid;
+    }
+    uint8_t q;
+    if (lo == 0) q = 0;
+    else if (lo == t.n) q = (uint8_t)(t.n - 1);
+    else q = (__fsub_rn(x, t.v[lo - 1]) <= __fsub_rn(t.v[lo], x)) ? (uint8_t)(lo - 1) : (uint8_t)lo;
+    codes[e] = q;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packing (pack.cpp:15-55): one thread per output byte / per code.
+// ---------------------------------------------------------------------------
+__global__ void k_pack(const uint8_t* __restrict__ codes, int64_t rows, int64_t cols, int bits,
+                       uint8_t* __restrict__ out, int* err) {
+  int64_t bpr = (cols * bits + 7) / 8;
+  int64_t total = rows * bpr;
+  uint32_t limit = 1u << bits;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / bpr, b = e % bpr;
+    int64_t j0 = (8 * b) / bits, j1 = min(cols - 1, (8 * b + 7) / bits);
+    uint32_t byte = 0;
+    for (int64_t j = j0; j <= j1; ++j) {
+      uint32_t c = codes[i * cols + j];
+      if (c >= limit) dev_fail(err, ANYQ_ERR_CODE_RANGE);
+      int64_t bit = j * bits;
+      if ((bit >> 3) == b) byte |= (c << (bit & 7)) & 0xFFu;
+      else if ((bit & 7) + bits > 8 && (bit >> 3) + 1 == b) byte |= (c >> (8 - (bit & 7))) & 0xFFu;
+    }
+    out[e] = (uint8_t)byte;
+  }
+}
+
+__device__ __forceinline__ uint32_t code_at(const uint8_t* __restrict__ row, int64_t j, int bits) {
+  int64_t bit = j * bits;
+  uint32_t v = (uint32_t)row[bit >> 3] >> (bit & 7);
+  if ((bit & 7) + bits > 8) v |= (uint32_t)row[(bit >> 3) + 1] << (8 - (bit & 7));
+  return v & ((1u << bits) - 1u);
+}
+
+__global__ void k_unpack(const uint8_t* __restrict__ packed, int64_t rows, int64_t cols, int bits,
+                         uint8_t* __restrict__ codes) {
+  int64_t bpr = (cols * bits + 7) / 8;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, j = e % cols;
+    codes[e] = (uint8_t)code_at(packed + i * bpr, j, bits);
+  }
+}
+
+// Logical codes -> k-tiled logical codes (inverse=0), or back (inverse=1).
+__global__ void k_ktile(const uint8_t* __restrict__ in, int64_t rows, int64_t cols, int64_t tile_k,
+                        int inverse, uint8_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, j = e % cols;
+    int64_t p = ktiled_pos(j, cols, tile_k);
+    if (inverse) out[e] = in[i * cols + p];
+    else out[i * cols + p] = in[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// narrowed() (pack.cpp:159-169)
+// ---------------------------------------------------------------------------
+__global__ void k_narrow(float* __restrict__ v, int64_t n, int store, int is_alpha, int* err) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int st = ANYQ_OK;
+    float r = narrow_widen(v[e], store, &st);
+    if (st != ANYQ_OK) dev_fail(err, st);
+    else if (is_alpha && !(r > 0.0f)) dev_fail(err, ANYQ_ERR_INVARIANT);
+    v[e] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dequantize(qt) (pack.cpp:205-238 + scaling.cpp:85-96)
+// ---------------------------------------------------------------------------
+__global__ void k_dequant(const uint8_t* __restrict__ packed, int64_t rows, int64_t cols, int bits,
+                          int ktiled, int64_t tile_k, const float* __restrict__ luts, Table fixed,
+                          GroupMap gm, const float* __restrict__ alphas,
+                          const float* __restrict__ betas, float* __restrict__ w, int* err) {
+  int64_t bpr = (cols * bits + 7) / 8;
+  int lut_n = 1 << bits;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols, j = e % cols;
+    int64_t pos = ktiled ? ktiled_pos(j, cols, tile_k) : j;
+    uint32_t c = code_at(packed + i * bpr, pos, bits);
+    float v;
+    if (luts) {
+      v = luts[i * lut_n + c];
+    } else {
+      if ((int)c >= fixed.n) {
+        dev_fail(err, ANYQ_ERR_CODE_RANGE);
+        v = 0.0f;
+      } else {
+        v = fixed.v[c];
+      }
+    }
+    int64_t g = gm(i, j);
+    w[e] = __fadd_rn(__fmul_rn(alphas[g], v), betas[g]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bit-exact LUT GEMM, gemm_fused semantics (qgemm.cpp:71-128): per output
+// element, k ascending, fp32 accumulate, no contraction. One thread per
+// (row of W, row of x). Used for arbitrary configs (any bits, codebook,
+// granularity, layout, ragged K) and as the exact mode of the C-ABI.
+// ---------------------------------------------------------------------------
+__global__ void k_gemm_exact(const float* __restrict__ x, int64_t m, int64_t k,
+                             const uint8_t* __restrict__ packed, int64_t n, int bits, int ktiled,
+                             int64_t tile_k, const float* __restrict__ luts, Table fixed,
+                             GroupMap gm, const float* __restrict__ alphas,
+                             const float* __restrict__ betas, float* __restrict__ y, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // row of W
+  int64_t r = blockIdx.y;                                         // row of x
+  if (i >= n || r >= m) return;
+  int64_t bpr = (k * bits + 7) / 8;
+  const uint8_t* row = packed + i * bpr;
+  const float* xr = x + r * k;
+  const float* table = luts ? luts + i * (int64_t(1) << bits) : fixed.v;
+  int tsize = luts ? (1 << bits) : fixed.n;
+  float acc = 0.0f;
+  for (int64_t j = 0; j < k; ++j) {
+    int64_t pos = ktiled ? ktiled_pos(j, k, tile_k) : j;
+    uint32_t c = code_at(row, pos, bits);
+    if ((int)c >= tsize) {
+      dev_fail(err, ANYQ_ERR_CODE_RANGE);
+      c = 0;
+    }
+    int64_t g = gm(i, j);
+    float wv = __fadd_rn(__fmul_rn(alphas[g], table[c]), betas[g]);
+    acc = __fadd_rn(acc, __fmul_rn(xr[j], wv));
+  }
+  y[r * n + i] = acc;
+}
+
+// gemm_dense (qgemm.cpp:22-34), same order and rounding.
+__global__ void k_gemm_dense(const float* __restrict__ x, int64_t m, const float* __restrict__ w,
+                             int64_t n, int64_t k, float* __restrict__ y) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t r = blockIdx.y;
+  if (i >= n || r >= m) return;
+  float acc = 0.0f;
+  for (int64_t j = 0; j < k; ++j) acc = __fadd_rn(acc, __fmul_rn(x[r * k + j], w[i * k + j]));
+  y[r * n + i] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int grid_for(int64_t n, int block = 256) {
+  int64_t g = (n + block - 1) / block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+void launch_check_finite(const float* p, int64_t n, int* err, int status, cudaStream_t s) {
+  if (n <= 0) return;
+  k_check_finite<<<grid_for(n), 256, 0, s>>>(p, n, err, status);
+  ANYQ_LAUNCHED();
+}
+
+void launch_check_stats(const float* p, int64_t n, int* err, cudaStream_t s) {
+  if (n <= 0) return;
+  k_check_stats<<<grid_for(n), 256, 0, s>>>(p, n, err);
+  ANYQ_LAUNCHED();
+}
+
+void launch_scales(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg, float qmin,
+                   float qmax, float* alphas, float* betas, cudaStream_t s) {
+  GroupMap gm = make_group_map(cfg, cols);
+  if (cfg.granularity == ANYQ_G_GROUP || cfg.granularity == ANYQ_G_ROW) {
+    int64_t gsize = cfg.granularity == ANYQ_G_ROW ? cols : cfg.group_size;
+    int64_t gpr = (cols + gsize - 1) / gsize;
+    int64_t warps = rows * gpr;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    k_scales_rowgroup<<<(unsigned)blocks, 256, 0, s>>>(w, rows, cols, gsize, gpr, cfg.symmetric != 0,
+                                                       qmin, qmax, alphas, betas);
+    ANYQ_LAUNCHED();
+    return;
+  }
+  if (rows * cols >= (int64_t(1) << 32)) fail(ANYQ_ERR_SHAPE, "tensor too large for scale reduction");
+  int64_t ng = group_count(cfg, rows, cols);
+  DevBuf<unsigned long long> kmin(ng), kmax(ng);
+  ANYQ_CUDA(cudaMemsetAsync(kmin.p, 0xFF, sizeof(unsigned long long) * ng, s));
+  ANYQ_CUDA(cudaMemsetAsync(kmax.p, 0x00, sizeof(unsigned long long) * ng, s));
+  k_scales_atomic<<<grid_for(rows * cols), 256, 0, s>>>(w, rows, cols, gm, kmin.p, kmax.p);
+  ANYQ_LAUNCHED();
+  k_scales_finish<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(w, ng, kmin.p, kmax.p,
+                                                              cfg.symmetric != 0, qmin, qmax,
+                                                              alphas, betas);
+  ANYQ_LAUNCHED();
+  ANYQ_CUDA(cudaStreamSynchronize(s));  // scratch freed on return
+}
+
+void launch_scale_rows(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg,
+                       const float* alphas, const float* betas, const float* exj, float* ws,
+                       float* sw, int* err, cudaStream_t s) {
+  GroupMap gm = make_group_map(cfg, cols);
+  k_scale_rows<<<(unsigned)rows, 256, 0, s>>>(w, rows, cols, gm, alphas, betas, exj, cfg.weighting,
+                                              ws, sw, err);
+  ANYQ_LAUNCHED();
+}
+
+void launch_round(const float* ws, int64_t n, const Table& t, uint8_t* codes, cudaStream_t s) {
+  k_round_to_table<<<grid_for(n), 256, 0, s>>>(ws, n, t, codes);
+  ANYQ_LAUNCHED();
+}
+
+void launch_pack(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
+                 int* err, cudaStream_t s) {
+  int64_t total = rows * packed_bpr(cols, bits);
+  k_pack<<<grid_for(total), 256, 0, s>>>(codes, rows, cols, bits, out, err);
+  ANYQ_LAUNCHED();
+}
+
+void launch_unpack(const uint8_t* packed, int64_t rows, int64_t cols, int bits, uint8_t* codes,
+                   cudaStream_t s) {
+  k_unpack<<<grid_for(rows * cols), 256, 0, s>>>(packed, rows, cols, bits, codes);
+  ANYQ_LAUNCHED();
+}
+
+void launch_ktile(const uint8_t* in, int64_t rows, int64_t cols, int64_t tile_k, int inverse,
+                  uint8_t* out, cudaStream_t s) {
+  k_ktile<<<grid_for(rows * cols), 256, 0, s>>>(in, rows, cols, tile_k, inverse, out);
+  ANYQ_LAUNCHED();
+}
+
+void launch_narrow(float* v, int64_t n, int store, int is_alpha, int* err, cudaStream_t s) {
+  if (n <= 0 || store == ANYQ_STORE_FP32) {
+    if (is_alpha && n > 0) {  // fp32 store still requires alpha > 0 after narrowing (identity)
+      k_narrow<<<grid_for(n), 256, 0, s>>>(v, n, ANYQ_STORE_FP32, is_alpha, err);
+      ANYQ_LAUNCHED();
+    }
+    return;
+  }
+  k_narrow<<<grid_for(n), 256, 0, s>>>(v, n, store, is_alpha, err);
+  ANYQ_LAUNCHED();
+}
+
+void launch_dequant(const uint8_t* packed, int64_t rows, int64_t cols, int bits, int ktiled,
+                    int64_t tile_k, const float* luts, const Table& fixed, const anyq_config& cfg,
+                    const float* alphas, const float* betas, float* w, int* err, cudaStream_t s) {
+  GroupMap gm = make_group_map(cfg, cols);
+  k_dequant<<<grid_for(rows * cols), 256, 0, s>>>(packed, rows, cols, bits, ktiled, tile_k, luts,
+                                                  fixed, gm, alphas, betas, w, err);
+  ANYQ_LAUNCHED();
+}
+
+void launch_gemm_exact(const float* x, int64_t m, int64_t k, const uint8_t* packed, int64_t n,
+                       int bits, int ktiled, int64_t tile_k, const float* luts, const Table& fixed,
+                       const anyq_config& cfg, const float* alphas, const float* betas, float* y,
+                       int* err, cudaStream_t s) {
+  GroupMap gm = make_group_map(cfg, k);
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);
+  k_gemm_exact<<<grid, 128, 0, s>>>(x, m, k, packed, n, bits, ktiled, tile_k, luts, fixed, gm,
+                                    alphas, betas, y, err);
+  ANYQ_LAUNCHED();
+}
+
+void launch_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int64_t k, float* y,
+                       cudaStream_t s) {
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);
+  k_gemm_dense<<<grid, 128, 0, s>>>(x, m, w, n, k, y);
+  ANYQ_LAUNCHED();
+}
+
+}  // namespace anyq_b200

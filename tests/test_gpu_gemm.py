@@ -1,0 +1,182 @@
+"""GEMM on the GPU vs the oracle.
+
+* anyq_gemm_fused (exact path): bit-identical to the reference gemm_fused /
+  gemm_reference for every format, layout and M (test_qgemm.cpp:53-160).
+* tensor-core LUT GEMM (device path, bf16 x, fp32 accumulate): within
+  |dy| <= 1e-5 * sum_j |x_j| * (|alpha*T| + |beta|) of
+  gemm_reference(bf16(x), narrowed(qt)) computed by the oracle in fp32.
+"""
+import numpy as np
+import pytest
+
+from anyq_testutil import bits_equal, cfg
+
+pytestmark = pytest.mark.gpu
+
+
+def quantize_format(aq, orc, w, fmt, seed, group_size):
+    c = cfg(granularity=3, group_size=group_size, seed=seed)
+    aq.apply_format(c, fmt)
+    return orc.quantize(w, c)
+
+
+def test_hand_case(aq):
+    from paper_2507_04610_b200.qtensor import QuantizedTensor
+
+    c = cfg(codebook=0, bits=4, granularity=1, symmetric=1)
+    qt = QuantizedTensor.empty(4, 4, c)
+    codes = np.array([[8, 9, 10, 11], [12, 13, 14, 15], [0, 2, 4, 6], [7, 8, 9, 15]], np.uint8)
+    qt.codes = aq.pack_codes(codes, 4)
+    qt.alphas[:] = 0.2
+    qt.betas[:] = 0
+    y = aq.gemm_reference(np.array([[1, 2, 3, 4]], np.float32), qt)
+    exp = 0.2 * np.array([0 + 2 + 6 + 12, 4 + 10 + 18 + 28, -8 - 12 - 12 - 8, -1 + 0 + 3 + 28])
+    assert np.allclose(y[0], exp, rtol=1e-6)
+    assert np.abs(aq.gemm_fused(np.zeros((2, 4), np.float32), qt)).max() == 0
+
+
+@pytest.mark.parametrize("fmt", ["int4", "fp4", "nf4", "any4", "any2", "any3", "int8"])
+@pytest.mark.parametrize("m", [1, 5, 16])
+def test_fused_bit_exact_vs_reference(aq, orc, fmt, m):
+    w = orc.gaussian(24, 56, 11)
+    qt = quantize_format(aq, orc, w, fmt, 5, 8)
+    x = orc.gaussian(m, 56, 13 + m)
+    y = aq.gemm_fused(x, qt)
+    assert bits_equal(y, orc.gemm_fused(x, qt))
+    assert bits_equal(y, orc.gemm_reference(x, qt))
+    assert bits_equal(aq.gemm_reference(x, qt), orc.gemm_reference(x, qt))
+
+
+@pytest.mark.parametrize("tile_k", [2, 8, 32])
+def test_ktiled_equals_rowmajor(aq, orc, tile_k):
+    w = orc.gaussian(17, 40, 17)
+    qt = quantize_format(aq, orc, w, "any4", 9, 8)
+    tiled = aq.to_ktiled(qt, tile_k)
+    x = orc.gaussian(4, 40, 19)
+    assert bits_equal(aq.gemm_fused(x, tiled), aq.gemm_fused(x, qt))
+    assert bits_equal(aq.gemm_fused(x, tiled), orc.gemm_fused(x, tiled))
+
+
+def test_plan_mismatch_rejected(aq, orc):
+    w = orc.gaussian(6, 16, 53)
+    qt = quantize_format(aq, orc, w, "int4", 1, 8)
+    x = orc.gaussian(2, 16, 59)
+    plan = aq.make_plan(x, qt)
+    plan.layout, plan.tile_k = 1, 4
+    with pytest.raises(aq.ConfigError):
+        aq.gemm_fused(x, qt, plan)
+    with pytest.raises(aq.ShapeError):
+        aq.gemm_reference(orc.gaussian(2, 17, 61), qt)
+
+
+def test_fp4_code_15_raises(aq, orc):
+    w = orc.gaussian(4, 32, 3)
+    qt = quantize_format(aq, orc, w, "fp4", 1, 16)
+    qt.codes[0] = 0xFF
+    with pytest.raises(aq.CodeRangeError):
+        aq.gemm_fused(orc.gaussian(1, 32, 2), qt)
+
+
+@pytest.mark.slow
+def test_property_sweep_1000_cases(aq, orc):
+    """acceptance.cpp:415-453: M in 1..16, K,N in 8..256, 4 formats, both layouts."""
+    r = orc.rng_double(4242, 0, 6000)
+    fmts = ["int4", "fp4", "nf4", "any4"]
+    for t in range(200):
+        m = 1 + int(r[6 * t] * 16)
+        n = 8 + int(r[6 * t + 1] * 249)
+        k = 8 + int(r[6 * t + 2] * 249)
+        fmt = fmts[int(r[6 * t + 3] * 4)]
+        tile = [1, 2, 8, 32][int(r[6 * t + 4] * 4)]
+        w = orc.gaussian(n, k, 7000 + t)
+        qt = quantize_format(aq, orc, w, fmt, t, min(128, k) if k >= 2 else 2)
+        if r[6 * t + 5] < 0.5:
+            qt = orc.to_ktiled(qt, tile)
+        x = orc.gaussian(m, k, 9000 + t)
+        assert bits_equal(aq.gemm_fused(x, qt), orc.gemm_fused(x, qt)), (m, n, k, fmt)
+
+
+# ---------------------------------------------------------------------------
+# tensor-core path
+# ---------------------------------------------------------------------------
+def bf16(x):
+    from oracle.refpy import bf16_round
+
+    return bf16_round(x)
+
+
+def tc_gemm(aq, cuda, qt, x):
+    import torch
+
+    dt = aq.DeviceTensor(qt)
+    xt = torch.from_numpy(bf16(x)).to("cuda", torch.bfloat16).contiguous()
+    y = torch.empty((x.shape[0], qt.rows), dtype=torch.bfloat16, device="cuda")
+    y32 = torch.empty((x.shape[0], qt.rows), dtype=torch.float32, device="cuda")
+    dt.gemm(xt, y, y32)
+    torch.cuda.synchronize()
+    out = y32.cpu().numpy(), y.float().cpu().numpy()
+    dt.close()
+    return out
+
+
+def tc_tolerance(orc, x, qt):
+    """1e-5 * sum_j |x_j| (|alpha T[c]| + |beta|) per output element.
+
+    Fixed tables are not narrowed by the reference (pack.cpp:159-169 narrows
+    only learned LUTs) while the tensor-core path holds every table in fp16:
+    for nf4 (the only fixed table with values that are not fp16-exact) the
+    bound adds the table rounding, sum_j |x_j| * alpha * 2^-11 |T[c]|.
+    """
+    n = orc.narrowed(qt)
+    nq = n.clone()
+    nq.betas[:] = 0
+    aT = np.abs(orc.dequantize(nq))
+    b = np.abs(orc.dequantize(n) - orc.dequantize(nq))
+    tol = 1e-5 * (np.abs(x) @ (aT + b).T)
+    if qt.cfg.codebook == 2:  # nf4
+        tol = tol + 2.0 ** -11 * (np.abs(x) @ aT.T)
+    return tol + 1e-30
+
+
+@pytest.mark.parametrize("fmt", ["any4", "int4", "nf4", "fp4"])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8, 9, 16])
+def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m):
+    n, k = 200, 384  # ragged rows (not a multiple of 32), 3 chunks, 3 groups
+    w = orc.gaussian(n, k, 31)
+    c = cfg(granularity=3, group_size=128, seed=2)
+    aq.apply_format(c, fmt)
+    qt = orc.quantize(w, c)
+    x = bf16(orc.gaussian(m, k, 33))
+    y32, ybf = tc_gemm(aq, cuda, qt, x)
+    ref = orc.gemm_reference(x, orc.narrowed(qt))
+    tol = tc_tolerance(orc, x, qt)
+    err = np.abs(y32 - ref)
+    assert np.all(err <= tol), f"max err {err.max()} tol {tol.min()}"
+    assert np.all(np.abs(ybf - bf16(ref)) <= np.abs(ref) * 2 ** -7 + tol)
+
+
+@pytest.mark.parametrize("n,k,g", [(4096, 4096, 128), (1024, 4096, 128), (4096, 1024, 256),
+                                   (96, 1280, 1280), (33, 128, 128)])
+def test_tc_gemm_shapes(aq, orc, cuda, n, k, g):
+    w = orc.gaussian(n, k, 41)
+    gran = 1 if g == k else 3
+    c = cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=8)
+    qt = aq.quantize_any(w, c)
+    x = bf16(orc.gaussian(3, k, 43))
+    y32, _ = tc_gemm(aq, cuda, qt, x)
+    ref = orc.gemm_reference(x, orc.narrowed(qt))
+    tol = tc_tolerance(orc, x, qt)
+    assert np.all(np.abs(y32 - ref) <= tol)
+
+
+def test_tc_gemm_is_deterministic_and_rowwise_consistent(aq, orc, cuda):
+    w = orc.gaussian(512, 1024, 5)
+    qt = aq.quantize_any(w, cfg(codebook=3, max_iters=5))
+    x1 = bf16(orc.gaussian(1, 1024, 6))
+    x16 = np.repeat(x1, 16, axis=0)
+    a, _ = tc_gemm(aq, cuda, qt, x1)
+    b, _ = tc_gemm(aq, cuda, qt, x1)
+    c, _ = tc_gemm(aq, cuda, qt, x16)
+    assert bits_equal(a, b)
+    for r in range(16):
+        assert np.allclose(c[r], a[0], rtol=0, atol=1e-5 * np.abs(a[0]).max())
