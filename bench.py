@@ -1,0 +1,546 @@
+#!/usr/bin/env python
+"""Benchmark of the any4 hot path on B200 (contract: see DESIGN.md §Measurement).
+
+Headline (BASELINE.json metric "any4 GEMM µs and % HBM peak at M=1–16 (Llama-3
+shapes); k-means rows/s", config[1] "Llama-3-8B layer shapes ... M=1..16"):
+
+  step   = the seven Llama-3-8B decoder-layer GEMMs (q,k,v,o,gate,up,down) at
+           M=1 on any4 g128 weights, y = x W^T, bf16 x/y, tensor-core LUT path.
+           Weights rotate over LAYERS layers (> L2), so every step streams its
+           weights from HBM. CUDA graphs remove host launch overhead.
+  value  = algorithmic bytes streamed per step / device time per step (GB/s),
+           whole job over all ranks.
+  e2e    = same metric through the public API with HOST buffers: every GEMM's
+           x is copied H2D from pinned memory and y copied back D2H inside the
+           timed region.
+  extras = per-shape µs and % of HBM peak, the M=1..16 sweep, k-means rows/s
+           (config 1), roofline of the dominant kernel, CPU baseline.
+
+`--impl reference` times the reference's own CPU GEMM (oracle/_ref, the
+unmodified reference built in place) on the host cores with the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Llama-3-8B linear layers (N x K) — SURVEY.md §8(d) config 2.
+LAYER = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
+         ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+GROUP = 128
+METRIC = "any4 GEMM µs and % HBM peak at M=1–16 (Llama-3 shapes); k-means rows/s"
+UNIT = "GB/s"
+
+
+def algo_bytes(n, k, m, bits=4, group=GROUP):
+    """Algorithmic bytes of one GEMM: codes + fp16 alpha/beta
+    + fp16 LUT + bf16 x + bf16 y."""
+    codes = n * ((k * bits + 7) // 8)
+    scales = n * ((k + group - 1) // group) * 2 * 2
+    lut = n * (1 << bits) * 2
+    return codes + scales + lut + m * k * 2 + m * n * 2
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi equivalent through NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, dev_index=0, period=0.05):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic any4 weights
+# ---------------------------------------------------------------------------
+def synthetic_qtensor(n, k, seed):
+    from paper_2507_04610_b200 import _abi
+    from paper_2507_04610_b200.qtensor import QuantizedTensor
+
+    rng = np.random.default_rng(seed)
+    cfg = _abi.default_config(codebook=_abi.CB_ANY, group_size=GROUP)
+    qt = QuantizedTensor.empty(n, k, cfg)
+    qt.codes[:] = rng.integers(0, 256, qt.codes.size, dtype=np.uint8)
+    # any4 LUTs live in the scaled domain [0, 15], sorted (pack.hpp invariants)
+    lut = np.sort(rng.random((n, 16), dtype=np.float32) * 15.0, axis=1)
+    qt.luts[:] = lut.ravel()
+    qt.alphas[:] = (0.01 + 0.04 * rng.random(qt.alphas.size, dtype=np.float32))
+    qt.betas[:] = -0.3 * rng.random(qt.betas.size, dtype=np.float32)
+    return qt
+
+
+def make_layers(nlayers, shard=(0, 1)):
+    """Device tensors for `nlayers` layers; with shard=(r, P) each tensor holds
+    rows [r*N/P, (r+1)*N/P) of every weight (column-sharded TP)."""
+    from paper_2507_04610_b200 import anyq
+
+    r, P = shard
+    layers = []
+    for l in range(nlayers):
+        mats = []
+        for i, (name, n, k) in enumerate(LAYER):
+            ns = n // P
+            qt = synthetic_qtensor(ns, k, seed=1000 * l + 10 * i + r)
+            mats.append((name, ns, k, anyq.DeviceTensor(qt)))
+        layers.append(mats)
+    return layers
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU)
+# ---------------------------------------------------------------------------
+def reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.refpy import REF_SO, have_ref, oracle, ref
+
+    lib = ref() if have_ref() else oracle()
+    kind = "reference" if have_ref() else "port"
+    threads = os.cpu_count() or 1
+    # one full decoder layer at M=1, rows split over the host threads
+    # (gemm_fused is single-threaded by design, qgemm.cpp:113-126; the split
+    # over output rows is harness parallelism, labelled as such)
+    m = 1
+    work = []
+    for i, (name, n, k) in enumerate(LAYER):
+        qt = synthetic_qtensor(n, k, seed=10 * i)
+        x = np.random.default_rng(i).standard_normal((m, k)).astype(np.float32)
+        parts = []
+        step = (n + threads - 1) // threads
+        for r0 in range(0, n, step):
+            r1 = min(n, r0 + step)
+            sub = qt.clone()
+            sub.rows = r1 - r0
+            bpr = (k * 4 + 7) // 8
+            gpr = (k + GROUP - 1) // GROUP
+            sub.codes = qt.codes[r0 * bpr:r1 * bpr].copy()
+            sub.luts = qt.luts[r0 * 16:r1 * 16].copy()
+            sub.alphas = qt.alphas[r0 * gpr:r1 * gpr].copy()
+            sub.betas = qt.betas[r0 * gpr:r1 * gpr].copy()
+            parts.append(sub)
+        work.append((n, k, x, parts))
+    step_bytes = sum(algo_bytes(n, k, m) for (_, n, k) in LAYER)
+
+    def one_step(pool):
+        futs = [pool.submit(lib.gemm_fused, x, sub) for (n, k, x, parts) in work for sub in parts]
+        for f in futs:
+            f.result()
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        for _ in range(args.warmup):
+            one_step(pool)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(pool)
+        dt = (time.perf_counter() - t0) / args.steps
+    value = step_bytes / dt / 1e9
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dt * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "llama3-8b-layer-gemms", "M": m, "group_size": GROUP,
+                   "shapes": [[n, k] for (_, n, k) in LAYER]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": "one Llama-3-8B layer (7 GEMMs) at M=1, reference gemm_fused "
+                                   f"(qgemm.cpp:71) over {threads} row slices (harness-parallel)",
+                         "library": os.path.relpath(REF_SO, ROOT) if kind == "reference" else
+                         "oracle/_build/liboracle.so"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample():
+    """Reference CPU GEMM on a bounded sample (q-proj shape, M=1, 1 core)."""
+    from oracle.refpy import have_ref, oracle, ref
+
+    lib = ref() if have_ref() else oracle()
+    kind = "reference" if have_ref() else "port"
+    n, k = 4096, 4096
+    qt = synthetic_qtensor(n, k, seed=7)
+    x = np.random.default_rng(1).standard_normal((1, k)).astype(np.float32)
+    secs = lib.time_gemm_fused(x, qt, repeats=5)
+    return {"value": algo_bytes(n, k, 1) / secs / 1e9, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": "reference gemm_fused (qgemm.cpp:71-128, single-threaded by design) on one "
+                      "4096x4096 any4 g128 weight at M=1, median of 5"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_04610_b200 import anyq
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peak, peak_kind = hbm_peak()
+    M = args.m
+    P = world
+    layers = make_layers(args.layers, shard=(rank, P))
+    launches0 = anyq.launch_count()
+
+    # per-layer buffers
+    xs = {k: torch.randn(M, k, device=dev).to(torch.bfloat16) for k in {k for _, _, k in LAYER}}
+    ys = [[torch.empty(M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L] for L in layers]
+    gathered = [[torch.empty(M, ns * P, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L]
+                for L in layers] if P > 1 else None
+    stream = torch.cuda.Stream(dev)
+
+    def run_layer(li, s):
+        for j, (name, ns, k, dt) in enumerate(layers[li]):
+            dt.gemm_ptr(xs[k].data_ptr(), M, ys[li][j].data_ptr(), None, s.cuda_stream)
+            if P > 1:
+                dist.all_gather_into_tensor(gathered[li][j].view(-1), ys[li][j].view(-1))
+
+    # warm-up: first calls configure kernels (cudaFuncSetAttribute) before capture
+    with torch.cuda.stream(stream):
+        for li in range(len(layers)):
+            run_layer(li, stream)
+    torch.cuda.synchronize()
+
+    graphs = None
+    if P == 1:
+        graphs = []
+        for li in range(len(layers)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                run_layer(li, stream)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def step(i):
+        li = i % len(layers)
+        if graphs is not None:
+            graphs[li].replay()
+        else:
+            with torch.cuda.stream(stream):
+                run_layer(li, stream)
+
+    # let the clocks ramp, then the untimed warm-up steps
+    t_end = time.time() + 0.3
+    while time.time() < t_end:
+        with torch.cuda.stream(stream):
+            for i in range(len(layers)):
+                step(i)
+        torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, max over ranks)
+    l0 = anyq.launch_count()
+    if P > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for i in range(args.steps):
+                step(i)
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if P > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    per_step_launches = 2 * len(LAYER)  # x-prep + LUT-GEMM per matrix
+    gpu_launches = per_step_launches * args.steps
+    step_bytes_all = sum(algo_bytes(n, k, M) for (_, n, k) in LAYER)  # whole job (all shards)
+    value = step_bytes_all / (ms * 1e-3) / 1e9
+
+    # ---- e2e through host buffers (pinned), H2D x + D2H y per GEMM, in the timed region
+    xh = {k: torch.randn(M, k).to(torch.bfloat16).pin_memory() for k in xs}
+    yh = [[torch.empty(M, ns, dtype=torch.bfloat16).pin_memory() for (_, ns, _, _) in L] for L in layers]
+    xd = {k: torch.empty(M, k, device=dev, dtype=torch.bfloat16) for k in xs}
+
+    def e2e_layer(li, s):
+        for j, (name, ns, k, dt) in enumerate(layers[li]):
+            xd[k].copy_(xh[k], non_blocking=True)
+            dt.gemm_ptr(xd[k].data_ptr(), M, ys[li][j].data_ptr(), None, s.cuda_stream)
+            yh[li][j].copy_(ys[li][j], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for li in range(len(layers)):
+            e2e_layer(li, stream)
+    torch.cuda.synchronize()
+    e2e_graphs = []
+    if P == 1:
+        for li in range(len(layers)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                e2e_layer(li, stream)
+            e2e_graphs.append(g)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            (e2e_graphs[i % len(layers)].replay() if e2e_graphs else e2e_layer(i % len(layers), stream))
+        e0.record(stream)
+        for i in range(args.steps):
+            (e2e_graphs[i % len(layers)].replay() if e2e_graphs else e2e_layer(i % len(layers), stream))
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if P > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = sum(M * k * 2 for (_, _, k) in LAYER)
+    d2h = sum(M * n * 2 for (_, n, _) in LAYER)
+
+    # ---- per-shape timing (graph of 1 GEMM replayed over the rotating layers)
+    per_shape = {}
+    kernel_ms_total, kernel_bytes_total = 0.0, 0
+    for j, (name, n, k) in enumerate(LAYER):
+        gs = []
+        for li in range(len(layers)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                _, ns, kk, dt = layers[li][j]
+                dt.gemm_ptr(xs[kk].data_ptr(), M, ys[li][j].data_ptr(), None, stream.cuda_stream)
+            gs.append(g)
+        reps = 20 * len(layers)
+        with torch.cuda.stream(stream):
+            for r in range(2 * len(layers)):
+                gs[r % len(gs)].replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for r in range(reps):
+                gs[r % len(gs)].replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / reps * 1e3
+        nb = algo_bytes(n // P, k, M)
+        per_shape[name] = {"N": n // P, "K": k, "us": round(us, 3),
+                           "GBps": round(nb / (us * 1e-6) / 1e9, 1),
+                           "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
+        kernel_ms_total += us * 1e-3
+        kernel_bytes_total += nb
+
+    # ---- M sweep on the q/o shape and gate/up (per-GEMM µs, % HBM peak)
+    sweep = {}
+    if not args.quick and P == 1:
+        for mm in (1, 2, 4, 8, 16):
+            xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in xs}
+            for j, (name, n, k) in enumerate(LAYER):
+                if name not in ("q", "gate", "down"):
+                    continue
+                ym = torch.empty(mm, n, device=dev, dtype=torch.bfloat16)
+                gs = []
+                for li in range(len(layers)):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        layers[li][j][3].gemm_ptr(xm[k].data_ptr(), mm, ym.data_ptr(), None,
+                                                  stream.cuda_stream)
+                    gs.append(g)
+                reps = 10 * len(layers)
+                with torch.cuda.stream(stream):
+                    for r in range(len(layers)):
+                        gs[r % len(gs)].replay()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    for r in range(reps):
+                        gs[r % len(gs)].replay()
+                    b.record(stream)
+                torch.cuda.synchronize()
+                us = a.elapsed_time(b) / reps * 1e3
+                nb = algo_bytes(n, k, mm)
+                sweep[f"{name}_M{mm}"] = {"us": round(us, 3),
+                                          "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
+
+    # ---- k-means quantizer throughput (config 1: 4096x4096 any4 g128, device-resident)
+    kmeans = None
+    if not args.quick and P == 1:
+        from paper_2507_04610_b200 import _abi
+
+        w = torch.randn(4096, 4096, device=dev)
+        cfg = _abi.default_config(codebook=_abi.CB_ANY)
+        anyq.dev_quantize_any(w[:256].contiguous(), cfg)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        anyq.dev_quantize_any(w, cfg)
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        kmeans = {"rows_per_s": round(4096 / secs, 1), "matrix": "4096x4096 gaussian any4 g128",
+                  "seconds": round(secs, 4)}
+
+    roof_achieved = kernel_bytes_total / (kernel_ms_total * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch_q_m1")
+        except Exception:
+            traffic = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_sample()
+        except Exception as e:  # oracle not built on this host
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 2),
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 5),
+            "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None,
+            "dtype": "f16",
+            "data": "synthetic",
+            "config": {
+                "workload": "llama3-8b-layer-gemms (q,k,v,o,gate,up,down) any4 g128",
+                "M": M,
+                "group_size": GROUP,
+                "layers_rotated": args.layers,
+                "l2": f"weights rotate over {args.layers} layers "
+                      f"({args.layers * sum(algo_bytes(n, k, M) for (_, n, k) in LAYER) / 1e6:.0f} MB"
+                      " > 126 MB L2)",
+                "parallelism": f"tp{world} column-sharded + NCCL all-gather" if world > 1 else "single",
+                "graphs": P == 1,
+            },
+            "e2e": {"value": round(step_bytes_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": round(e2e_ms, 5)},
+            "roofline": {"bound": "hbm", "achieved": round(roof_achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(roof_achieved / peak, 4),
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_lutgemm (+k_xprep) per GEMM, per-shape graphs"},
+            "cpu_baseline": cpu,
+            "gpu_launches": gpu_launches,
+            "launches_counted_host": anyq.launch_count() - launches0,
+            "clocks": clk.summary(),
+            "per_shape": per_shape,
+            "m_sweep": sweep,
+            "kmeans": kmeans,
+            "pct_hbm_peak_step": round(100 * value / peak, 2),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    for L in layers:
+        for (_, _, _, dt) in L:
+            dt.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--quick", action="store_true", help="skip the M sweep and k-means extras")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()
