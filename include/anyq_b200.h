@@ -184,6 +184,14 @@ anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
                                int64_t m, void* y_bf16, float* y_f32,
                                void* stream);
 
+/* Same, with the kernel chosen explicitly (tests and the M sweep):
+ *   ANYQ_PATH_GEMV  CUDA-core LUT GEMV, m <= 4 (gemv.cu)
+ *   ANYQ_PATH_TC    tensor-core (tcgen05, A in TMEM) LUT GEMM, m <= 16
+ *   ANYQ_PATH_AUTO  the faster of the two for m (what anyq_dev_gemm_bf16 uses) */
+enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2 };
+anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
+                                    void* y_bf16, float* y_f32, int32_t path, void* stream);
+
 /* Device quantize: rows [row_offset, row_offset+rows) of a matrix, fp32 in,
  * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device. */
 anyq_status anyq_dev_quantize_any(const float* w_dev, int64_t rows, int64_t cols,

@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
         "anyq_dev_tensor_rows": (i64, [vp]),
         "anyq_dev_tensor_cols": (i64, [vp]),
         "anyq_dev_gemm_bf16": (st, [vp, vp, i64, vp, vp, vp]),
+        "anyq_dev_gemm_bf16_path": (st, [vp, vp, i64, vp, vp, i32, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -145,7 +146,7 @@ EXPORTED_SYMBOLS = (
     "anyq_unpack_codes", "anyq_ktile_codes", "anyq_narrow_inplace", "anyq_dequantize",
     "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
     "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
-    "anyq_dev_gemm_bf16", "anyq_dev_quantize_any", "anyq_launch_count",
+    "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_quantize_any", "anyq_launch_count",
 )
 
 
@@ -342,7 +343,8 @@ def gemm_fused(x, qt: QuantizedTensor, plan: GemmPlan | None = None) -> np.ndarr
 
 
 # ---------------------------------------------------------------------------
-# device-resident fast path (tensor-core LUT GEMM)
+# device-resident fast path (LUT GEMV / tensor-core LUT GEMM)
+PATH_AUTO, PATH_GEMV, PATH_TC = 0, 1, 2
 # ---------------------------------------------------------------------------
 class DeviceTensor:
     """A prepacked any4/int4/nf4/fp4 weight resident in HBM.
@@ -370,12 +372,13 @@ class DeviceTensor:
         except Exception:
             pass
 
-    def gemm_ptr(self, x_ptr: int, m: int, y_ptr: int, y32_ptr: int | None, stream: int):
-        _check(lib().anyq_dev_gemm_bf16(self._h, C.c_void_p(x_ptr), m, C.c_void_p(y_ptr),
-                                        C.c_void_p(y32_ptr) if y32_ptr else None,
-                                        C.c_void_p(stream)))
+    def gemm_ptr(self, x_ptr: int, m: int, y_ptr: int, y32_ptr: int | None, stream: int,
+                 path: int = 0):
+        _check(lib().anyq_dev_gemm_bf16_path(self._h, C.c_void_p(x_ptr), m, C.c_void_p(y_ptr),
+                                             C.c_void_p(y32_ptr) if y32_ptr else None, path,
+                                             C.c_void_p(stream)))
 
-    def gemm(self, x, y=None, y32=None, stream=None):
+    def gemm(self, x, y=None, y32=None, stream=None, path: int = 0):
         import torch
 
         assert x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous()
@@ -386,7 +389,7 @@ class DeviceTensor:
             y = torch.empty((m, self.rows), dtype=torch.bfloat16, device=x.device)
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         self.gemm_ptr(x.data_ptr(), m, y.data_ptr(), y32.data_ptr() if y32 is not None else None,
-                      s.cuda_stream)
+                      s.cuda_stream, path)
         return y
 
 

@@ -485,16 +485,29 @@ int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t) {
   return reinterpret_cast<const LutTensor*>(t)->cols;
 }
 
+anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
+                                    void* y_bf16, float* y_f32, int32_t path, void* stream) {
+  return guard([&] {
+    const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
+    if (path == ANYQ_PATH_AUTO)
+      path = (m <= 1 && lt && lt->gv_gshift >= 0) ? ANYQ_PATH_GEMV : ANYQ_PATH_TC;
+    if (path == ANYQ_PATH_GEMV)
+      lutgemv_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_TC)
+      lutgemm_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
+    else
+      fail(ANYQ_ERR_CONFIG, "unknown GEMM path");
+  });
+}
+
 anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                void* y_bf16, float* y_f32, void* stream) {
-  return guard([&] {
-    lutgemm_run(reinterpret_cast<const LutTensor*>(t), x_bf16, m, y_bf16, y_f32,
-                (cudaStream_t)stream);
-  });
+  return anyq_dev_gemm_bf16_path(t, x_bf16, m, y_bf16, y_f32, ANYQ_PATH_AUTO, stream);
 }
 
 // Debug hook (not part of the reference interface): record a per-CTA
 // globaltimer timeline of the tensor-core GEMM into dev ([ncta][16] int64).
 void anyq_debug_set_trace(long long* dev) { lutgemm_set_trace(dev); }
+void anyq_debug_set_gemv_trace(long long* dev) { lutgemv_set_trace(dev); }
 
 }  // extern "C"

@@ -856,6 +856,7 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
     ANYQ_CUDA(cudaMalloc(&t->part, sizeof(float) * (size_t)t->RB * cmax * kMaxMP * 32));
     ANYQ_CUDA(cudaMalloc(&t->counters, sizeof(int) * t->RB));
     ANYQ_CUDA(cudaMemset(t->counters, 0, sizeof(int) * t->RB));
+    lutgemv_setup(t);
   } catch (...) {
     lutgemm_destroy(t);
     throw;
@@ -875,6 +876,9 @@ void lutgemm_destroy(LutTensor* t) {
   cudaFree(t->xsum);
   cudaFree(t->part);
   cudaFree(t->counters);
+  cudaFree(t->gv_part);
+  cudaFree(t->gv_counters);
+  cudaFree(t->gv_err);
   delete t;
 }
 

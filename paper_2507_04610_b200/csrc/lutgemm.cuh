@@ -26,11 +26,21 @@ struct LutTensor {
   int* counters = nullptr; // [RB]
   int cmax = 0;
   int sms = 148;
+  // CUDA-core GEMV (gemv.cu) work split + workspace
+  float* gv_part = nullptr;   // [RB - gv_rbA][gv_cmax][4][32]
+  int* gv_counters = nullptr; // [RB - gv_rbA]
+  int* gv_err = nullptr;      // device error word of the GEMV
+  int gv_ncta = 0, gv_fullA = 0, gv_rbA = 0, gv_cmax = 1, gv_gshift = -1;
 };
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt);
 void lutgemm_destroy(LutTensor* t);
 void lutgemm_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
+// K1a CUDA-core GEMV (m <= 4) over the same prepacked tensor (gemv.cu).
+void lutgemv_setup(LutTensor* t);
+void lutgemv_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
+void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
+                 cudaStream_t s);
 void lutgemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
 

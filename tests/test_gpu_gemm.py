@@ -2,7 +2,9 @@
 
 * anyq_gemm_fused (exact path): bit-identical to the reference gemm_fused /
   gemm_reference for every format, layout and M (test_qgemm.cpp:53-160).
-* tensor-core LUT GEMM (device path, bf16 x, fp32 accumulate): within
+* device LUT GEMM paths (bf16 x, exact fp16 x fp16 products, fp32
+  accumulation): the CUDA-core GEMV (m <= 4, gemv.cu) and the tcgen05 LUT GEMM
+  (m <= 16, lutgemm.cu), each within
   |dy| <= 1e-5 * sum_j |x_j| * (|alpha*T| + |beta|) of
   gemm_reference(bf16(x), narrowed(qt)) computed by the oracle in fp32.
 """
@@ -105,14 +107,17 @@ def bf16(x):
     return bf16_round(x)
 
 
-def tc_gemm(aq, cuda, qt, x):
+PATHS = {"gemv": 1, "tc": 2}
+
+
+def tc_gemm(aq, cuda, qt, x, path=2):
     import torch
 
     dt = aq.DeviceTensor(qt)
     xt = torch.from_numpy(bf16(x)).to("cuda", torch.bfloat16).contiguous()
     y = torch.empty((x.shape[0], qt.rows), dtype=torch.bfloat16, device="cuda")
     y32 = torch.empty((x.shape[0], qt.rows), dtype=torch.float32, device="cuda")
-    dt.gemm(xt, y, y32)
+    dt.gemm(xt, y, y32, path=path)
     torch.cuda.synchronize()
     out = y32.cpu().numpy(), y.float().cpu().numpy()
     dt.close()
@@ -138,16 +143,19 @@ def tc_tolerance(orc, x, qt):
     return tol + 1e-30
 
 
+@pytest.mark.parametrize("path", ["gemv", "tc"])
 @pytest.mark.parametrize("fmt", ["any4", "int4", "nf4", "fp4"])
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8, 9, 16])
-def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m):
+def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m, path):
+    if path == "gemv" and m > 4:
+        pytest.skip("the GEMV serves m <= 4")
     n, k = 200, 384  # ragged rows (not a multiple of 32), 3 chunks, 3 groups
     w = orc.gaussian(n, k, 31)
     c = cfg(granularity=3, group_size=128, seed=2)
     aq.apply_format(c, fmt)
     qt = orc.quantize(w, c)
     x = bf16(orc.gaussian(m, k, 33))
-    y32, ybf = tc_gemm(aq, cuda, qt, x)
+    y32, ybf = tc_gemm(aq, cuda, qt, x, PATHS[path])
     ref = orc.gemm_reference(x, orc.narrowed(qt))
     tol = tc_tolerance(orc, x, qt)
     err = np.abs(y32 - ref)
@@ -155,28 +163,46 @@ def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m):
     assert np.all(np.abs(ybf - bf16(ref)) <= np.abs(ref) * 2 ** -7 + tol)
 
 
+@pytest.mark.parametrize("path", ["gemv", "tc"])
 @pytest.mark.parametrize("n,k,g", [(4096, 4096, 128), (1024, 4096, 128), (4096, 1024, 256),
-                                   (96, 1280, 1280), (33, 128, 128)])
-def test_tc_gemm_shapes(aq, orc, cuda, n, k, g):
+                                   (96, 1280, 1280), (33, 128, 128),
+                                   # GEMV work split: 151 row blocks (one full wave +
+                                   # 3 split over 148 CTAs, some with empty ranges)
+                                   (151 * 32 - 5, 512, 128)])
+def test_tc_gemm_shapes(aq, orc, cuda, n, k, g, path):
     w = orc.gaussian(n, k, 41)
     gran = 1 if g == k else 3
     c = cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=8)
     qt = aq.quantize_any(w, c)
     x = bf16(orc.gaussian(3, k, 43))
-    y32, _ = tc_gemm(aq, cuda, qt, x)
+    y32, _ = tc_gemm(aq, cuda, qt, x, PATHS[path])
     ref = orc.gemm_reference(x, orc.narrowed(qt))
     tol = tc_tolerance(orc, x, qt)
     assert np.all(np.abs(y32 - ref) <= tol)
 
 
-def test_tc_gemm_is_deterministic_and_rowwise_consistent(aq, orc, cuda):
+@pytest.mark.parametrize("path", ["gemv", "tc"])
+def test_tc_gemm_is_deterministic_and_rowwise_consistent(aq, orc, cuda, path):
     w = orc.gaussian(512, 1024, 5)
     qt = aq.quantize_any(w, cfg(codebook=3, max_iters=5))
     x1 = bf16(orc.gaussian(1, 1024, 6))
-    x16 = np.repeat(x1, 16, axis=0)
-    a, _ = tc_gemm(aq, cuda, qt, x1)
-    b, _ = tc_gemm(aq, cuda, qt, x1)
-    c, _ = tc_gemm(aq, cuda, qt, x16)
+    mm = 4 if path == "gemv" else 16
+    xm = np.repeat(x1, mm, axis=0)
+    a, _ = tc_gemm(aq, cuda, qt, x1, PATHS[path])
+    b, _ = tc_gemm(aq, cuda, qt, x1, PATHS[path])
+    c, _ = tc_gemm(aq, cuda, qt, xm, PATHS[path])
     assert bits_equal(a, b)
-    for r in range(16):
+    for r in range(mm):
         assert np.allclose(c[r], a[0], rtol=0, atol=1e-5 * np.abs(a[0]).max())
+
+
+def test_gemv_rejects_unsupported_group(aq, orc, cuda):
+    """group_size 384 is not 128 * 2^j: the GEMV refuses, AUTO falls back to tcgen05."""
+    w = orc.gaussian(64, 768, 3)
+    qt = aq.quantize_any(w, cfg(codebook=3, group_size=384, max_iters=3))
+    x = bf16(orc.gaussian(1, 768, 4))
+    with pytest.raises(aq.ConfigError):
+        tc_gemm(aq, cuda, qt, x, PATHS["gemv"])
+    y32, _ = tc_gemm(aq, cuda, qt, x, 0)
+    ref = orc.gemm_reference(x, orc.narrowed(qt))
+    assert np.all(np.abs(y32 - ref) <= tc_tolerance(orc, x, qt))
