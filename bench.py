@@ -5,14 +5,16 @@ Headline (BASELINE.json metric "any4 GEMM µs and % HBM peak at M=1–16 (Llama-
 shapes); k-means rows/s", config[1] "Llama-3-8B layer shapes ... M=1..16"):
 
   step   = the seven Llama-3-8B decoder-layer GEMMs (q,k,v,o,gate,up,down) at
-           M=1 on any4 g128 weights, y = x W^T, bf16 x/y, tensor-core LUT path.
-           Weights rotate over LAYERS layers (> L2), so every step streams its
-           weights from HBM. CUDA graphs remove host launch overhead.
+           M=1 on any4 g128 weights, y = x W^T, bf16 x/y, with the decoder's
+           data dependencies (o reads y_q, gate/up read y_o, down reads y_up),
+           as ONE k_lutgemv chain launch per layer. Weights rotate over LAYERS
+           layers (> L2), so every step streams its weights from HBM. CUDA
+           graphs remove host launch overhead.
   value  = algorithmic bytes streamed per step / device time per step (GB/s),
            whole job over all ranks.
-  e2e    = same metric through the public API with HOST buffers: every GEMM's
-           x is copied H2D from pinned memory and y copied back D2H inside the
-           timed region.
+  e2e    = same metric through the public API with HOST buffers: the layer
+           input is copied H2D from pinned memory and all seven outputs D2H
+           inside the timed region, every step.
   extras = per-shape µs and % of HBM peak, the M=1..16 sweep, k-means rows/s
            (config 1), roofline of the dominant kernel, CPU baseline.
 
@@ -253,6 +255,14 @@ def cpu_baseline_sample():
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+# decoder-layer dependency pattern over LAYER = (q, k, v, o, gate, up, down):
+# q,k,v read the layer input; o reads y_q; gate/up read y_o; down reads y_up
+# (the GEMMs of a Llama decoder layer with the non-GEMM ops between them elided)
+X_SRC = [-1, -1, -1, 0, 3, 3, 5]
+WAITS = [0, 0, 0, 1, 1, 0, 1]
+BATCHES = [[0, 1, 2], [3], [4, 5], [6]]
+
+
 def gpu_arm(args):
     import torch
     import torch.distributed as dist
@@ -269,24 +279,44 @@ def gpu_arm(args):
     P = world
     layers = make_layers(args.layers, shard=(rank, P))
     launches0 = anyq.launch_count()
-
-    # per-layer buffers
-    xs = {k: torch.randn(M, k, device=dev).to(torch.bfloat16) for k in {k for _, _, k in LAYER}}
-    ys = [[torch.empty(M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L] for L in layers]
-    gathered = [[torch.empty(M, ns * P, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L]
-                for L in layers] if P > 1 else None
+    use_chain = M <= 2  # CUDA-core GEMV chain; larger M runs the tcgen05 path per GEMM
     stream = torch.cuda.Stream(dev)
 
-    def run_layer(li, s):
-        for j, (name, ns, k, dt) in enumerate(layers[li]):
-            dt.gemm_ptr(xs[k].data_ptr(), M, ys[li][j].data_ptr(), None, s.cuda_stream)
-            if P > 1:
-                dist.all_gather_into_tensor(gathered[li][j].view(-1), ys[li][j].view(-1))
+    # buffers: layer input x, per-layer local y shards, gathered y (TP)
+    x_in = torch.randn(M, 4096, device=dev).to(torch.bfloat16)
+    ys = [[torch.empty(M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L] for L in layers]
+    yg = [[torch.empty(M, ns * P, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L]
+          for L in layers] if P > 1 else None
 
-    # warm-up: first calls configure kernels (cudaFuncSetAttribute) before capture
+    def x_of(li, j):
+        src = X_SRC[j]
+        if src < 0:
+            return x_in
+        return yg[li][src] if P > 1 else ys[li][src]
+
+    def run_layer(li, s):
+        L = layers[li]
+        if P == 1 and use_chain:
+            anyq.gemm_chain_ptrs([d for (_, _, _, d) in L], [x_of(li, j).data_ptr() for j in range(7)],
+                                 [y.data_ptr() for y in ys[li]], M, s.cuda_stream, WAITS)
+            return
+        for bt in BATCHES:  # TP: one launch per batch, all-gather of the slices read next
+            if use_chain:
+                anyq.gemm_chain_ptrs([L[j][3] for j in bt], [x_of(li, j).data_ptr() for j in bt],
+                                     [ys[li][j].data_ptr() for j in bt], M, s.cuda_stream)
+            else:
+                for j in bt:
+                    L[j][3].gemm_ptr(x_of(li, j).data_ptr(), M, ys[li][j].data_ptr(), None, s.cuda_stream)
+            if P > 1:
+                for j in bt:
+                    dist.all_gather_into_tensor(yg[li][j], ys[li][j].contiguous())
+
+    # warm-up (configures kernels) + launches per step
     with torch.cuda.stream(stream):
         for li in range(len(layers)):
+            c0 = anyq.launch_count()
             run_layer(li, stream)
+            per_step_launches = anyq.launch_count() - c0
     torch.cuda.synchronize()
 
     graphs = None
@@ -304,8 +334,7 @@ def gpu_arm(args):
         if graphs is not None:
             graphs[li].replay()
         else:
-            with torch.cuda.stream(stream):
-                run_layer(li, stream)
+            run_layer(li, stream)
 
     # let the clocks ramp, then the untimed warm-up steps
     t_end = time.time() + 0.3
@@ -320,7 +349,6 @@ def gpu_arm(args):
     torch.cuda.synchronize()
 
     # ---- timed region (device time, max over ranks)
-    l0 = anyq.launch_count()
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -337,41 +365,37 @@ def gpu_arm(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    per_step_launches = 2 * len(LAYER)  # x-prep + LUT-GEMM per matrix
     gpu_launches = per_step_launches * args.steps
     step_bytes_all = sum(algo_bytes(n, k, M) for (_, n, k) in LAYER)  # whole job (all shards)
     value = step_bytes_all / (ms * 1e-3) / 1e9
 
-    # ---- e2e through host buffers (pinned), H2D x + D2H y per GEMM, in the timed region
-    xh = {k: torch.randn(M, k).to(torch.bfloat16).pin_memory() for k in xs}
-    yh = [[torch.empty(M, ns, dtype=torch.bfloat16).pin_memory() for (_, ns, _, _) in L] for L in layers]
-    xd = {k: torch.empty(M, k, device=dev, dtype=torch.bfloat16) for k in xs}
+    # ---- e2e through the public API with host buffers: H2D of the layer input
+    # (pinned) + D2H of all seven outputs, every step, inside the timed region
+    xh = torch.randn(M, 4096).to(torch.bfloat16).pin_memory()
+    yh = [[torch.empty(M, ns * P, dtype=torch.bfloat16).pin_memory() for (_, ns, _, _) in L]
+          for L in layers]
 
-    def e2e_layer(li, s):
-        for j, (name, ns, k, dt) in enumerate(layers[li]):
-            xd[k].copy_(xh[k], non_blocking=True)
-            dt.gemm_ptr(xd[k].data_ptr(), M, ys[li][j].data_ptr(), None, s.cuda_stream)
-            yh[li][j].copy_(ys[li][j], non_blocking=True)
+    def e2e_step(i, s):
+        li = i % len(layers)
+        x_in.copy_(xh, non_blocking=True)
+        if graphs is not None:
+            graphs[li].replay()
+        else:
+            run_layer(li, s)
+        for j in range(7):
+            yh[li][j].copy_(yg[li][j] if P > 1 else ys[li][j], non_blocking=True)
 
-    with torch.cuda.stream(stream):
-        for li in range(len(layers)):
-            e2e_layer(li, stream)
-    torch.cuda.synchronize()
-    e2e_graphs = []
-    if P == 1:
-        for li in range(len(layers)):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                e2e_layer(li, stream)
-            e2e_graphs.append(g)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            (e2e_graphs[i % len(layers)].replay() if e2e_graphs else e2e_layer(i % len(layers), stream))
+            e2e_step(i, stream)
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
         e0.record(stream)
         for i in range(args.steps):
-            (e2e_graphs[i % len(layers)].replay() if e2e_graphs else e2e_layer(i % len(layers), stream))
+            e2e_step(i, stream)
         e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -379,65 +403,54 @@ def gpu_arm(args):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    h2d = sum(M * k * 2 for (_, _, k) in LAYER)
+    h2d = M * 4096 * 2
     d2h = sum(M * n * 2 for (_, n, _) in LAYER)
 
-    # ---- per-shape timing (graph of 1 GEMM replayed over the rotating layers)
-    per_shape = {}
-    kernel_ms_total, kernel_bytes_total = 0.0, 0
-    for j, (name, n, k) in enumerate(LAYER):
-        gs = []
-        for li in range(len(layers)):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                _, ns, kk, dt = layers[li][j]
-                dt.gemm_ptr(xs[kk].data_ptr(), M, ys[li][j].data_ptr(), None, stream.cuda_stream)
-            gs.append(g)
-        reps = 20 * len(layers)
+    # ---- per-shape single-GEMM timing (graph of the rotated layers' copies)
+    def time_graph(fn, reps):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
         with torch.cuda.stream(stream):
-            for r in range(2 * len(layers)):
-                gs[r % len(gs)].replay()
+            for _ in range(2):
+                g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            for r in range(reps):
-                gs[r % len(gs)].replay()
+            for _ in range(reps):
+                g.replay()
             b.record(stream)
         torch.cuda.synchronize()
-        us = a.elapsed_time(b) / reps * 1e3
-        nb = algo_bytes(n // P, k, M)
-        per_shape[name] = {"N": n // P, "K": k, "us": round(us, 3),
-                           "GBps": round(nb / (us * 1e-6) / 1e9, 1),
-                           "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
-        kernel_ms_total += us * 1e-3
-        kernel_bytes_total += nb
+        return a.elapsed_time(b) / reps * 1e3  # us per replay
 
-    # ---- M sweep on the q/o shape and gate/up (per-GEMM µs, % HBM peak)
+    per_shape = {}
+    xk = {4096: x_in, 14336: torch.randn(M, 14336, device=dev).to(torch.bfloat16)}
+    if P == 1:
+        for j, (name, n, k) in enumerate(LAYER):
+            def one():
+                for li in range(len(layers)):
+                    layers[li][j][3].gemm_ptr(xk[k].data_ptr(), M, ys[li][j].data_ptr(), None,
+                                              stream.cuda_stream)
+            us = time_graph(one, 20) / len(layers)
+            nb = algo_bytes(n, k, M)
+            per_shape[name] = {"N": n, "K": k, "us": round(us, 3),
+                               "GBps": round(nb / (us * 1e-6) / 1e9, 1),
+                               "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
+
+    # ---- M sweep (per-GEMM launches, AUTO path: GEMV for m = 1, tcgen05 above)
     sweep = {}
     if not args.quick and P == 1:
         for mm in (1, 2, 4, 8, 16):
-            xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in xs}
+            xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in (4096, 14336)}
             for j, (name, n, k) in enumerate(LAYER):
                 if name not in ("q", "gate", "down"):
                     continue
                 ym = torch.empty(mm, n, device=dev, dtype=torch.bfloat16)
-                gs = []
-                for li in range(len(layers)):
-                    g = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g, stream=stream):
+
+                def one():
+                    for li in range(len(layers)):
                         layers[li][j][3].gemm_ptr(xm[k].data_ptr(), mm, ym.data_ptr(), None,
                                                   stream.cuda_stream)
-                    gs.append(g)
-                reps = 10 * len(layers)
-                with torch.cuda.stream(stream):
-                    for r in range(len(layers)):
-                        gs[r % len(gs)].replay()
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                    for r in range(reps):
-                        gs[r % len(gs)].replay()
-                    b.record(stream)
-                torch.cuda.synchronize()
-                us = a.elapsed_time(b) / reps * 1e3
+                us = time_graph(one, 10) / len(layers)
                 nb = algo_bytes(n, k, mm)
                 sweep[f"{name}_M{mm}"] = {"us": round(us, 3),
                                           "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
@@ -458,13 +471,15 @@ def gpu_arm(args):
         kmeans = {"rows_per_s": round(4096 / secs, 1), "matrix": "4096x4096 gaussian any4 g128",
                   "seconds": round(secs, 4)}
 
-    roof_achieved = kernel_bytes_total / (kernel_ms_total * 1e-3) / 1e9
+    # roofline of the dominant kernel: the step IS one k_lutgemv chain launch per
+    # layer at M=1 (P=1), so its launch duration is the step time
+    roof_achieved = value
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch_q_m1")
+                traffic = json.load(f).get("dram_bytes_per_launch_layer_chain")
         except Exception:
             traffic = None
     cpu = None
@@ -489,14 +504,18 @@ def gpu_arm(args):
             "dtype": "f16",
             "data": "synthetic",
             "config": {
-                "workload": "llama3-8b-layer-gemms (q,k,v,o,gate,up,down) any4 g128",
+                "workload": "llama3-8b decoder-layer GEMMs (q,k,v,o,gate,up,down) any4 g128, "
+                            "decoder data dependencies (o<-q, gate/up<-o, down<-up)",
                 "M": M,
                 "group_size": GROUP,
                 "layers_rotated": args.layers,
                 "l2": f"weights rotate over {args.layers} layers "
                       f"({args.layers * sum(algo_bytes(n, k, M) for (_, n, k) in LAYER) / 1e6:.0f} MB"
                       " > 126 MB L2)",
-                "parallelism": f"tp{world} column-sharded + NCCL all-gather" if world > 1 else "single",
+                "launch": ("one k_lutgemv chain launch per layer" if (use_chain and P == 1) else
+                           "one launch per dependency batch" if use_chain else "one launch per GEMM"),
+                "parallelism": f"tp{world} row-sharded W + NCCL all-gather per batch" if world > 1
+                else "single",
                 "graphs": P == 1,
             },
             "e2e": {"value": round(step_bytes_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": UNIT,
@@ -505,7 +524,8 @@ def gpu_arm(args):
             "roofline": {"bound": "hbm", "achieved": round(roof_achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(roof_achieved / peak, 4),
                          "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_lutgemm (+k_xprep) per GEMM, per-shape graphs"},
+                         "kernel": "k_lutgemv chain (one launch = one decoder layer, 117.4 MB "
+                                   "algorithmic bytes at M=1), CUDA events on its stream"},
             "cpu_baseline": cpu,
             "gpu_launches": gpu_launches,
             "launches_counted_host": anyq.launch_count() - launches0,

@@ -185,12 +185,24 @@ anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
                                void* stream);
 
 /* Same, with the kernel chosen explicitly (tests and the M sweep):
- *   ANYQ_PATH_GEMV  CUDA-core LUT GEMV, m <= 4 (gemv.cu)
+ *   ANYQ_PATH_GEMV  CUDA-core LUT GEMV, m <= 2 (gemv.cu)
  *   ANYQ_PATH_TC    tensor-core (tcgen05, A in TMEM) LUT GEMM, m <= 16
  *   ANYQ_PATH_AUTO  the faster of the two for m (what anyq_dev_gemm_bf16 uses) */
 enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2 };
 anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                     void* y_bf16, float* y_f32, int32_t path, void* stream);
+
+/* A chain of small-M GEMMs in ONE persistent launch (e.g. the projections of a
+ * decoder layer): y_i[m x rows_i] = x_i[m x cols_i] * dequant(W_i)^T for
+ * i < n (n <= 8, the same 1 <= m <= 2 for all; CUDA-core GEMV path). Problem
+ * i > 0 with wait_prev[i] != 0 reads x_i only after every earlier problem has
+ * completed grid-wide, so x_i may be (or depend on) an earlier y_j; the
+ * weights of later problems stream in while it waits. y32 may be NULL (or any
+ * entry of it). A tensor may appear once per chain. */
+anyq_status anyq_dev_gemm_chain(int32_t n, const anyq_dev_tensor* const* t,
+                                const void* const* x_bf16, void* const* y_bf16,
+                                float* const* y_f32, const int32_t* wait_prev, int64_t m,
+                                void* stream);
 
 /* Device quantize: rows [row_offset, row_offset+rows) of a matrix, fp32 in,
  * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device. */

@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
         "anyq_dev_tensor_cols": (i64, [vp]),
         "anyq_dev_gemm_bf16": (st, [vp, vp, i64, vp, vp, vp]),
         "anyq_dev_gemm_bf16_path": (st, [vp, vp, i64, vp, vp, i32, vp]),
+        "anyq_dev_gemm_chain": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                     C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -146,7 +148,8 @@ EXPORTED_SYMBOLS = (
     "anyq_unpack_codes", "anyq_ktile_codes", "anyq_narrow_inplace", "anyq_dequantize",
     "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
     "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
-    "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_quantize_any", "anyq_launch_count",
+    "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
+    "anyq_dev_quantize_any", "anyq_launch_count",
 )
 
 
@@ -391,6 +394,36 @@ class DeviceTensor:
         self.gemm_ptr(x.data_ptr(), m, y.data_ptr(), y32.data_ptr() if y32 is not None else None,
                       s.cuda_stream, path)
         return y
+
+
+def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None, y32_ptrs=None):
+    """One launch of y_i = x_i W_i^T for a list of DeviceTensors (anyq_dev_gemm_chain).
+
+    wait_prev[i] = 1 makes problem i read x_i only after all earlier problems
+    completed (x_i may be an earlier y). Pointers are raw device addresses.
+    """
+    n = len(tensors)
+    VP = C.c_void_p * n
+    t = VP(*[d._h.value for d in tensors])
+    xs = VP(*x_ptrs)
+    ys = VP(*y_ptrs)
+    y32 = VP(*[p or 0 for p in y32_ptrs]) if y32_ptrs is not None else None
+    w = (C.c_int32 * n)(*(wait_prev or [0] * n))
+    _check(lib().anyq_dev_gemm_chain(n, t, xs, ys, y32, w, m, C.c_void_p(stream)))
+
+
+def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None):
+    """gemm_chain_ptrs on torch CUDA tensors; returns the list of y (bf16)."""
+    import torch
+
+    m = xs[0].shape[0]
+    if ys is None:
+        ys = [torch.empty((m, d.rows), dtype=torch.bfloat16, device=xs[0].device) for d in tensors]
+    s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
+    gemm_chain_ptrs(tensors, [x.data_ptr() for x in xs], [y.data_ptr() for y in ys], m,
+                    s.cuda_stream, wait_prev,
+                    [y.data_ptr() for y in y32s] if y32s is not None else None)
+    return ys
 
 
 def dev_quantize_any(w, cfg: Config, exj=None, row_offset: int = 0, stream=None):

@@ -500,6 +500,17 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
   });
 }
 
+anyq_status anyq_dev_gemm_chain(int32_t n, const anyq_dev_tensor* const* t,
+                                const void* const* x_bf16, void* const* y_bf16,
+                                float* const* y_f32, const int32_t* wait_prev, int64_t m,
+                                void* stream) {
+  return guard([&] {
+    if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
+    lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32,
+                      wait_prev, m, (cudaStream_t)stream);
+  });
+}
+
 anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                void* y_bf16, float* y_f32, void* stream) {
   return anyq_dev_gemm_bf16_path(t, x_bf16, m, y_bf16, y_f32, ANYQ_PATH_AUTO, stream);

@@ -1,4 +1,4 @@
-// K1a — CUDA-core any4 LUT GEMV for M <= 4 (the memory-bound decode path), sm_100a.
+// K1a — CUDA-core any4 LUT GEMV for M <= 2 (the memory-bound decode path), sm_100a.
 //
 //   y[m][n] = sum_k x[m][k] * (alpha[n][g(k)] * T_n[c[n][k]] + beta[n][g(k)])
 //
@@ -11,31 +11,39 @@
 // fp32, so the result differs from the fp32 reference only by summation order
 // (tolerance 1e-5 * sum|x*w|, tests/test_gpu_gemm.py).
 //
-// Data path (one persistent CTA of 16 warps per SM):
-//  * lane L of every warp owns row L of a 32-row block. The unit of work is a
-//    chunk = 32 rows x 128 k = 2 KB contiguous in the prepacked code tensor
-//    (layout of lutgemm.cu: [RB][C][4 slabs][32 rows][16 B]); a warp reads it
-//    with 4 coalesced LDG.128 (512 B each) and keeps two chunks in flight in
-//    registers (no shared-memory staging: the smem crossbar is the second
-//    tightest resource after HBM).
+// One persistent CTA per SM: 16 compute warps + 1 writer warp.
+//  * Work items are whole 32-row blocks. A launch runs a chain of GEMMs split
+//    into batches (runs of problems without a dependency); the row blocks of a
+//    batch, concatenated in problem order, are dealt round-robin to the CTAs.
+//    An item is computed by one CTA only, so y needs no cross-CTA combine and
+//    the result is deterministic.
+//  * Inside a CTA the 16 compute warps split the item's 128-k chunks; lane L
+//    of every warp owns row L. A chunk = 32 rows x 128 k = 2 KB contiguous in
+//    the prepacked code tensor (layout of lutgemm.cu: [RB][C][4 slabs][32 rows]
+//    [16 B]). Each warp streams its own chunks with cp.async.bulk into a
+//    private 2-slot shared-memory ring (the L1 load queue stays free for the
+//    latency-critical LUT / x traffic).
 //  * LUT lookup: the row's 16 fp16 values are expanded once per row block into
 //    a 256-entry pair table T2[byte] = (T[lo], T[hi]); entry e of lane L lives
 //    at shared address 0x10000 + e*256 + buf*128 + L*4. Every lookup of a warp
 //    hits bank L (conflict free), the address is ONE prmt of the code byte into
 //    the lane word (no add: the table is 64 KB aligned in the shared window),
-//    and ONE LDS dequantises two weights. buf 0/1 double-buffer consecutive
-//    row blocks.
-//  * x enters once per CTA as the permuted fp16 image the code bytes index,
-//    plus per-chunk (2^-e, sum x), in shared memory.
-//  * Work split: whole row blocks round-robin over CTAs ("phase A"); the
-//    remaining RB mod ncta row blocks are split by chunk over all CTAs ("phase
-//    B", each CTA range spans <= 2 row blocks). Inside a CTA each row-block
-//    segment is divided evenly over the 16 warps; warp partials are reduced in
-//    shared memory in a fixed order and row blocks split over CTAs are combined
-//    in slot order by the last-arriving CTA: deterministic.
-//  * Programmatic dependent launch: codes, LUT and the first table are fetched
-//    before griddepcontrol.wait, overlapping the previous kernel's tail.
+//    and ONE LDS dequantises two weights. Two buffers, handed between warps
+//    with mbarriers (warps drift by up to one item instead of meeting at a CTA
+//    barrier).
+//  * x enters once per batch: raw bf16 rows by cp.async.bulk, converted in
+//    place to the permuted fp16 image the code bytes index, plus per-chunk
+//    (2^-e, sum x). Problems of a batch that read the same x share the image.
+//  * The writer warp reduces the 16 warp partials of an item in a fixed order
+//    and stores y; after a batch it releases it grid-wide (done[batch end]).
+//    A dependent problem reads its x only after every CTA released the batch
+//    before it, so x_i may be an earlier y_j; its weights already stream in.
+//    The grid is co-resident (cooperative launch), so the waits cannot
+//    deadlock.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
+#include <string>
 
 #include "kernels.cuh"
 #include "lutgemm.cuh"
@@ -44,52 +52,51 @@ namespace anyq_b200 {
 
 namespace {
 
-constexpr int kW = 16;  // warps per CTA (piece split uses >> 4)
-constexpr int kT = kW * 32;
-constexpr int kMaxMP = 4;
+constexpr int kW = 16;                // compute warps per CTA
+constexpr int kT = (kW + 1) * 32;     // + one writer warp
+constexpr int kMaxMP = 2;
+constexpr int kRing = 2;              // TMA ring slots (2-KB chunks) per compute warp
+constexpr int kMaxProb = 8;
 constexpr uint32_t kTblAddr = 0x10000;  // shared-window address of the pair table
 constexpr uint32_t kDynBase = 0x400;    // shared-window address of dynamic smem (sm_100)
 constexpr uint32_t kPre = kTblAddr - kDynBase;  // bytes of dynamic smem before the table
 constexpr uint32_t kTblBytes = 0x10000;
+constexpr uint32_t kSmemMax = 227u * 1024u;
+constexpr uint32_t kParamOff = 0;     // dynamic-smem copy of the parameter block
 
-// Shared-memory layout (offsets into dynamic smem). The small arrays live in
-// the 63 KB in front of the table when they fit, else behind it.
-template <int MP>
-struct GvLayout {
-  uint32_t red, xs, xh, total;
-  __host__ __device__ GvLayout(int C) {
-    const uint32_t nred = 2u * kW * MP * 32 * 4;
-    const uint32_t nxs = (uint32_t)MP * C * 8;
-    const uint32_t nxh = (uint32_t)MP * C * 256;
-    red = 0;
-    xs = nred;
-    if (nred + nxs + nxh <= kPre) {
-      xh = nred + nxs;
-      total = kPre + kTblBytes;
-    } else {
-      xh = kPre + kTblBytes;
-      total = xh + nxh;
-    }
-  }
-};
-
-struct GvParams {
+struct GvProb {
   const uint4* codes;    // [RB][C][4][32] uint4
   const uint4* lut;      // [RB*32][2] uint4 (16 fp16)
   const uint32_t* ab;    // [RB][GR][32] half2 (alpha, beta)
   const __nv_bfloat16* x;
   __nv_bfloat16* y;
   float* y32;
-  float* part;           // [RB - rbA][cmax][MP][32]
-  int* counters;         // [RB - rbA]
-  int* err;              // device error word
-  uint32_t UB;           // phase-B chunks
-  int N, K, M, RB, C, GR;
+  uint32_t xh, xs;       // dynamic-smem offsets of this problem's x image / chunk scales
+  int N, K, C, GR, RB;
   int gshift;            // chunk -> scale group: g = c >> gshift
-  int fullA, rbA, ncta, cmax;
-  long long* trace;      // debug: [ncta][16] globaltimer stamps, or null
+  int wait;              // 1: read x only after all earlier problems completed
+  int dup;               // x image shared with an earlier problem of the same batch
+  int tma;               // x rows staged by cp.async.bulk into the image region
+  int bstart, bend;      // batch of this problem: problems [bstart, bend]
+  int rboff;             // first item of this problem within its batch
+  int btot;              // items (row blocks) of the whole batch
 };
 
+struct GvParams {
+  GvProb p[kMaxProb];
+  int np, M, ncta;
+  uint32_t red;          // dynamic-smem offset of the reduction buffer [2][kW][MP][32]
+  uint32_t bars;         // dynamic-smem offset of the mbarriers
+  uint32_t ring;         // dynamic-smem offset of the code ring [kW][kRing][2048]
+  uint32_t abring;       // dynamic-smem offset of the (alpha, beta) ring [kW][kRing][128]
+  int* done;             // [kMaxProb] batch release counters (self-resetting)
+  int* err;              // device error word
+  long long* trace;      // debug: [ncta][64] globaltimer stamps, or null
+};
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ float fhfma_lo(uint32_t a, uint32_t b, float c) {
   float r;
   asm("{ .reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2;"
@@ -126,6 +133,61 @@ __device__ __forceinline__ float2 lds64f(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+// Same, backing off between polls (for waits that are usually long).
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+        "p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(200);
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void cw_sync() {  // barrier of the kW compute warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kW * 32) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= target, then acquire (one fence, not an L1 invalidation per poll).
+__device__ __forceinline__ void wait_geq(const int* p, int target) {
+  while (ld_relaxed(p) < target) __nanosleep(32);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -133,93 +195,65 @@ __device__ __forceinline__ long long gtimer() {
 }
 #define GV_TRACE(slot)                                                             \
   do {                                                                             \
-    if (P.trace && threadIdx.x == 0) P.trace[blockIdx.x * 16 + (slot)] = gtimer(); \
+    if (P.trace && threadIdx.x == 0) P.trace[blockIdx.x * 64 + (slot)] = gtimer(); \
   } while (0)
 
-// CTA whose phase-B range holds chunk u (all products fit 32 bits: the host
-// checks UB * ncta < 2^32).
-__device__ __forceinline__ int cta_of(uint32_t u, uint32_t U, uint32_t ncta) {
-  return (int)(((u + 1) * ncta + U - 1) / U) - 1;
-}
-
-// Segment of a CTA: row block and chunk range [c0, c1).
-struct Seg {
-  int rb, c0, c1;
+// ---------------------------------------------------------------------------
+// Work items: (problem, row block), dealt round-robin per batch
+// ---------------------------------------------------------------------------
+struct Item {
+  int p, rb, j;  // p == np: end; j = item index within the batch
 };
 
-// This CTA's segments: fullA whole row blocks (phase A), then at most two
-// pieces of the phase-B range (its length is <= C because RB - rbA < ncta).
-struct Work {
-  int fullA, ncta, b, C, nseg;
-  int rb0, c0a, c0b, c1b;  // phase B: rb0 [c0a, c0b), then rb0 + 1 [0, c1b)
-  __device__ __forceinline__ Seg get(int i) const {
-    Seg g;
-    if (i < fullA) {
-      g.rb = i * ncta + b;
-      g.c0 = 0;
-      g.c1 = C;
-    } else if (i == fullA) {
-      g.rb = rb0;
-      g.c0 = c0a;
-      g.c1 = c0b;
-    } else {
-      g.rb = rb0 + 1;
-      g.c0 = 0;
-      g.c1 = c1b;
+// Resolve item index it.j of the batch holding problem it.p; past the batch's
+// end move to the next batch (starting again at this CTA's index b).
+__device__ __forceinline__ void locate(const GvParams& P, int b, Item& it) {
+  while (it.p < P.np) {
+    const GvProb& h = P.p[P.p[it.p].bstart];
+    if (it.j < h.btot) {
+      int p = h.bstart;
+      while (it.j >= P.p[p].rboff + P.p[p].RB) ++p;
+      it.p = p;
+      it.rb = it.j - P.p[p].rboff;
+      return;
     }
-    return g;
+    it.p = h.bend + 1;
+    it.j = b;
   }
-};
-
-__device__ __forceinline__ Work make_work(uint32_t UB, int C, int ncta, int fullA, int rbA, int b) {
-  Work w;
-  w.fullA = fullA;
-  w.ncta = ncta;
-  w.b = b;
-  w.C = C;
-  w.nseg = fullA;
-  w.rb0 = rbA;
-  w.c0a = w.c0b = w.c1b = 0;
-  const uint32_t lo = (uint32_t)b * UB / (uint32_t)ncta, hi = (uint32_t)(b + 1) * UB / (uint32_t)ncta;
-  if (lo < hi) {
-    const int len = (int)(hi - lo);
-    w.rb0 = rbA + (int)(lo / (uint32_t)C);
-    w.c0a = (int)(lo % (uint32_t)C);
-    w.c0b = min(C, w.c0a + len);
-    w.nseg += 1;
-    if (w.c0a + len > C) {
-      w.c1b = w.c0a + len - C;
-      w.nseg += 1;
-    }
-  }
-  return w;
+}
+__device__ __forceinline__ Item item_begin(const GvParams& P, int b) {
+  Item it{0, 0, b};
+  locate(P, b, it);
+  return it;
+}
+__device__ __forceinline__ void item_next(const GvParams& P, int b, Item& it) {
+  it.j += P.ncta;
+  locate(P, b, it);
+}
+__device__ __forceinline__ void piece_of(int C, int warp, int& a, int& e) {
+  a = (warp * C) / kW;
+  e = ((warp + 1) * C) / kW;
 }
 
-// Load cursor of one warp: segment li, chunk lc of its piece [.., le); cp is
-// this lane's first uint4 of chunk lc, abrow the lane's (alpha, beta) row.
+// Weight-stream cursor of one compute warp over its chunk pieces of all items.
 struct Cursor {
-  int li, lc, le;
-  const uint4* cp;
-  const uint32_t* abrow;
+  Item it;
+  int lc, le, gshift;
+  const uint8_t* cg;     // global address of chunk lc (2 KB)
+  const uint8_t* abrow;  // global address of the row block's (alpha, beta) lines (128 B each)
 };
 
-__device__ __forceinline__ void piece_of(const Seg& sg, int warp, int& a, int& e) {
-  const int n = sg.c1 - sg.c0;
-  a = sg.c0 + ((warp * n) >> 4);
-  e = sg.c0 + (((warp + 1) * n) >> 4);
-}
-
-// Advance to the next segment whose piece for this warp is non-empty.
-__device__ __forceinline__ void next_piece(const Work& W, const uint4* codes, const uint32_t* ab,
-                                           int GR, int warp, int lane, Cursor& c) {
-  while (true) {
-    ++c.li;
-    if (c.li >= W.nseg) return;
-    const Seg sg = W.get(c.li);
-    piece_of(sg, warp, c.lc, c.le);
-    c.cp = codes + ((size_t)sg.rb * W.C + c.lc) * 128 + lane;
-    c.abrow = ab + (size_t)sg.rb * GR * 32 + lane;
-    if (c.lc < c.le) return;
+__device__ __forceinline__ void settle(const GvParams& P, int b, int warp, Cursor& c) {
+  while (c.it.p < P.np) {
+    const GvProb& q = P.p[c.it.p];
+    piece_of(q.C, warp, c.lc, c.le);
+    if (c.lc < c.le) {
+      c.cg = reinterpret_cast<const uint8_t*>(q.codes) + ((size_t)c.it.rb * q.C + c.lc) * 2048;
+      c.abrow = reinterpret_cast<const uint8_t*>(q.ab) + (size_t)c.it.rb * q.GR * 128;
+      c.gshift = q.gshift;
+      return;
+    }
+    item_next(P, b, c.it);
   }
 }
 
@@ -228,10 +262,11 @@ struct Chunk {
   uint32_t ab;
 };
 
-// Pair table for row `lane` into buffer buf; warp w writes the 16 entries
-// whose high nibble is w.
+// Pair table for row `lane` into buffer buf: entry e = 16*hi + lo holds
+// (T[lo], T[hi]); compute warp w writes the slice hi = w.
 __device__ __forceinline__ void build_table(const uint4 l0, const uint4 l1, int warp, int buf,
                                             uint32_t laneoff) {
+  static_assert(kW == 16, "one high nibble per compute warp");
   const uint32_t t[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
   const int h = warp >> 1;  // word of T[warp] (selects, not a local-memory index)
   const uint32_t s0 = (h & 1) ? l0.y : l0.x, s1 = (h & 1) ? l0.w : l0.z;
@@ -286,155 +321,85 @@ __device__ __forceinline__ void consume(const Chunk& ch, const uint32_t tb, cons
   }
 }
 
+// x of problem q -> permuted fp16 image + per-chunk (2^-e, sum x). A warp task
+// covers (m, 4 consecutive chunks): lanes 8u..8u+7 own chunk c0+u, 16
+// consecutive k each (k = 128c + 16*sub + t), so the max/sum trees are 3
+// shuffles deep. Image position of k = 128c + 64h + 16s + 2j (+1): slab s,
+// pair 8h + j -> a lane's 16 values are pairs 8*(sub/4) .. +7 of slab sub%4.
 template <int MP>
-__global__ void __launch_bounds__(kT, 1) k_lutgemv(GvParams P) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  asm volatile("griddepcontrol.launch_dependents;");
-  GV_TRACE(0);
-  if (P.trace && threadIdx.x == 0) P.trace[blockIdx.x * 16 + 12] = clock64();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x;
-  const uint32_t laneoff = (uint32_t)lane << 2;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  if (sbase != kDynBase) {  // the table must sit at shared address 0x10000
-    if (threadIdx.x == 0) atomicMax(P.err, (int)ANYQ_ERR_INTERNAL);
-    return;
+__device__ __forceinline__ void prep_x(const GvProb& q, int M, uint8_t* smem, int task, int lane) {
+  const int cq = (q.C + 3) >> 2;
+  const int m = task / cq, c = (task % cq) * 4 + (lane >> 3), sub = lane & 7;
+  const int k0 = c * 128 + sub * 16;
+  float v[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) v[t] = 0.0f;
+  const bool live = m < M && c < q.C;
+  if (live && q.tma) {
+    // raw row m was staged in place: chunk c's 256 B sit where its image goes
+    const uint8_t* src = smem + q.xh + ((size_t)m * q.K + k0) * 2;
+    const uint4 r0 = *reinterpret_cast<const uint4*>(src), r1 = *reinterpret_cast<const uint4*>(src + 16);
+    const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const __nv_bfloat162 p2 = *reinterpret_cast<const __nv_bfloat162*>(&w[t]);
+      v[2 * t] = __low2float(p2);
+      v[2 * t + 1] = __high2float(p2);
+    }
+  } else if (live) {  // direct loads (K not a multiple of 128 or unaligned x)
+    const unsigned short* xr = reinterpret_cast<const unsigned short*>(q.x + (size_t)m * q.K);
+    unsigned short r[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) r[t] = (k0 + t < q.K) ? __ldcg(xr + k0 + t) : (unsigned short)0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = __bfloat162float(__ushort_as_bfloat16(r[t]));
   }
-  const GvLayout<MP> lay(P.C);
-  float* red = reinterpret_cast<float*>(smem + lay.red);
-  const uint32_t xbase = sbase + lay.xh, xstride = (uint32_t)P.C * 256;
-  const uint32_t xsbase = sbase + lay.xs, xsstride = (uint32_t)P.C * 8;
-  const Work W = make_work(P.UB, P.C, P.ncta, P.fullA, P.rbA, b);
-  const int nseg = W.nseg;
-  const uint4* const codes = P.codes;
-  const uint32_t* const abp = P.ab;
-  const int GR = P.GR, gshift = P.gshift;
-
-  // ---- load cursor over this warp's pieces of all segments; 2-chunk ring
-  Cursor cur;
-  cur.li = -1;
-  cur.lc = cur.le = 0;
-  cur.cp = P.codes;
-  cur.abrow = P.ab;
-  if (nseg > 0) next_piece(W, codes, abp, GR, warp, lane, cur);
-  auto load = [&](Chunk& ch) {
-    if (cur.li < nseg) {
+  float amax = 0.0f, sum = 0.0f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ch.w[q] = __ldcs(cur.cp + q * 32);
-      ch.ab = __ldg(cur.abrow + ((cur.lc >> gshift) << 5));
-      cur.cp += 128;
-      if (++cur.lc >= cur.le) next_piece(W, codes, abp, GR, warp, lane, cur);
-    }
-  };
-  Chunk r0, r1;
-  load(r0);
-  load(r1);
-  GV_TRACE(1);
-
-  // ---- LUT of segment 0 -> table 0; LUT of segment 1 prefetched
-  uint4 nl0 = make_uint4(0, 0, 0, 0), nl1 = nl0;
-  if (nseg > 0) {
-    const uint4* lp = P.lut + ((size_t)W.get(0).rb * 32 + lane) * 2;
-    build_table(__ldg(lp), __ldg(lp + 1), warp, 0, laneoff);
+  for (int t = 0; t < 16; ++t) {
+    amax = fmaxf(amax, fabsf(v[t]));
+    sum += v[t];
   }
-  if (nseg > 1) {
-    const uint4* lp = P.lut + ((size_t)W.get(1).rb * 32 + lane) * 2;
-    nl0 = __ldg(lp);
-    nl1 = __ldg(lp + 1);
+#pragma unroll
+  for (int off = 4; off; off >>= 1) {
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    sum += __shfl_xor_sync(0xffffffffu, sum, off);
   }
-  GV_TRACE(2);
-
-  // ---- x: permuted fp16 image + per-chunk (2^-e, sum x); depends on the
-  // previous kernel in the stream
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  GV_TRACE(3);
-  for (int task = warp; task < MP * P.C; task += kW) {
-    const int m = task / P.C, c = task % P.C;
-    const int k0 = c * 128 + lane * 4;
-    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    if (m < P.M) {
-      const __nv_bfloat16* xr = P.x + (size_t)m * P.K;
-      if ((P.K & 3) == 0 && k0 + 3 < P.K) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(xr + k0);
-        const __nv_bfloat162 p0 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-        const __nv_bfloat162 p1 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-        v[0] = __low2float(p0);
-        v[1] = __high2float(p0);
-        v[2] = __low2float(p1);
-        v[3] = __high2float(p1);
-      } else {
+  // e puts max|x| in [2^14, 2^15): exponent arithmetic on the bits (ldexpf /
+  // ilogbf are library calls, many times the instructions of this block)
+  const int ex = (__float_as_int(amax) >> 23) & 0xff;  // biased exponent (amax >= 0)
+  const int e = (amax > 0.0f && ex < 255) ? min(141 - ex, 126) : 0;
+  const float sc = __int_as_float((127 + e) << 23), isc = __int_as_float((127 - e) << 23);
+  uint32_t h[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (k0 + j < P.K) v[j] = __bfloat162float(xr[k0 + j]);
-      }
-    }
-    float amax = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
-    float sum = (v[0] + v[1]) + (v[2] + v[3]);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-      sum += __shfl_xor_sync(0xffffffffu, sum, off);
-    }
-    const int e = (amax > 0.0f && isfinite(amax)) ? 14 - ilogbf(amax) : 0;
-    // k = 128c + 4L + j  <->  slab q = (L%16)/4, pair b = 8(L/16) + 2(L%4) + j/2
-    const int q = (lane & 15) >> 2, bp = 8 * (lane >> 4) + 2 * (lane & 3);
-    const __half2 h01 = __floats2half2_rn(ldexpf(v[0], e), ldexpf(v[1], e));
-    const __half2 h23 = __floats2half2_rn(ldexpf(v[2], e), ldexpf(v[3], e));
-    uint2 pk;
-    pk.x = *reinterpret_cast<const uint32_t*>(&h01);
-    pk.y = *reinterpret_cast<const uint32_t*>(&h23);
-    *reinterpret_cast<uint2*>(smem + lay.xh + (size_t)m * P.C * 256 + c * 256 + (q * 16 + bp) * 4) = pk;
-    if (lane == 0)
-      *reinterpret_cast<float2*>(smem + lay.xs + ((size_t)m * P.C + c) * 8) =
-          make_float2(ldexpf(1.0f, -e), sum);
+  for (int t = 0; t < 8; ++t) {
+    const __half2 p2 = __floats2half2_rn(v[2 * t] * sc, v[2 * t + 1] * sc);
+    h[t] = *reinterpret_cast<const uint32_t*>(&p2);
   }
-  GV_TRACE(4);
-  __syncthreads();
-  GV_TRACE(5);
+  __syncwarp();  // every lane has read its raw x before the images overwrite it
+  if (live) {
+    uint8_t* dst = smem + q.xh + (size_t)m * q.C * 256 + c * 256 + ((sub & 3) * 16 + 8 * (sub >> 2)) * 4;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(dst + 16) = make_uint4(h[4], h[5], h[6], h[7]);
+    if (sub == 0)
+      *reinterpret_cast<float2*>(smem + q.xs + ((size_t)m * q.C + c) * 8) = make_float2(isc, sum);
+  }
+}
 
-  // ---- main loop over segments
-  for (int i = 0; i < nseg; ++i) {
-    const Seg sg = W.get(i);
-    int a, e;
-    piece_of(sg, warp, a, e);
-    const uint32_t tb = kTblAddr | ((uint32_t)(i & 1) << 7) | laneoff;
-    float y[MP];
-#pragma unroll
-    for (int m = 0; m < MP; ++m) y[m] = 0.0f;
-    uint32_t xa = xbase + (uint32_t)a * 256, xsa = xsbase + (uint32_t)a * 8;
-    int c = a;
-    for (; c + 2 <= e; c += 2) {
-      consume<MP>(r0, tb, xa, xsa, xstride, xsstride, y);
-      load(r0);
-      consume<MP>(r1, tb, xa + 256, xsa + 8, xstride, xsstride, y);
-      load(r1);
-      xa += 512;
-      xsa += 16;
-    }
-    if (c < e) {
-      consume<MP>(r0, tb, xa, xsa, xstride, xsstride, y);
-      load(r0);
-      const Chunk t = r0;  // rotate: r1 is the next chunk to consume
-      r0 = r1;
-      r1 = t;
-    }
-    // next row block's table (its buffer was last read in segment i-1)
-    if (i + 1 < nseg) {
-      build_table(nl0, nl1, warp, (i + 1) & 1, laneoff);
-      if (i + 2 < nseg) {
-        const uint4* lp = P.lut + ((size_t)W.get(i + 2).rb * 32 + lane) * 2;
-        nl0 = __ldg(lp);
-        nl1 = __ldg(lp + 1);
-      }
-    }
-    float* rp = red + (size_t)(i & 1) * kW * MP * 32;
-#pragma unroll
-    for (int m = 0; m < MP; ++m) rp[(warp * MP + m) * 32 + lane] = y[m];
-    if (i < 3) GV_TRACE(6 + 2 * i);
-    __syncthreads();
-    if (i < 3) GV_TRACE(7 + 2 * i);
-    if (warp == 0) {
-      const int rb = sg.rb;
+// Writer warp: per item reduce the kW warp partials (fixed order) and store y;
+// after a batch release it grid-wide.
+template <int MP>
+__device__ __forceinline__ void writer_loop(const GvParams& P, const float* red, uint32_t bar_full,
+                                            uint32_t bar_empty, int b, int lane) {
+  Item it = item_begin(P, b);
+  int g = 0;
+  for (int p0 = 0; p0 < P.np;) {
+    const int p1 = P.p[p0].bend;
+    while (it.p <= p1) {
+      const GvProb& q = P.p[it.p];
+      const int par = g & 1;
+      mbar_wait_sleep(bar_full + 8 * par, (uint32_t)((g >> 1) & 1));
+      const float* rp = red + (size_t)par * kW * MP * 32;
       float acc[MP];
 #pragma unroll
       for (int m = 0; m < MP; ++m) {
@@ -443,101 +408,345 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(GvParams P) {
         for (int w = 0; w < kW; ++w) t += rp[(w * MP + m) * 32 + lane];
         acc[m] = t;
       }
-      bool write = true;
-      if (rb >= P.rbA) {
-        const uint32_t ub0 = (uint32_t)(rb - P.rbA) * P.C;
-        const int first = cta_of(ub0, P.UB, P.ncta);
-        const int last = cta_of(ub0 + P.C - 1, P.UB, P.ncta);
-        if (last > first) {
-          // CTAs first..last share this row block. When UB < ncta some CTAs
-          // have empty ranges; the others hold exactly one chunk each, so the
-          // contributors are the C chunks of the row block (slot = chunk).
-          const bool sparse = P.UB < P.ncta;
-          const int ncontrib = sparse ? P.C : last - first + 1;
-          const int slot = sparse ? (int)((uint32_t)b * P.UB / (uint32_t)P.ncta - ub0) : b - first;
-          float* pp = P.part + ((size_t)(rb - P.rbA) * P.cmax + slot) * MP * 32;
-#pragma unroll
-          for (int m = 0; m < MP; ++m) pp[m * 32 + lane] = acc[m];
-          __threadfence();
-          __syncwarp();
-          int old = 0;
-          if (lane == 0) old = atomicAdd(&P.counters[rb - P.rbA], 1);
-          old = __shfl_sync(0xffffffffu, old, 0);
-          write = old == ncontrib - 1;
-          if (write) {
-            __threadfence();
-#pragma unroll
-            for (int m = 0; m < MP; ++m) {
-              float t = 0.0f;
-              for (int sl = 0; sl < ncontrib; ++sl)
-                t += __ldcg(P.part + ((size_t)(rb - P.rbA) * P.cmax + sl) * MP * 32 + m * 32 + lane);
-              acc[m] = t;
-            }
-            if (lane == 0) P.counters[rb - P.rbA] = 0;
-          }
-        }
-      }
-      const int row = rb * 32 + lane;
-      if (write && row < P.N) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * par);
+      const int row = it.rb * 32 + lane;
+      if (row < q.N) {
 #pragma unroll
         for (int m = 0; m < MP; ++m) {
           if (m < P.M) {
-            P.y[(size_t)m * P.N + row] = __float2bfloat16_rn(acc[m]);
-            if (P.y32) P.y32[(size_t)m * P.N + row] = acc[m];
+            q.y[(size_t)m * q.N + row] = __float2bfloat16_rn(acc[m]);
+            if (q.y32) q.y32[(size_t)m * q.N + row] = acc[m];
           }
         }
       }
+      item_next(P, b, it);
+      ++g;
     }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      const int old = atomicAdd(&P.done[p1], 1);
+      if (p1 == P.np - 1 && old == P.ncta - 1)  // last CTA of the last batch: reset
+        for (int r = 0; r < P.np; ++r) P.done[r] = 0;
+    }
+    __syncwarp();
+    p0 = p1 + 1;
   }
-  GV_TRACE(15);
-  if (P.trace && threadIdx.x == 0) P.trace[blockIdx.x * 16 + 13] = clock64();
+}
+
+template <int MP>
+__global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvParams Pk) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  asm volatile("griddepcontrol.launch_dependents;");
+  // The parameter block (indexed by problem) is copied to shared memory in one
+  // parallel pass: register-indexed constant loads would otherwise miss the
+  // constant cache one dependent round trip at a time.
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&Pk);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(smem + kParamOff);
+    for (int i = threadIdx.x; i < (int)(sizeof(GvParams) / 4); i += kT) dst[i] = src[i];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x;
+  const uint32_t laneoff = (uint32_t)lane << 2;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const GvParams& P = *reinterpret_cast<const GvParams*>(smem + kParamOff);
+  __syncthreads();
+  const uint32_t bar_full = sbase + P.bars, bar_empty = bar_full + 16, bar_x = bar_full + 32;
+  // table hand-off: item g reads pair-table buffer g&1; tready = all slices of
+  // the buffer written, tfree = every compute warp finished reading it
+  const uint32_t tready = bar_full + 40, tfree = tready + 16;
+  const uint32_t rbar0 = bar_full + 72;  // [kW][kRing] weight-ring barriers
+  GV_TRACE(0);
+  if (sbase != kDynBase) {  // the table must sit at shared address 0x10000
+    if (threadIdx.x == 0) atomicMax(P.err, (int)ANYQ_ERR_INTERNAL);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar_full, kW);
+    mbar_init(bar_full + 8, kW);
+    mbar_init(bar_empty, 1);
+    mbar_init(bar_empty + 8, 1);
+    mbar_init(bar_x, 1);
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(tready + 8 * j, kW);
+      mbar_init(tfree + 8 * j, kW);
+    }
+    for (int j = 0; j < kW * kRing; ++j) mbar_init(rbar0 + 8 * j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem + P.red);
+  if (warp == kW) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    writer_loop<MP>(P, red, bar_full, bar_empty, b, lane);
+    return;
+  }
+
+  // ---- compute warps -------------------------------------------------------
+  // weight stream: each warp streams its chunk pieces with cp.async.bulk into
+  // its private ring (started before griddepcontrol.wait: weights do not
+  // depend on the previous kernel)
+  Item s = item_begin(P, b);
+  Cursor cur;
+  cur.it = s;
+  cur.lc = cur.le = 0;
+  cur.gshift = 0;
+  cur.cg = nullptr;
+  cur.abrow = nullptr;
+  settle(P, b, warp, cur);
+  const uint32_t ring = sbase + P.ring + (uint32_t)warp * kRing * 2048;
+  const uint32_t abring = sbase + P.abring + (uint32_t)warp * kRing * 128;
+  const uint32_t rbar = rbar0 + (uint32_t)warp * kRing * 8;
+  auto issue = [&](int slot) {  // next chunk of the cursor into `slot` (lane 0)
+    if (cur.it.p < P.np) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(rbar + 8 * slot, 2048 + 128);
+        bulk_g2s(ring + slot * 2048, cur.cg, 2048, rbar + 8 * slot);
+        bulk_g2s(abring + slot * 128, cur.abrow + ((cur.lc >> cur.gshift) << 7), 128, rbar + 8 * slot);
+      }
+      cur.cg += 2048;
+      if (++cur.lc >= cur.le) {
+        item_next(P, b, cur.it);
+        settle(P, b, warp, cur);
+      }
+    }
+  };
+  for (int j = 0; j < kRing; ++j) issue(j);
+  int nfetch = 0;  // chunks taken from the ring by this warp
+  auto fetch = [&](Chunk& ch) {
+    const int slot = nfetch % kRing;
+    mbar_wait(rbar + 8 * slot, (uint32_t)((nfetch / kRing) & 1));
+    const uint32_t a = ring + slot * 2048 + lane * 16;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ch.w[q] = lds128(a + q * 512);
+    ch.ab = lds32(abring + slot * 128 + lane * 4);
+    __syncwarp();
+    issue(slot);
+    ++nfetch;
+  };
+
+  // pair tables: item s -> buffer 0 now; the LUT of the next item prefetched
+  Item nx = s;
+  item_next(P, b, nx);
+  auto lut_of = [&](const Item& it) { return P.p[it.p].lut + ((size_t)it.rb * 32 + lane) * 2; };
+  uint4 nl0 = make_uint4(0, 0, 0, 0), nl1 = nl0;
+  if (s.p < P.np) {
+    const uint4* lp = lut_of(s);
+    build_table(__ldg(lp), __ldg(lp + 1), warp, 0, laneoff);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tready);
+  }
+  if (nx.p < P.np) {
+    const uint4* lp = lut_of(nx);
+    nl0 = __ldg(lp);
+    nl1 = __ldg(lp + 1);
+  }
+  GV_TRACE(1);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  int xbatch = 0;     // x batches staged so far (parity of bar_x)
+  int xready = -1;    // x images are ready for problems <= xready
+  int g = 0;          // items processed by this CTA
+  while (s.p < P.np) {
+    const int p = s.p;
+    const GvProb& q = P.p[p];
+    if (p > xready) {  // first item of a new batch: x images of the batch
+      const int p0 = q.bstart, p1 = q.bend;
+      if (P.p[p0].wait && p0 > 0) {  // every CTA must have released batch p0-1
+        GV_TRACE(16 + p0);
+        if (threadIdx.x == 0) wait_geq(&P.done[p0 - 1], P.ncta);
+        cw_sync();
+        GV_TRACE(24 + p0);
+      }
+      if (threadIdx.x == 0) {  // raw x rows by TMA (bypasses the L1 load queue)
+        uint32_t bytes = 0;
+        for (int pp = p0; pp <= p1; ++pp)
+          if (P.p[pp].tma && !P.p[pp].dup) bytes += (uint32_t)P.M * P.p[pp].K * 2;
+        mbar_expect_tx(bar_x, bytes);
+        for (int pp = p0; pp <= p1; ++pp) {
+          const GvProb& r = P.p[pp];
+          if (!r.tma || r.dup) continue;
+          for (int m = 0; m < P.M; ++m)
+            bulk_g2s(sbase + r.xh + (uint32_t)m * r.K * 2, r.x + (size_t)m * r.K, (uint32_t)r.K * 2,
+                     bar_x);
+        }
+      }
+      mbar_wait(bar_x, (uint32_t)(xbatch & 1));
+      ++xbatch;
+      int base = 0;  // conversion tasks of the batch dealt round-robin to the warps
+      for (int pp = p0; pp <= p1; ++pp) {
+        if (P.p[pp].dup) continue;
+        const int nt = MP * ((P.p[pp].C + 3) >> 2);
+        for (int task = (warp - base % kW + kW) % kW; task < nt; task += kW)
+          prep_x<MP>(P.p[pp], P.M, smem, task, lane);
+        base += nt;
+      }
+      xready = p1;
+      cw_sync();
+      GV_TRACE(2 + (p0 & 7));
+    }
+    int a, e;
+    piece_of(q.C, warp, a, e);
+    const uint32_t tb = kTblAddr | ((uint32_t)(g & 1) << 7) | laneoff;
+    mbar_wait(tready + 8 * (g & 1), (uint32_t)((g >> 1) & 1));
+    float y[MP];
+#pragma unroll
+    for (int m = 0; m < MP; ++m) y[m] = 0.0f;
+    const uint32_t xstride = (uint32_t)q.C * 256, xsstride = (uint32_t)q.C * 8;
+    uint32_t xa = sbase + q.xh + (uint32_t)a * 256, xsa = sbase + q.xs + (uint32_t)a * 8;
+    for (int c = a; c < e; ++c) {
+      Chunk ch;
+      fetch(ch);
+      consume<MP>(ch, tb, xa, xsa, xstride, xsstride, y);
+      xa += 256;
+      xsa += 8;
+    }
+    // partial sums to the writer warp
+    const int par = g & 1;
+    if (g >= 2) mbar_wait(bar_empty + 8 * par, (uint32_t)(((g >> 1) - 1) & 1));
+    float* rp = red + (size_t)par * kW * MP * 32;
+#pragma unroll
+    for (int m = 0; m < MP; ++m) rp[(warp * MP + m) * 32 + lane] = y[m];
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(bar_full + 8 * par);
+      mbar_arrive(tfree + 8 * (g & 1));  // done reading this item's table
+    }
+    // the next item's table goes into the other buffer once every warp has
+    // finished the previous item
+    if (nx.p < P.np) {
+      const int nb = (g + 1) & 1;
+      if (g >= 1) mbar_wait(tfree + 8 * nb, (uint32_t)(((g - 1) >> 1) & 1));
+      build_table(nl0, nl1, warp, nb, laneoff);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tready + 8 * nb);
+      Item nn = nx;
+      item_next(P, b, nn);
+      if (nn.p < P.np) {
+        const uint4* lp = lut_of(nn);
+        nl0 = __ldg(lp);
+        nl1 = __ldg(lp + 1);
+      }
+    }
+    if (g < 8) GV_TRACE(32 + g);
+    s = nx;
+    item_next(P, b, nx);
+    ++g;
+  }
+  GV_TRACE(63);
 }
 
 long long* g_gv_trace = nullptr;
 
+// Per-problem parameters, batches and shared-memory placement; returns the
+// dynamic shared memory bytes.
 template <int MP>
-void launch_gv(const LutTensor* t, const void* x, int64_t m, void* y, float* y32, cudaStream_t s) {
-  GvParams P;
-  P.codes = reinterpret_cast<const uint4*>(t->codes);
-  P.lut = reinterpret_cast<const uint4*>(t->lut);
-  P.ab = reinterpret_cast<const uint32_t*>(t->ab);
-  P.x = reinterpret_cast<const __nv_bfloat16*>(x);
-  P.y = reinterpret_cast<__nv_bfloat16*>(y);
-  P.y32 = y32;
-  P.part = t->gv_part;
-  P.counters = t->gv_counters;
-  P.err = t->gv_err;
-  P.N = (int)t->rows;
-  P.K = (int)t->cols;
+uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
+                    float* const* y32s, const int32_t* waits, int64_t m, GvParams& P) {
+  if (n < 1 || n > kMaxProb) fail(ANYQ_ERR_SHAPE, "LUT GEMV chain: 1..8 problems");
+  P.np = n;
   P.M = (int)m;
-  P.RB = t->RB;
-  P.C = t->C;
-  P.GR = t->GR;
-  P.gshift = t->gv_gshift;
-  P.ncta = t->gv_ncta;
-  P.fullA = t->gv_fullA;
-  P.rbA = t->gv_rbA;
-  P.UB = (uint32_t)((t->RB - t->gv_rbA) * P.C);
-  P.cmax = t->gv_cmax;
+  P.ncta = ts[0]->gv_ncta;
+  P.err = ts[0]->gv_err;
+  P.done = ts[0]->gv_done;
   P.trace = g_gv_trace;
-  const GvLayout<MP> lay(P.C);
-  if (lay.total > 227u * 1024u) fail(ANYQ_ERR_SHAPE, "LUT GEMV: x image too large for shared memory");
-  static uint32_t configured = 0;
-  if (lay.total > configured) {
-    ANYQ_CUDA(cudaFuncSetAttribute(k_lutgemv<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)lay.total));
-    configured = lay.total;
+  // placement: pieces go in front of the 64-KB table while they fit, else behind it
+  uint32_t front = kParamOff + (((uint32_t)sizeof(GvParams) + 255u) & ~255u);
+  uint32_t back = kPre + kTblBytes;
+  auto place = [&](uint32_t bytes) {
+    bytes = (bytes + 255u) & ~255u;
+    if (front + bytes <= kPre) {
+      const uint32_t o = front;
+      front += bytes;
+      return o;
+    }
+    const uint32_t o = back;
+    back += bytes;
+    return o;
+  };
+  P.ring = place((uint32_t)kW * kRing * 2048);
+  P.bars = place(72 + (uint32_t)kW * kRing * 8);
+  P.abring = place((uint32_t)kW * kRing * 128);
+  P.red = place(2u * kW * MP * 32 * 4);
+  for (int i = 0; i < n; ++i) {
+    const LutTensor* t = ts[i];
+    if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");
+    if (t->gv_gshift < 0)
+      fail(ANYQ_ERR_CONFIG, "LUT GEMV needs rowwise scales or group_size = 128 * 2^j");
+    if (t->gv_ncta != P.ncta) fail(ANYQ_ERR_SHAPE, "chain tensors were prepared for different devices");
+    GvProb& q = P.p[i];
+    q.codes = reinterpret_cast<const uint4*>(t->codes);
+    q.lut = reinterpret_cast<const uint4*>(t->lut);
+    q.ab = reinterpret_cast<const uint32_t*>(t->ab);
+    q.x = reinterpret_cast<const __nv_bfloat16*>(xs[i]);
+    q.y = reinterpret_cast<__nv_bfloat16*>(ys[i]);
+    q.y32 = y32s ? y32s[i] : nullptr;
+    q.N = (int)t->rows;
+    q.K = (int)t->cols;
+    q.C = t->C;
+    q.GR = t->GR;
+    q.RB = t->RB;
+    q.gshift = t->gv_gshift;
+    q.wait = (waits && i > 0) ? (waits[i] != 0) : 0;
+    // raw x rows are staged in place of their image: needs K = 128 * C
+    q.tma = (q.K % 128 == 0) && ((reinterpret_cast<uintptr_t>(xs[i]) & 15) == 0);
+    q.bstart = (i == 0 || q.wait) ? i : P.p[i - 1].bstart;
+    q.rboff = (q.bstart == i) ? 0 : P.p[i - 1].rboff + P.p[i - 1].RB;
+    // problems of one batch that read the same x share its image
+    q.dup = 0;
+    for (int j = q.bstart; j < i; ++j) {
+      if (P.p[j].x == q.x && P.p[j].K == q.K && !P.p[j].dup) {
+        q.dup = 1;
+        q.xs = P.p[j].xs;
+        q.xh = P.p[j].xh;
+        break;
+      }
+    }
+    if (!q.dup) {
+      q.xs = place((uint32_t)MP * t->C * 8);
+      q.xh = place((uint32_t)MP * t->C * 256);
+    }
   }
-  cudaLaunchAttribute attr[1];
+  for (int i = n - 1; i >= 0; --i) {
+    GvProb& q = P.p[i];
+    q.bend = (i == n - 1 || P.p[i + 1].wait) ? i : P.p[i + 1].bend;
+  }
+  for (int i = 0; i < n; ++i) {
+    GvProb& q = P.p[i];
+    q.btot = P.p[q.bend].rboff + P.p[q.bend].RB;
+  }
+  if (back > kSmemMax)
+    fail(ANYQ_ERR_SHAPE, "LUT GEMV chain: x images exceed shared memory (" + std::to_string(back) +
+                             " > " + std::to_string(kSmemMax) + " B)");
+  return back;
+}
+
+template <int MP>
+void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
+               float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s) {
+  GvParams P;
+  const uint32_t smem_bytes = plan_chain<MP>(n, ts, xs, ys, y32s, waits, m, P);
+  static uint32_t configured = 0;
+  if (smem_bytes > configured) {
+    ANYQ_CUDA(cudaFuncSetAttribute(k_lutgemv<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_bytes));
+    configured = smem_bytes;
+  }
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;  // co-residency for the chain waits
+  attr[1].val.cooperative = 1;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)P.ncta);
   lc.blockDim = dim3(kT);
-  lc.dynamicSmemBytes = lay.total;
+  lc.dynamicSmemBytes = smem_bytes;
   lc.stream = s;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = 2;
   ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_lutgemv<MP>, P));
   ANYQ_LAUNCHED();
 }
@@ -546,45 +755,35 @@ void launch_gv(const LutTensor* t, const void* x, int64_t m, void* y, float* y32
 
 void lutgemv_set_trace(long long* dev) { g_gv_trace = dev; }
 
-// Work split + workspace of the GEMV (called once from lutgemm_create).
+// GEMV settings of a tensor (called once from lutgemm_create).
 void lutgemv_setup(LutTensor* t) {
-  const int ncta = t->sms;
-  t->gv_ncta = ncta;
-  t->gv_fullA = t->RB / ncta;
-  t->gv_rbA = t->gv_fullA * ncta;
-  const int rbB = t->RB - t->gv_rbA;
-  const int C = t->C;
-  int cmax = 1;
-  if (rbB > 0) {
-    const long long UB = (long long)rbB * C;
-    auto cta = [&](long long u) { return ((u + 1) * ncta + UB - 1) / UB - 1; };
-    for (int r = 0; r < rbB; ++r)
-      cmax = std::max<int>(cmax, (int)(cta((long long)(r + 1) * C - 1) - cta((long long)r * C) + 1));
-  }
-  t->gv_cmax = cmax;
-  if ((unsigned long long)rbB * C * (ncta + 1) >= (1ull << 32))
-    fail(ANYQ_ERR_SHAPE, "LUT GEMV: tensor too large for the 32-bit work split");
+  t->gv_ncta = t->sms;
   // chunk -> scale-group index as a shift (rowwise: always group 0)
   t->gv_gshift = -1;
   if (t->GR == 1) t->gv_gshift = 30;
   else if ((t->GC & (t->GC - 1)) == 0) t->gv_gshift = __builtin_ctz((unsigned)t->GC);
-  const int nb = std::max(rbB, 1);
-  ANYQ_CUDA(cudaMalloc(&t->gv_part, sizeof(float) * (size_t)nb * cmax * kMaxMP * 32));
-  ANYQ_CUDA(cudaMalloc(&t->gv_counters, sizeof(int) * nb));
-  ANYQ_CUDA(cudaMemset(t->gv_counters, 0, sizeof(int) * nb));
   ANYQ_CUDA(cudaMalloc(&t->gv_err, sizeof(int)));
   ANYQ_CUDA(cudaMemset(t->gv_err, 0, sizeof(int)));
+  ANYQ_CUDA(cudaMalloc(&t->gv_done, sizeof(int) * kMaxProb));
+  ANYQ_CUDA(cudaMemset(t->gv_done, 0, sizeof(int) * kMaxProb));
+}
+
+void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
+                       float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s) {
+  if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "LUT GEMV supports 1 <= m <= 2");
+  if (n < 1 || !ts) fail(ANYQ_ERR_SHAPE, "empty GEMM chain");
+  if (m == 1) launch_gv<1>(n, ts, xs, ys, y32s, waits, m, s);
+  else launch_gv<2>(n, ts, xs, ys, y32s, waits, m, s);
 }
 
 void lutgemv_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y32,
                  cudaStream_t s) {
   if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");
-  if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "LUT GEMV supports 1 <= m <= 4");
-  if (t->gv_gshift < 0)
-    fail(ANYQ_ERR_CONFIG, "LUT GEMV needs rowwise scales or group_size = 128 * 2^j");
-  if (m == 1) launch_gv<1>(t, x, m, y, y32, s);
-  else if (m == 2) launch_gv<2>(t, x, m, y, y32, s);
-  else launch_gv<4>(t, x, m, y, y32, s);
+  const LutTensor* ts[1] = {t};
+  const void* xs[1] = {x};
+  void* ys[1] = {y};
+  float* y32s[1] = {y32};
+  lutgemv_chain_run(1, ts, xs, ys, y32s, nullptr, m, s);
 }
 
 }  // namespace anyq_b200

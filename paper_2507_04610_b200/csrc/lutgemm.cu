@@ -876,9 +876,8 @@ void lutgemm_destroy(LutTensor* t) {
   cudaFree(t->xsum);
   cudaFree(t->part);
   cudaFree(t->counters);
-  cudaFree(t->gv_part);
-  cudaFree(t->gv_counters);
   cudaFree(t->gv_err);
+  cudaFree(t->gv_done);
   delete t;
 }
 

@@ -27,18 +27,21 @@ struct LutTensor {
   int cmax = 0;
   int sms = 148;
   // CUDA-core GEMV (gemv.cu) work split + workspace
-  float* gv_part = nullptr;   // [RB - gv_rbA][gv_cmax][4][32]
-  int* gv_counters = nullptr; // [RB - gv_rbA]
   int* gv_err = nullptr;      // device error word of the GEMV
-  int gv_ncta = 0, gv_fullA = 0, gv_rbA = 0, gv_cmax = 1, gv_gshift = -1;
+  int* gv_done = nullptr;     // [8] chain completion counters (self-resetting)
+  int gv_ncta = 0, gv_gshift = -1;
 };
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt);
 void lutgemm_destroy(LutTensor* t);
 void lutgemm_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
-// K1a CUDA-core GEMV (m <= 4) over the same prepacked tensor (gemv.cu).
+// K1a CUDA-core GEMV (m <= 2) over the same prepacked tensor (gemv.cu).
 void lutgemv_setup(LutTensor* t);
 void lutgemv_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
+// A chain of n <= 8 GEMMs (same m <= 2) in one launch; problem i > 0 with
+// waits[i] != 0 reads x_i only after all earlier problems completed.
+void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
+                       float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s);
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
 void lutgemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,

@@ -55,13 +55,14 @@ def main():
     ap.add_argument("--ms", default="1,2,4")
     ap.add_argument("--shapes", default="q,k,gate,down")
     ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--chain", action="store_true", help="also time the 8B layer as one chain launch")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["hbm_gbs"]
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
     out = {}
-    for name in args.shapes.split(","):
+    for name in [s for s in args.shapes.split(",") if s]:
         n, k = SHAPES[name]
         qt = synthetic(n, k)
         w = dequant_f16(qt)
@@ -115,6 +116,41 @@ def main():
                 print(key, out[key], flush=True)
         for d in dts:
             d.close()
+    # the 8B decoder layer as ONE chain launch (q,k,v <- x; o <- y_q; gate,up <- y_o;
+    # down <- y_up), weights rotated over enough layers to defeat L2
+    if args.chain:
+        layer = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
+                 ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+        nl = 4
+        tens = [[anyq.DeviceTensor(synthetic(n, k, seed=10 * l + i)) for i, (_, n, k) in enumerate(layer)]
+                for l in range(nl)]
+        for m in (int(v) for v in args.ms.split(",")):
+            if m > 4:
+                continue
+            x = torch.randn(m, 4096, device=dev).to(torch.bfloat16)
+            ys = [torch.empty(m, n, device=dev, dtype=torch.bfloat16) for _, n, _ in layer]
+            xs = [x, x, x, ys[0], ys[3], ys[3], ys[5]]
+            waits = [0, 0, 0, 1, 1, 0, 1]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for l in range(nl):
+                    anyq.gemm_chain(tens[l], xs, ys, wait_prev=waits, stream=stream)
+            reps = 20
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    g.replay()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    g.replay()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / (reps * nl)
+            nb = sum(n * k // 2 + n * (k // 128) * 4 + n * 32 + m * k * 2 + m * n * 2 for _, n, k in layer)
+            gbs = nb / (us * 1e-6) / 1e9
+            out[f"layer_chain_m{m}"] = {"us": round(us, 3), "GBps": round(gbs, 1), "pct": round(100 * gbs / peak, 1)}
+            print(f"layer_chain_m{m}", out[f"layer_chain_m{m}"], flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/gemv_probe.json", "w") as f:
         json.dump(out, f, indent=1)

@@ -29,7 +29,7 @@ def main():
     dt = anyq.DeviceTensor(synthetic(n, k))
     x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
     y = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
-    tr = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(148 * 64, dtype=torch.int64, device="cuda")
     t_end = time.time() + 0.3
     while time.time() < t_end:
         for _ in range(50):
@@ -41,7 +41,7 @@ def main():
         dt.gemm(x, y, path=1)
         torch.cuda.synchronize()
         L.anyq_debug_set_gemv_trace(None)
-        t = tr.cpu().numpy().reshape(148, 16)
+        t = tr.cpu().numpy().reshape(148, 64)
         t0 = t[:, 0][t[:, 0] > 0].min()
         print(f"{name} M={m} rep {rep}: us after first CTA start: median / min / max")
         ghz = (t[:, 13] - t[:, 12]) / np.maximum(t[:, 15] - t[:, 0], 1)

@@ -3,7 +3,7 @@
 * anyq_gemm_fused (exact path): bit-identical to the reference gemm_fused /
   gemm_reference for every format, layout and M (test_qgemm.cpp:53-160).
 * device LUT GEMM paths (bf16 x, exact fp16 x fp16 products, fp32
-  accumulation): the CUDA-core GEMV (m <= 4, gemv.cu) and the tcgen05 LUT GEMM
+  accumulation): the CUDA-core GEMV (m <= 2, gemv.cu) and the tcgen05 LUT GEMM
   (m <= 16, lutgemm.cu), each within
   |dy| <= 1e-5 * sum_j |x_j| * (|alpha*T| + |beta|) of
   gemm_reference(bf16(x), narrowed(qt)) computed by the oracle in fp32.
@@ -147,8 +147,8 @@ def tc_tolerance(orc, x, qt):
 @pytest.mark.parametrize("fmt", ["any4", "int4", "nf4", "fp4"])
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8, 9, 16])
 def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m, path):
-    if path == "gemv" and m > 4:
-        pytest.skip("the GEMV serves m <= 4")
+    if path == "gemv" and m > 2:
+        pytest.skip("the GEMV serves m <= 2")
     n, k = 200, 384  # ragged rows (not a multiple of 32), 3 chunks, 3 groups
     w = orc.gaussian(n, k, 31)
     c = cfg(granularity=3, group_size=128, seed=2)
@@ -174,7 +174,7 @@ def test_tc_gemm_shapes(aq, orc, cuda, n, k, g, path):
     gran = 1 if g == k else 3
     c = cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=8)
     qt = aq.quantize_any(w, c)
-    x = bf16(orc.gaussian(3, k, 43))
+    x = bf16(orc.gaussian(2 if path == "gemv" else 3, k, 43))
     y32, _ = tc_gemm(aq, cuda, qt, x, PATHS[path])
     ref = orc.gemm_reference(x, orc.narrowed(qt))
     tol = tc_tolerance(orc, x, qt)
@@ -186,7 +186,7 @@ def test_tc_gemm_is_deterministic_and_rowwise_consistent(aq, orc, cuda, path):
     w = orc.gaussian(512, 1024, 5)
     qt = aq.quantize_any(w, cfg(codebook=3, max_iters=5))
     x1 = bf16(orc.gaussian(1, 1024, 6))
-    mm = 4 if path == "gemv" else 16
+    mm = 2 if path == "gemv" else 16
     xm = np.repeat(x1, mm, axis=0)
     a, _ = tc_gemm(aq, cuda, qt, x1, PATHS[path])
     b, _ = tc_gemm(aq, cuda, qt, x1, PATHS[path])
@@ -206,3 +206,38 @@ def test_gemv_rejects_unsupported_group(aq, orc, cuda):
     y32, _ = tc_gemm(aq, cuda, qt, x, 0)
     ref = orc.gemm_reference(x, orc.narrowed(qt))
     assert np.all(np.abs(y32 - ref) <= tc_tolerance(orc, x, qt))
+
+
+def test_gemm_chain_matches_single_launches(aq, orc, cuda):
+    """anyq_dev_gemm_chain: one launch of a dependent chain equals the single
+    launches bit for bit (x of problem i may be the y of problem i-1)."""
+    import torch
+
+    shapes = [(256, 384), (192, 384), (5000, 256), (384, 5000)]  # phase A + B + sparse split
+    dts, qts = [], []
+    for i, (n, k) in enumerate(shapes):
+        qt = aq.quantize_any(orc.gaussian(n, k, 70 + i), cfg(codebook=3, max_iters=4, seed=i))
+        qts.append(qt)
+        dts.append(aq.DeviceTensor(qt))
+    for m in (1, 2):
+        x0 = torch.from_numpy(bf16(orc.gaussian(m, 384, 80 + m))).cuda().to(torch.bfloat16)
+        x2 = torch.from_numpy(bf16(orc.gaussian(m, 256, 90 + m))).cuda().to(torch.bfloat16)
+        # chain: y0 = x0 W0, y1 = x0 W1 (independent), y2 = x2 W2, y3 = y2 W3 (waits on y2)
+        ys = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for n, _ in shapes]
+        y32 = [torch.empty(m, n, device="cuda", dtype=torch.float32) for n, _ in shapes]
+        aq.gemm_chain(dts, [x0, x0, x2, ys[2]], ys, wait_prev=[0, 0, 1, 1], y32s=y32)
+        torch.cuda.synchronize()
+        xs = [x0, x0, x2, ys[2].clone()]
+        for i, d in enumerate(dts):
+            r = torch.empty(m, shapes[i][0], device="cuda", dtype=torch.float32)
+            d.gemm(xs[i], None, r, path=1)
+            torch.cuda.synchronize()
+            assert torch.equal(r, y32[i]), i
+            ref = orc.gemm_reference(xs[i].float().cpu().numpy(), orc.narrowed(qts[i]))
+            assert np.all(np.abs(r.cpu().numpy() - ref) <= tc_tolerance(orc, xs[i].float().cpu().numpy(), qts[i]))
+        # repeated launches reuse the self-resetting counters
+        for _ in range(3):
+            aq.gemm_chain(dts, [x0, x0, x2, ys[2]], ys, wait_prev=[0, 0, 1, 1])
+        torch.cuda.synchronize()
+    for d in dts:
+        d.close()
