@@ -62,6 +62,15 @@ def hbm_peak():
         return 6650.0, "fallback"
 
 
+def hbm_peak_tflops():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 1590.0
+
+
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
         os.environ.get("LOCAL_RANK", "0"))
@@ -285,14 +294,20 @@ def gpu_arm(args):
     # buffers: layer input x, per-layer local y shards, gathered y (TP)
     x_in = torch.randn(M, 4096, device=dev).to(torch.bfloat16)
     ys = [[torch.empty(M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L] for L in layers]
-    yg = [[torch.empty(M, ns * P, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L]
+    # TP gather buffers: all_gather_into_tensor concatenates the [M, N/P] slices
+    # along dim 0 -> [P*M, N/P]; for M = 1 that memory IS the [1, N] row
+    yg = [[torch.empty(P * M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L]
           for L in layers] if P > 1 else None
+
+    def gathered(li, j):
+        g = yg[li][j]
+        return g.view(M, -1) if M == 1 else g.view(P, M, -1).permute(1, 0, 2).reshape(M, -1)
 
     def x_of(li, j):
         src = X_SRC[j]
         if src < 0:
             return x_in
-        return yg[li][src] if P > 1 else ys[li][src]
+        return gathered(li, src) if P > 1 else ys[li][src]
 
     def run_layer(li, s):
         L = layers[li]
@@ -383,7 +398,7 @@ def gpu_arm(args):
         else:
             run_layer(li, s)
         for j in range(7):
-            yh[li][j].copy_(yg[li][j] if P > 1 else ys[li][j], non_blocking=True)
+            yh[li][j].copy_(gathered(li, j) if P > 1 else ys[li][j], non_blocking=True)
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
@@ -438,8 +453,9 @@ def gpu_arm(args):
 
     # ---- M sweep (per-GEMM launches, AUTO path: GEMV for m = 1, tcgen05 above)
     sweep = {}
+    tpeak = hbm_peak_tflops()
     if not args.quick and P == 1:
-        for mm in (1, 2, 4, 8, 16):
+        for mm in (1, 2, 4, 8, 16, 64, 256, 1024, 4096):
             xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in (4096, 14336)}
             for j, (name, n, k) in enumerate(LAYER):
                 if name not in ("q", "gate", "down"):
@@ -450,26 +466,44 @@ def gpu_arm(args):
                     for li in range(len(layers)):
                         layers[li][j][3].gemm_ptr(xm[k].data_ptr(), mm, ym.data_ptr(), None,
                                                   stream.cuda_stream)
-                us = time_graph(one, 10) / len(layers)
+                us = time_graph(one, 10 if mm <= 256 else 3) / len(layers)
                 nb = algo_bytes(n, k, mm)
+                tf = 2.0 * mm * n * k / (us * 1e-6) / 1e12
                 sweep[f"{name}_M{mm}"] = {"us": round(us, 3),
-                                          "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
+                                          "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2),
+                                          "TFLOPs": round(tf, 1),
+                                          "pct_bf16_peak": round(100 * tf / tpeak, 2),
+                                          "path": "gemv" if mm == 1 else "tcgen05" if mm <= 16
+                                          else "dequant+cublas"}
 
-    # ---- k-means quantizer throughput (config 1: 4096x4096 any4 g128, device-resident)
+    # ---- k-means quantizer throughput (config 1 / config 4): each rank quantizes
+    # its 4096-row shard of a (4096*P) x 4096 gaussian matrix, device-resident,
+    # rows keyed by global index (no collective); max time over ranks
     kmeans = None
-    if not args.quick and P == 1:
+    if not args.quick:
         from paper_2507_04610_b200 import _abi
 
-        w = torch.randn(4096, 4096, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234 + rank)
+        w = torch.randn(4096, 4096, device=dev, generator=g)
         cfg = _abi.default_config(codebook=_abi.CB_ANY)
         anyq.dev_quantize_any(w[:256].contiguous(), cfg)  # warm
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        anyq.dev_quantize_any(w, cfg)
+        if P > 1:
+            dist.barrier()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
+        anyq.dev_quantize_any(w, cfg, row_offset=4096 * rank)
+        k1.record()
         torch.cuda.synchronize()
-        secs = time.perf_counter() - t0
-        kmeans = {"rows_per_s": round(4096 / secs, 1), "matrix": "4096x4096 gaussian any4 g128",
-                  "seconds": round(secs, 4)}
+        secs = k0.elapsed_time(k1) * 1e-3
+        if P > 1:
+            t = torch.tensor([secs], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            secs = float(t.item())
+        kmeans = {"rows_per_s": round(4096 * P / secs, 1),
+                  "matrix": f"{4096 * P}x4096 gaussian any4 g128, 4096 rows per GPU",
+                  "seconds": round(secs, 4), "gpus": P}
 
     # roofline of the dominant kernel: the step IS one k_lutgemv chain launch per
     # layer at M=1 (P=1), so its launch duration is the step time

@@ -178,8 +178,9 @@ int64_t anyq_dev_tensor_weight_bytes(const anyq_dev_tensor* t);
 int64_t anyq_dev_tensor_rows(const anyq_dev_tensor* t);
 int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t);
 
-/* y[m x rows] (bf16) = x[m x cols] (bf16) * dequant(W)^T on the tensor-core
- * LUT path (fp32 accumulation). m <= 64. Device pointers. */
+/* y[m x rows] (bf16) = x[m x cols] (bf16) * dequant(W)^T (fp32 accumulation),
+ * any m >= 1; the kernel is chosen by m (ANYQ_PATH_AUTO below). y_f32 may be
+ * NULL. Device pointers. */
 anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
                                int64_t m, void* y_bf16, float* y_f32,
                                void* stream);
@@ -187,8 +188,10 @@ anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
 /* Same, with the kernel chosen explicitly (tests and the M sweep):
  *   ANYQ_PATH_GEMV  CUDA-core LUT GEMV, m <= 2 (gemv.cu)
  *   ANYQ_PATH_TC    tensor-core (tcgen05, A in TMEM) LUT GEMM, m <= 16
- *   ANYQ_PATH_AUTO  the faster of the two for m (what anyq_dev_gemm_bf16 uses) */
-enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2 };
+ *   ANYQ_PATH_DEQUANT  bf16 dequantization + cuBLAS GEMM, any m (large-M path)
+ *   ANYQ_PATH_AUTO  GEMV for m = 1, tcgen05 for m <= 16, dequant above (what
+ *                   anyq_dev_gemm_bf16 uses) */
+enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2, ANYQ_PATH_DEQUANT = 3 };
 anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                     void* y_bf16, float* y_f32, int32_t path, void* stream);
 

@@ -490,11 +490,15 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
   return guard([&] {
     const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
     if (path == ANYQ_PATH_AUTO)
-      path = (m <= 1 && lt && lt->gv_gshift >= 0) ? ANYQ_PATH_GEMV : ANYQ_PATH_TC;
+      path = (m <= 1 && lt && lt->gv_gshift >= 0) ? ANYQ_PATH_GEMV
+             : m <= 16                              ? ANYQ_PATH_TC
+                                                    : ANYQ_PATH_DEQUANT;
     if (path == ANYQ_PATH_GEMV)
       lutgemv_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else if (path == ANYQ_PATH_TC)
       lutgemm_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_DEQUANT)
+      dequant_gemm_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else
       fail(ANYQ_ERR_CONFIG, "unknown GEMM path");
   });

@@ -30,6 +30,10 @@ struct LutTensor {
   int* gv_err = nullptr;      // device error word of the GEMV
   int* gv_done = nullptr;     // [8] chain completion counters (self-resetting)
   int gv_ncta = 0, gv_gshift = -1;
+  // large-M dequant + cuBLAS path (dequant_gemm.cu): lazily sized workspace
+  void* dq_w = nullptr;      // [<= 4096 rows][K] bf16
+  float* dq_acc = nullptr;   // [m][<= 4096] fp32
+  int64_t dq_acc_n = 0;
 };
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt);
@@ -44,6 +48,9 @@ void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs,
                        float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s);
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
+// M > 16: bf16 dequantization in row slices + cuBLAS GEMM (dequant_gemm.cu).
+void dequant_gemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
+                      cudaStream_t s);
 void lutgemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
 

@@ -107,7 +107,7 @@ def bf16(x):
     return bf16_round(x)
 
 
-PATHS = {"gemv": 1, "tc": 2}
+PATHS = {"gemv": 1, "tc": 2, "dequant": 3}
 
 
 def tc_gemm(aq, cuda, qt, x, path=2):
@@ -241,3 +241,22 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         torch.cuda.synchronize()
     for d in dts:
         d.close()
+
+
+@pytest.mark.parametrize("m", [1, 17, 64, 300])
+@pytest.mark.parametrize("n,k,g", [(200, 384, 128), (4096, 1024, 256), (96, 1280, 1280), (70, 200, 128)])
+def test_dequant_gemm_large_m(aq, orc, cuda, m, n, k, g):
+    """Large-M path: bf16 dequantization + cuBLAS (fp32 accumulation), within
+    2^-8 * sum|x*w| of gemm_reference(bf16(x), narrowed(qt))."""
+    w = orc.gaussian(n, k, 51)
+    gran = 1 if g == k else 3
+    qt = aq.quantize_any(w, cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=6))
+    x = bf16(orc.gaussian(m, k, 52))
+    y32, ybf = tc_gemm(aq, cuda, qt, x, PATHS["dequant"])
+    nq = orc.narrowed(qt)
+    ref = orc.gemm_reference(x, nq)
+    tol = 2.0 ** -8 * (np.abs(x) @ np.abs(orc.dequantize(nq)).T) + 1e-30
+    assert np.all(np.abs(y32 - ref) <= tol)
+    if m > 16:  # AUTO picks this path above m = 16
+        y32a, _ = tc_gemm(aq, cuda, qt, x, 0)
+        assert bits_equal(y32a, y32)
