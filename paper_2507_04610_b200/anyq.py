@@ -30,7 +30,8 @@ from ._abi import (  # noqa: F401  (re-exported vocabulary)
 )
 from .qtensor import QuantizedTensor
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libanyq_b200.so")
+LIB_PATH = os.environ.get("ANYQ_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                     "libanyq_b200.so")
 
 
 # ---------------------------------------------------------------------------

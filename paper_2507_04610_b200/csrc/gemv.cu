@@ -48,14 +48,21 @@
 #include "kernels.cuh"
 #include "lutgemm.cuh"
 
+#ifndef GV_WARPS
+#define GV_WARPS 16
+#endif
+#ifndef GV_RING
+#define GV_RING 2
+#endif
+
 namespace anyq_b200 {
 
 namespace {
 
-constexpr int kW = 16;                // compute warps per CTA
+constexpr int kW = GV_WARPS;          // compute warps per CTA
 constexpr int kT = (kW + 1) * 32;     // + one writer warp
 constexpr int kMaxMP = 2;
-constexpr int kRing = 2;              // TMA ring slots (2-KB chunks) per compute warp
+constexpr int kRing = GV_RING;         // TMA ring slots (2-KB chunks) per compute warp
 constexpr int kMaxProb = 8;
 constexpr uint32_t kTblAddr = 0x10000;  // shared-window address of the pair table
 constexpr uint32_t kDynBase = 0x400;    // shared-window address of dynamic smem (sm_100)
@@ -266,7 +273,8 @@ struct Chunk {
 // (T[lo], T[hi]); compute warp w writes the slice hi = w.
 __device__ __forceinline__ void build_table(const uint4 l0, const uint4 l1, int warp, int buf,
                                             uint32_t laneoff) {
-  static_assert(kW == 16, "one high nibble per compute warp");
+  static_assert(kW >= 16, "one high nibble per compute warp");
+  if (warp >= 16) return;
   const uint32_t t[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
   const int h = warp >> 1;  // word of T[warp] (selects, not a local-memory index)
   const uint32_t s0 = (h & 1) ? l0.y : l0.x, s1 = (h & 1) ? l0.w : l0.z;
@@ -600,7 +608,11 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
     for (int c = a; c < e; ++c) {
       Chunk ch;
       fetch(ch);
+#ifdef GV_SKIPCOMPUTE
+      y[0] += __uint_as_float((ch.w[0].x ^ ch.w[1].y ^ ch.w[2].z ^ ch.w[3].w ^ ch.ab) & 0x3fffffff) * 1e-30f;
+#else
       consume<MP>(ch, tb, xa, xsa, xstride, xsstride, y);
+#endif
       xa += 256;
       xsa += 8;
     }
