@@ -11,18 +11,19 @@
 // fp32, so the result differs from the fp32 reference only by summation order
 // (tolerance 1e-5 * sum|x*w|, tests/test_gpu_gemm.py).
 //
-// One persistent CTA per SM: 16 compute warps + 1 writer warp.
+// One persistent CTA per SM: 16 compute warps, 1 writer warp, 1 producer warp.
 //  * Work items are whole 32-row blocks. A launch runs a chain of GEMMs split
 //    into batches (runs of problems without a dependency); the row blocks of a
 //    batch, concatenated in problem order, are dealt round-robin to the CTAs.
 //    An item is computed by one CTA only, so y needs no cross-CTA combine and
 //    the result is deterministic.
-//  * Inside a CTA the 16 compute warps split the item's 128-k chunks; lane L
-//    of every warp owns row L. A chunk = 32 rows x 128 k = 2 KB contiguous in
-//    the prepacked code tensor (layout of lutgemm.cu: [RB][C][4 slabs][32 rows]
-//    [16 B]). Each warp streams its own chunks with cp.async.bulk into a
-//    private 2-slot shared-memory ring (the L1 load queue stays free for the
-//    latency-critical LUT / x traffic).
+//  * The producer warp (one lane) streams every item of the CTA: its 32 LUT
+//    rows (1 KB) and its codes in STAGES of 16 consecutive 128-k chunks
+//    (32 rows x 128 k = 2 KB each, contiguous in the prepacked layout
+//    [RB][C][4 slabs][32 rows][16 B]) plus their (alpha, beta) lines, each
+//    stage ONE cp.async.bulk into a 2..4-deep shared-memory ring. Compute
+//    warp w takes chunk w of every stage; lane L owns row L. Compute warps
+//    therefore never touch global memory and run no address / cursor code.
 //  * LUT lookup: the row's 16 fp16 values are expanded once per row block into
 //    a 256-entry pair table T2[byte] = (T[lo], T[hi]); entry e of lane L lives
 //    at shared address 0x10000 + e*256 + buf*128 + L*4. Every lookup of a warp
@@ -33,13 +34,14 @@
 //    barrier).
 //  * x enters once per batch: raw bf16 rows by cp.async.bulk, converted in
 //    place to the permuted fp16 image the code bytes index, plus per-chunk
-//    (2^-e, sum x). Problems of a batch that read the same x share the image.
+//    (2^-e, sum x). Problems of a batch that read the same x share the image;
+//    batches alternate between two image banks.
 //  * The writer warp reduces the 16 warp partials of an item in a fixed order
 //    and stores y; after a batch it releases it grid-wide (done[batch end]).
-//    A dependent problem reads its x only after every CTA released the batch
-//    before it, so x_i may be an earlier y_j; its weights already stream in.
-//    The grid is co-resident (cooperative launch), so the waits cannot
-//    deadlock.
+//    It also stages x: for a dependent batch it first waits until every CTA
+//    released the batch before (x_i may be an earlier y_j), while the weights
+//    of the batch already stream in. The grid is co-resident (cooperative
+//    launch), so the waits cannot deadlock.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -48,21 +50,19 @@
 #include "kernels.cuh"
 #include "lutgemm.cuh"
 
-#ifndef GV_WARPS
-#define GV_WARPS 16
-#endif
-#ifndef GV_RING
-#define GV_RING 2
-#endif
-
 namespace anyq_b200 {
 
 namespace {
 
-constexpr int kW = GV_WARPS;          // compute warps per CTA
-constexpr int kT = (kW + 1) * 32;     // + one writer warp
+constexpr int kW = 16;                // compute warps per CTA (one table slice each)
+constexpr int kWriterWarp = kW;
+constexpr int kProducerWarp = kW + 1;
+constexpr int kT = (kW + 2) * 32;
 constexpr int kMaxMP = 2;
-constexpr int kRing = GV_RING;         // TMA ring slots (2-KB chunks) per compute warp
+constexpr int kStageChunks = kW;      // chunks per ring stage: one per compute warp
+constexpr uint32_t kStageBytes = kStageChunks * 2048u;
+constexpr uint32_t kStageAb = kStageChunks * 128u;
+constexpr int kMaxRing = 4;
 constexpr int kMaxProb = 8;
 constexpr uint32_t kTblAddr = 0x10000;  // shared-window address of the pair table
 constexpr uint32_t kDynBase = 0x400;    // shared-window address of dynamic smem (sm_100)
@@ -70,6 +70,18 @@ constexpr uint32_t kPre = kTblAddr - kDynBase;  // bytes of dynamic smem before 
 constexpr uint32_t kTblBytes = 0x10000;
 constexpr uint32_t kSmemMax = 227u * 1024u;
 constexpr uint32_t kParamOff = 0;     // dynamic-smem copy of the parameter block
+
+// mbarriers (8 B each) at GvParams::bars
+constexpr uint32_t kBarRedFull = 0;    // [2] partials of an item ready (kW arrivals)
+constexpr uint32_t kBarRedEmpty = 16;  // [2] partials consumed by the writer (1)
+constexpr uint32_t kBarX = 32;         // x rows of a batch landed (writer + tx)
+constexpr uint32_t kBarTReady = 40;    // [2] pair-table buffer written (kW)
+constexpr uint32_t kBarTFree = 56;     // [2] pair-table buffer no longer read (kW)
+constexpr uint32_t kBarLFull = 72;     // [2] LUT rows of an item landed (producer + tx)
+constexpr uint32_t kBarLFree = 88;     // [2] LUT rows consumed (kW)
+constexpr uint32_t kBarSFull = 104;    // [kMaxRing] code stage landed (producer + tx)
+constexpr uint32_t kBarSEmpty = kBarSFull + 8 * kMaxRing;  // [kMaxRing] stage consumed (kW)
+constexpr uint32_t kBarBytes = kBarSEmpty + 8 * kMaxRing;
 
 struct GvProb {
   const uint4* codes;    // [RB][C][4][32] uint4
@@ -92,10 +104,12 @@ struct GvProb {
 struct GvParams {
   GvProb p[kMaxProb];
   int np, M, ncta;
+  int nring;             // code ring stages (2..kMaxRing)
   uint32_t red;          // dynamic-smem offset of the reduction buffer [2][kW][MP][32]
   uint32_t bars;         // dynamic-smem offset of the mbarriers
-  uint32_t ring;         // dynamic-smem offset of the code ring [kW][kRing][2048]
-  uint32_t abring;       // dynamic-smem offset of the (alpha, beta) ring [kW][kRing][128]
+  uint32_t ring[kMaxRing];  // dynamic-smem offsets of the code ring stages [16 chunks][2048]
+  uint32_t abring;       // dynamic-smem offset of the (alpha, beta) ring [nring][16][128]
+  uint32_t lutbuf;       // dynamic-smem offset of the LUT rows [2][32][32 B]
   int* done;             // [kMaxProb] batch release counters (self-resetting)
   int* err;              // device error word
   long long* trace;      // debug: [ncta][64] globaltimer stamps, or null
@@ -204,6 +218,10 @@ __device__ __forceinline__ long long gtimer() {
   do {                                                                             \
     if (P.trace && threadIdx.x == 0) P.trace[blockIdx.x * 64 + (slot)] = gtimer(); \
   } while (0)
+#define GV_TRACE_W(slot)                                        \
+  do {                                                          \
+    if (P.trace) P.trace[blockIdx.x * 64 + (slot)] = gtimer(); \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // Work items: (problem, row block), dealt round-robin per batch
@@ -237,33 +255,6 @@ __device__ __forceinline__ void item_next(const GvParams& P, int b, Item& it) {
   it.j += P.ncta;
   locate(P, b, it);
 }
-__device__ __forceinline__ void piece_of(int C, int warp, int& a, int& e) {
-  a = (warp * C) / kW;
-  e = ((warp + 1) * C) / kW;
-}
-
-// Weight-stream cursor of one compute warp over its chunk pieces of all items.
-struct Cursor {
-  Item it;
-  int lc, le, gshift;
-  const uint8_t* cg;     // global address of chunk lc (2 KB)
-  const uint8_t* abrow;  // global address of the row block's (alpha, beta) lines (128 B each)
-};
-
-__device__ __forceinline__ void settle(const GvParams& P, int b, int warp, Cursor& c) {
-  while (c.it.p < P.np) {
-    const GvProb& q = P.p[c.it.p];
-    piece_of(q.C, warp, c.lc, c.le);
-    if (c.lc < c.le) {
-      c.cg = reinterpret_cast<const uint8_t*>(q.codes) + ((size_t)c.it.rb * q.C + c.lc) * 2048;
-      c.abrow = reinterpret_cast<const uint8_t*>(q.ab) + (size_t)c.it.rb * q.GR * 128;
-      c.gshift = q.gshift;
-      return;
-    }
-    item_next(P, b, c.it);
-  }
-}
-
 struct Chunk {
   uint4 w[4];
   uint32_t ab;
@@ -394,15 +385,41 @@ __device__ __forceinline__ void prep_x(const GvProb& q, int M, uint8_t* smem, in
   }
 }
 
-// Writer warp: per item reduce the kW warp partials (fixed order) and store y;
-// after a batch release it grid-wide.
+// Writer warp: stages x per batch (after the batch it depends on was
+// released by every CTA), then per item reduces the kW warp partials (fixed
+// order) and stores y; after a batch releases it grid-wide.
 template <int MP>
-__device__ __forceinline__ void writer_loop(const GvParams& P, const float* red, uint32_t bar_full,
-                                            uint32_t bar_empty, int b, int lane) {
+__device__ __forceinline__ void writer_loop(const GvParams& P, const float* red, uint32_t bars,
+                                            uint32_t sbase, int b, int lane) {
+  const uint32_t bar_full = bars + kBarRedFull, bar_empty = bars + kBarRedEmpty;
+  const uint32_t bar_x = bars + kBarX;
   Item it = item_begin(P, b);
   int g = 0;
   for (int p0 = 0; p0 < P.np;) {
     const int p1 = P.p[p0].bend;
+    if (it.p <= p1) {  // this CTA has items in the batch: stage its x rows
+      if (lane == 0) {
+        if (P.p[p0].wait && p0 > 0) {
+          GV_TRACE_W(16 + p0);
+          wait_geq(&P.done[p0 - 1], P.ncta);
+          GV_TRACE_W(24 + p0);
+        }
+        // y of other CTAs (generic stores) is read below by the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        uint32_t bytes = 0;
+        for (int pp = p0; pp <= p1; ++pp)
+          if (P.p[pp].tma && !P.p[pp].dup) bytes += (uint32_t)P.M * P.p[pp].K * 2;
+        mbar_expect_tx(bar_x, bytes);
+        for (int pp = p0; pp <= p1; ++pp) {
+          const GvProb& r = P.p[pp];
+          if (!r.tma || r.dup) continue;
+          for (int m = 0; m < P.M; ++m)
+            bulk_g2s(sbase + r.xh + (uint32_t)m * r.K * 2, r.x + (size_t)m * r.K, (uint32_t)r.K * 2,
+                     bar_x);
+        }
+      }
+      __syncwarp();
+    }
     while (it.p <= p1) {
       const GvProb& q = P.p[it.p];
       const int par = g & 1;
@@ -443,6 +460,44 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
   }
 }
 
+// Producer (one lane): per item its LUT rows into lutbuf[g & 1], then its
+// codes stage by stage into the ring. Weights do not depend on the previous
+// kernel, so this runs before griddepcontrol.wait.
+__device__ __forceinline__ void producer_loop(const GvParams& P, uint32_t bars, uint32_t sbase,
+                                              int b) {
+  const uint32_t lfull = bars + kBarLFull, lfree = bars + kBarLFree;
+  const uint32_t sfull = bars + kBarSFull, sempty = bars + kBarSEmpty;
+  const uint32_t abring = sbase + P.abring, lutbuf = sbase + P.lutbuf;
+  Item it = item_begin(P, b);
+  int g = 0, slot = 0;
+  uint32_t round = 0;
+  while (it.p < P.np) {
+    const GvProb& q = P.p[it.p];
+    const int lb = g & 1;
+    if (g >= 2) mbar_wait(lfree + 8 * lb, (uint32_t)(((g >> 1) - 1) & 1));
+    mbar_expect_tx(lfull + 8 * lb, 1024);
+    bulk_g2s(lutbuf + lb * 1024, reinterpret_cast<const uint8_t*>(q.lut) + (size_t)it.rb * 1024, 1024,
+             lfull + 8 * lb);
+    const uint8_t* cg = reinterpret_cast<const uint8_t*>(q.codes) + (size_t)it.rb * q.C * 2048;
+    const uint8_t* ag = reinterpret_cast<const uint8_t*>(q.ab) + (size_t)it.rb * q.GR * 128;
+    for (int c0 = 0; c0 < q.C; c0 += kStageChunks) {
+      const int n = min(kStageChunks, q.C - c0);
+      const int g0 = c0 >> q.gshift, g1 = (c0 + n - 1) >> q.gshift;
+      if (round > 0) mbar_wait(sempty + 8 * slot, (round - 1) & 1);
+      mbar_expect_tx(sfull + 8 * slot, (uint32_t)n * 2048 + (uint32_t)(g1 - g0 + 1) * 128);
+      bulk_g2s(sbase + P.ring[slot], cg + (size_t)c0 * 2048, (uint32_t)n * 2048, sfull + 8 * slot);
+      bulk_g2s(abring + slot * kStageAb, ag + (size_t)g0 * 128, (uint32_t)(g1 - g0 + 1) * 128,
+               sfull + 8 * slot);
+      if (++slot == P.nring) {
+        slot = 0;
+        ++round;
+      }
+    }
+    item_next(P, b, it);
+    ++g;
+  }
+}
+
 template <int MP>
 __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvParams Pk) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -461,128 +516,78 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const GvParams& P = *reinterpret_cast<const GvParams*>(smem + kParamOff);
   __syncthreads();
-  const uint32_t bar_full = sbase + P.bars, bar_empty = bar_full + 16, bar_x = bar_full + 32;
-  // table hand-off: item g reads pair-table buffer g&1; tready = all slices of
-  // the buffer written, tfree = every compute warp finished reading it
-  const uint32_t tready = bar_full + 40, tfree = tready + 16;
-  const uint32_t rbar0 = bar_full + 72;  // [kW][kRing] weight-ring barriers
+  const uint32_t bars = sbase + P.bars;
   GV_TRACE(0);
   if (sbase != kDynBase) {  // the table must sit at shared address 0x10000
     if (threadIdx.x == 0) atomicMax(P.err, (int)ANYQ_ERR_INTERNAL);
     return;
   }
   if (threadIdx.x == 0) {
-    mbar_init(bar_full, kW);
-    mbar_init(bar_full + 8, kW);
-    mbar_init(bar_empty, 1);
-    mbar_init(bar_empty + 8, 1);
-    mbar_init(bar_x, 1);
     for (int j = 0; j < 2; ++j) {
-      mbar_init(tready + 8 * j, kW);
-      mbar_init(tfree + 8 * j, kW);
+      mbar_init(bars + kBarRedFull + 8 * j, kW);
+      mbar_init(bars + kBarRedEmpty + 8 * j, 1);
+      mbar_init(bars + kBarTReady + 8 * j, kW);
+      mbar_init(bars + kBarTFree + 8 * j, kW);
+      mbar_init(bars + kBarLFull + 8 * j, 1);
+      mbar_init(bars + kBarLFree + 8 * j, kW);
     }
-    for (int j = 0; j < kW * kRing; ++j) mbar_init(rbar0 + 8 * j, 1);
+    mbar_init(bars + kBarX, 1);
+    for (int j = 0; j < kMaxRing; ++j) {
+      mbar_init(bars + kBarSFull + 8 * j, 1);
+      mbar_init(bars + kBarSEmpty + 8 * j, kW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   float* red = reinterpret_cast<float*>(smem + P.red);
-  if (warp == kW) {
+  if (warp == kProducerWarp) {
+    if (lane == 0) producer_loop(P, bars, sbase, b);
+    return;
+  }
+  if (warp == kWriterWarp) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    writer_loop<MP>(P, red, bar_full, bar_empty, b, lane);
+    writer_loop<MP>(P, red, bars, sbase, b, lane);
     return;
   }
 
-  // ---- compute warps -------------------------------------------------------
-  // weight stream: each warp streams its chunk pieces with cp.async.bulk into
-  // its private ring (started before griddepcontrol.wait: weights do not
-  // depend on the previous kernel)
-  Item s = item_begin(P, b);
-  Cursor cur;
-  cur.it = s;
-  cur.lc = cur.le = 0;
-  cur.gshift = 0;
-  cur.cg = nullptr;
-  cur.abrow = nullptr;
-  settle(P, b, warp, cur);
-  const uint32_t ring = sbase + P.ring + (uint32_t)warp * kRing * 2048;
-  const uint32_t abring = sbase + P.abring + (uint32_t)warp * kRing * 128;
-  const uint32_t rbar = rbar0 + (uint32_t)warp * kRing * 8;
-  auto issue = [&](int slot) {  // next chunk of the cursor into `slot` (lane 0)
-    if (cur.it.p < P.np) {
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(rbar + 8 * slot, 2048 + 128);
-        bulk_g2s(ring + slot * 2048, cur.cg, 2048, rbar + 8 * slot);
-        bulk_g2s(abring + slot * 128, cur.abrow + ((cur.lc >> cur.gshift) << 7), 128, rbar + 8 * slot);
-      }
-      cur.cg += 2048;
-      if (++cur.lc >= cur.le) {
-        item_next(P, b, cur.it);
-        settle(P, b, warp, cur);
-      }
+  // ---- compute warps: shared memory only ------------------------------------
+  const uint32_t tready = bars + kBarTReady, tfree = bars + kBarTFree;
+  const uint32_t lfull = bars + kBarLFull, lfree = bars + kBarLFree;
+  const uint32_t sfull = bars + kBarSFull, sempty = bars + kBarSEmpty;
+  const uint32_t bar_full = bars + kBarRedFull, bar_empty = bars + kBarRedEmpty;
+  const uint32_t ring = sbase + (uint32_t)warp * 2048 + lane * 16;
+  const uint32_t abring = sbase + P.abring + laneoff;
+  const uint32_t lutrow = sbase + P.lutbuf + (uint32_t)lane * 32;
+  // pair table of item g from lutbuf[g & 1] into table buffer g & 1
+  auto table = [&](int gi) {
+    const int nb = gi & 1;
+    if (gi >= 2) mbar_wait(tfree + 8 * nb, (uint32_t)(((gi - 2) >> 1) & 1));
+    mbar_wait(lfull + 8 * nb, (uint32_t)((gi >> 1) & 1));
+    const uint4 l0 = lds128(lutrow + nb * 1024), l1 = lds128(lutrow + nb * 1024 + 16);
+    build_table(l0, l1, warp, nb, laneoff);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(lfree + 8 * nb);
+      mbar_arrive(tready + 8 * nb);
     }
   };
-  for (int j = 0; j < kRing; ++j) issue(j);
-  int nfetch = 0;  // chunks taken from the ring by this warp
-  auto fetch = [&](Chunk& ch) {
-    const int slot = nfetch % kRing;
-    mbar_wait(rbar + 8 * slot, (uint32_t)((nfetch / kRing) & 1));
-    const uint32_t a = ring + slot * 2048 + lane * 16;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) ch.w[q] = lds128(a + q * 512);
-    ch.ab = lds32(abring + slot * 128 + lane * 4);
-    __syncwarp();
-    issue(slot);
-    ++nfetch;
-  };
-
-  // pair tables: item s -> buffer 0 now; the LUT of the next item prefetched
+  Item s = item_begin(P, b);
   Item nx = s;
   item_next(P, b, nx);
-  auto lut_of = [&](const Item& it) { return P.p[it.p].lut + ((size_t)it.rb * 32 + lane) * 2; };
-  uint4 nl0 = make_uint4(0, 0, 0, 0), nl1 = nl0;
-  if (s.p < P.np) {
-    const uint4* lp = lut_of(s);
-    build_table(__ldg(lp), __ldg(lp + 1), warp, 0, laneoff);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(tready);
-  }
-  if (nx.p < P.np) {
-    const uint4* lp = lut_of(nx);
-    nl0 = __ldg(lp);
-    nl1 = __ldg(lp + 1);
-  }
+  if (s.p < P.np) table(0);
   GV_TRACE(1);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   int xbatch = 0;     // x batches staged so far (parity of bar_x)
   int xready = -1;    // x images are ready for problems <= xready
   int g = 0;          // items processed by this CTA
+  int slot = 0;       // ring stage
+  uint32_t round = 0;
   while (s.p < P.np) {
     const int p = s.p;
     const GvProb& q = P.p[p];
-    if (p > xready) {  // first item of a new batch: x images of the batch
+    if (p > xready) {  // first item of a new batch: convert its x rows
       const int p0 = q.bstart, p1 = q.bend;
-      if (P.p[p0].wait && p0 > 0) {  // every CTA must have released batch p0-1
-        GV_TRACE(16 + p0);
-        if (threadIdx.x == 0) wait_geq(&P.done[p0 - 1], P.ncta);
-        cw_sync();
-        GV_TRACE(24 + p0);
-      }
-      if (threadIdx.x == 0) {  // raw x rows by TMA (bypasses the L1 load queue)
-        uint32_t bytes = 0;
-        for (int pp = p0; pp <= p1; ++pp)
-          if (P.p[pp].tma && !P.p[pp].dup) bytes += (uint32_t)P.M * P.p[pp].K * 2;
-        mbar_expect_tx(bar_x, bytes);
-        for (int pp = p0; pp <= p1; ++pp) {
-          const GvProb& r = P.p[pp];
-          if (!r.tma || r.dup) continue;
-          for (int m = 0; m < P.M; ++m)
-            bulk_g2s(sbase + r.xh + (uint32_t)m * r.K * 2, r.x + (size_t)m * r.K, (uint32_t)r.K * 2,
-                     bar_x);
-        }
-      }
-      mbar_wait(bar_x, (uint32_t)(xbatch & 1));
+      mbar_wait(bars + kBarX, (uint32_t)(xbatch & 1));
       ++xbatch;
       int base = 0;  // conversion tasks of the batch dealt round-robin to the warps
       for (int pp = p0; pp <= p1; ++pp) {
@@ -596,25 +601,31 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
       cw_sync();
       GV_TRACE(2 + (p0 & 7));
     }
-    int a, e;
-    piece_of(q.C, warp, a, e);
     const uint32_t tb = kTblAddr | ((uint32_t)(g & 1) << 7) | laneoff;
     mbar_wait(tready + 8 * (g & 1), (uint32_t)((g >> 1) & 1));
     float y[MP];
 #pragma unroll
     for (int m = 0; m < MP; ++m) y[m] = 0.0f;
     const uint32_t xstride = (uint32_t)q.C * 256, xsstride = (uint32_t)q.C * 8;
-    uint32_t xa = sbase + q.xh + (uint32_t)a * 256, xsa = sbase + q.xs + (uint32_t)a * 8;
-    for (int c = a; c < e; ++c) {
+    const uint32_t xa0 = sbase + q.xh + (uint32_t)warp * 256, xsa0 = sbase + q.xs + (uint32_t)warp * 8;
+    for (int c0 = 0; c0 < q.C; c0 += kStageChunks) {
+      mbar_wait(sfull + 8 * slot, round & 1);
+      const int c = c0 + warp;
       Chunk ch;
-      fetch(ch);
-#ifdef GV_SKIPCOMPUTE
-      y[0] += __uint_as_float((ch.w[0].x ^ ch.w[1].y ^ ch.w[2].z ^ ch.w[3].w ^ ch.ab) & 0x3fffffff) * 1e-30f;
-#else
-      consume<MP>(ch, tb, xa, xsa, xstride, xsstride, y);
-#endif
-      xa += 256;
-      xsa += 8;
+      if (c < q.C) {
+        const uint32_t a = ring + P.ring[slot];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ch.w[j] = lds128(a + j * 512);
+        ch.ab = lds32(abring + slot * kStageAb + (uint32_t)(((c >> q.gshift) - (c0 >> q.gshift)) << 7));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + 8 * slot);  // release orders the reads above
+      if (c < q.C)
+        consume<MP>(ch, tb, xa0 + (uint32_t)c0 * 256, xsa0 + (uint32_t)c0 * 8, xstride, xsstride, y);
+      if (++slot == P.nring) {
+        slot = 0;
+        ++round;
+      }
     }
     // partial sums to the writer warp
     const int par = g & 1;
@@ -627,22 +638,8 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
       mbar_arrive(bar_full + 8 * par);
       mbar_arrive(tfree + 8 * (g & 1));  // done reading this item's table
     }
-    // the next item's table goes into the other buffer once every warp has
-    // finished the previous item
-    if (nx.p < P.np) {
-      const int nb = (g + 1) & 1;
-      if (g >= 1) mbar_wait(tfree + 8 * nb, (uint32_t)(((g - 1) >> 1) & 1));
-      build_table(nl0, nl1, warp, nb, laneoff);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tready + 8 * nb);
-      Item nn = nx;
-      item_next(P, b, nn);
-      if (nn.p < P.np) {
-        const uint4* lp = lut_of(nn);
-        nl0 = __ldg(lp);
-        nl1 = __ldg(lp + 1);
-      }
-    }
+    // the next item's table goes into the other buffer
+    if (nx.p < P.np) table(g + 1);
     if (g < 8) GV_TRACE(32 + g);
     s = nx;
     item_next(P, b, nx);
@@ -665,24 +662,7 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
   P.err = ts[0]->gv_err;
   P.done = ts[0]->gv_done;
   P.trace = g_gv_trace;
-  // placement: pieces go in front of the 64-KB table while they fit, else behind it
-  uint32_t front = kParamOff + (((uint32_t)sizeof(GvParams) + 255u) & ~255u);
-  uint32_t back = kPre + kTblBytes;
-  auto place = [&](uint32_t bytes) {
-    bytes = (bytes + 255u) & ~255u;
-    if (front + bytes <= kPre) {
-      const uint32_t o = front;
-      front += bytes;
-      return o;
-    }
-    const uint32_t o = back;
-    back += bytes;
-    return o;
-  };
-  P.ring = place((uint32_t)kW * kRing * 2048);
-  P.bars = place(72 + (uint32_t)kW * kRing * 8);
-  P.abring = place((uint32_t)kW * kRing * 128);
-  P.red = place(2u * kW * MP * 32 * 4);
+  // batches and x-image sharing
   for (int i = 0; i < n; ++i) {
     const LutTensor* t = ts[i];
     if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");
@@ -707,19 +687,12 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
     q.tma = (q.K % 128 == 0) && ((reinterpret_cast<uintptr_t>(xs[i]) & 15) == 0);
     q.bstart = (i == 0 || q.wait) ? i : P.p[i - 1].bstart;
     q.rboff = (q.bstart == i) ? 0 : P.p[i - 1].rboff + P.p[i - 1].RB;
-    // problems of one batch that read the same x share its image
     q.dup = 0;
     for (int j = q.bstart; j < i; ++j) {
       if (P.p[j].x == q.x && P.p[j].K == q.K && !P.p[j].dup) {
-        q.dup = 1;
-        q.xs = P.p[j].xs;
-        q.xh = P.p[j].xh;
+        q.dup = 1 + j;  // (index of the owner) + 1, resolved below
         break;
       }
-    }
-    if (!q.dup) {
-      q.xs = place((uint32_t)MP * t->C * 8);
-      q.xh = place((uint32_t)MP * t->C * 256);
     }
   }
   for (int i = n - 1; i >= 0; --i) {
@@ -730,9 +703,84 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
     GvProb& q = P.p[i];
     q.btot = P.p[q.bend].rboff + P.p[q.bend].RB;
   }
-  if (back > kSmemMax)
-    fail(ANYQ_ERR_SHAPE, "LUT GEMV chain: x images exceed shared memory (" + std::to_string(back) +
-                             " > " + std::to_string(kSmemMax) + " B)");
+  // x images: batches alternate between two banks (batch b+2 is staged only
+  // after every CTA released batch b+1, so nobody still reads batch b's bank)
+  auto img_bytes = [&](const GvProb& q) {
+    return (((uint32_t)MP * q.C * 8 + 255u) & ~255u) + (((uint32_t)MP * q.C * 256 + 255u) & ~255u);
+  };
+  uint32_t bank_need[2] = {0, 0};
+  int bidx[kMaxProb];
+  for (int i = 0, bi = -1; i < n; ++i) {
+    if (P.p[i].bstart == i) ++bi;
+    bidx[i] = bi;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (P.p[i].bstart != i) continue;
+    uint32_t need = 0;
+    for (int j = i; j <= P.p[i].bend; ++j)
+      if (!P.p[j].dup) need += img_bytes(P.p[j]);
+    bank_need[bidx[i] & 1] = std::max(bank_need[bidx[i] & 1], need);
+  }
+  // placement: pieces go in front of the 64-KB table while they fit, else behind it
+  uint32_t front = kParamOff + (((uint32_t)sizeof(GvParams) + 255u) & ~255u);
+  uint32_t back = kPre + kTblBytes;
+  auto place = [&](uint32_t bytes) {
+    bytes = (bytes + 255u) & ~255u;
+    if (front + bytes <= kPre) {
+      const uint32_t o = front;
+      front += bytes;
+      return o;
+    }
+    const uint32_t o = back;
+    back += bytes;
+    return o;
+  };
+  P.bars = place(kBarBytes);
+  P.lutbuf = place(2048);
+  P.red = place(2u * kW * MP * 32 * 4);
+  uint32_t bank_off[2];
+  for (int k = 0; k < 2; ++k) bank_off[k] = bank_need[k] ? place(bank_need[k]) : 0;
+  for (int i = 0; i < n; ++i) {
+    if (P.p[i].bstart != i) continue;
+    uint32_t o = bank_off[bidx[i] & 1];
+    for (int j = i; j <= P.p[i].bend; ++j) {
+      GvProb& q = P.p[j];
+      if (q.dup) continue;
+      q.xs = o;
+      q.xh = o + (((uint32_t)MP * q.C * 8 + 255u) & ~255u);
+      o += img_bytes(q);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    GvProb& q = P.p[i];
+    if (q.dup) {
+      const GvProb& own = P.p[q.dup - 1];
+      q.xs = own.xs;
+      q.xh = own.xh;
+      q.dup = 1;
+    }
+  }
+  // the code ring takes what is left: as many 32-KB stages as fit (2..4),
+  // each stage in front of the table if it still fits there
+  P.nring = 0;
+  for (int r = kMaxRing; r >= 2 && !P.nring; --r) {
+    const uint32_t f0 = front, b0 = back;
+    uint32_t ro[kMaxRing] = {0, 0, 0, 0};
+    for (int j = 0; j < r; ++j) ro[j] = place(kStageBytes);
+    const uint32_t ao = place((uint32_t)r * kStageAb);
+    if (back <= kSmemMax) {
+      P.nring = r;
+      for (int j = 0; j < kMaxRing; ++j) P.ring[j] = ro[j];
+      P.abring = ao;
+    } else {
+      front = f0;
+      back = b0;
+    }
+  }
+  if (!P.nring)
+    fail(ANYQ_ERR_SHAPE, "LUT GEMV chain: x images leave no room for the weight ring (" +
+                             std::to_string(back + 2 * (kStageBytes + kStageAb)) + " > " +
+                             std::to_string(kSmemMax) + " B)");
   return back;
 }
 
