@@ -107,6 +107,18 @@ int64_t group_count(const anyq_config& c, int64_t rows, int64_t cols) {
   fail(ANYQ_ERR_CONFIG, "unknown granularity");
 }
 
+void keep_default_pool() {
+  static int done_dev = -1;
+  int dev = 0;
+  ANYQ_CUDA(cudaGetDevice(&dev));
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  ANYQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;
+  ANYQ_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done_dev = dev;
+}
+
 void check_device_error(const int* d_err, const char* what) {
   int h = 0;
   ANYQ_CUDA(cudaMemcpy(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -166,21 +178,21 @@ static void quantize_device(const float* w, int64_t rows, int64_t cols, const an
   validate_config(cfg, rows, cols);
   float qmin, qmax;
   table_range(cfg, &qmin, &qmax);
-  DevBuf<int> err(1);
+  DevBuf<int> err(1, s);
   ANYQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
   launch_check_finite(w, rows * cols, err.p, ANYQ_ERR_NONFINITE, s);
   ANYQ_CUDA(cudaStreamSynchronize(s));
   check_device_error(err.p, cfg.codebook == ANYQ_CB_ANY ? "quantize_any" : "quantize_fixed");
   launch_scales(w, rows, cols, cfg, qmin, qmax, alphas, betas, s);
-  DevBuf<float> ws(rows * cols), sw;
-  DevBuf<uint8_t> codes(rows * cols);
+  DevBuf<float> ws(rows * cols, s), sw;
+  DevBuf<uint8_t> codes(rows * cols, s);
   if (cfg.codebook == ANYQ_CB_ANY) {
     if (exj) {
       launch_check_stats(exj, cols, err.p, s);
       ANYQ_CUDA(cudaStreamSynchronize(s));
       check_device_error(err.p, "sample weights");
     }
-    sw.alloc(rows * cols);
+    sw.alloc(rows * cols, s);
     launch_scale_rows(w, rows, cols, cfg, alphas, betas, exj, ws.p, sw.p, err.p, s);
     ANYQ_CUDA(cudaStreamSynchronize(s));
     check_device_error(err.p, "KmProblem");

@@ -250,19 +250,37 @@ Table int_grid_table(int bits, bool shifted);       // codebooks.cpp:8-19
 void validate_config(const anyq_config& c, int64_t rows, int64_t cols);  // core.hpp:124-142
 int64_t group_count(const anyq_config& c, int64_t rows, int64_t cols);   // scaling.cpp:8-24
 
-// Device scratch buffers with RAII.
+// Keep freed stream-ordered allocations cached in the device's default pool
+// (no cudaFree / unmap on the hot path).
+void keep_default_pool();
+
+// Device scratch buffers with RAII. With a stream, allocation and release are
+// stream-ordered (cudaMallocAsync / cudaFreeAsync from the cached pool).
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;
+  bool async = false;
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(size_t count, cudaStream_t s) { alloc(count, s); }
   void alloc(size_t count) {
     n = count;
     if (count) ANYQ_CUDA(cudaMalloc(&p, sizeof(T) * count));
   }
+  void alloc(size_t count, cudaStream_t s) {
+    n = count;
+    st = s;
+    async = true;
+    keep_default_pool();
+    if (count) ANYQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+  }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (async) cudaFreeAsync(p, st);
+      else cudaFree(p);
+    }
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;

@@ -24,6 +24,8 @@
 // the cumulative-mass sampling selects the same sample as the reference; the
 // RNG stream (core.hpp:164-200) is reproduced bit for bit.
 #include <cub/cub.cuh>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -52,6 +54,8 @@ struct KmParams {
   uint8_t* gscratch;  // per-block scratch when the row does not fit in smem
   size_t scratch_stride;
   int use_smem;
+  const int* row_list;  // if set: process rows row_list[0 .. *row_list_n)
+  const int* row_list_n;
 };
 
 struct Part {  // partial segment sums
@@ -562,7 +566,11 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
   const int64_t b = threadIdx.x * C, e = min(n, b + C);
 
   while (true) {
-    if (threadIdx.x == 0) sh.row = atomicAdd(P.row_counter, 1);
+    if (threadIdx.x == 0) {
+      const int64_t i = atomicAdd(P.row_counter, 1);
+      if (P.row_list) sh.row = i < *P.row_list_n ? P.row_list[i] : P.rows;
+      else sh.row = i;
+    }
     __syncthreads();
     const int64_t row = sh.row;
     if (row >= P.rows) break;
@@ -619,6 +627,759 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
   }
 }
 
+// ===========================================================================
+// Warp-per-row Lloyd (k <= 16): one warp learns one row at a time, no block
+// barriers. Same semantics as k_kmeans_rows (learner.cpp:132-369), with the
+// E-step done as a search for the k-1 segment boundaries of the sorted row:
+// for distinct centroid values the exact-rounded nearest rank is monotone in
+// x (costs are monotone in |x - c| after rounding and a tie between the two
+// bracketing centroids picks the same index across the whole tie zone), so
+// seg[t] = first sorted position whose nearest rank is >= t is found by
+// binary search with the reference predicate itself — O(k log n) per
+// iteration instead of O(n k). Rows where two centroids come within 2^-40 of
+// the data range (where a 3-way rounding tie could break monotonicity), k > 16
+// or check_invariants go to k_kmeans_rows instead (bail list).
+// The M-step and the loss scan each lane's contiguous chunk of the sorted
+// row (stored lane-interleaved in shared memory: conflict free) and combine
+// chunks in a fixed order; empty-cluster repairs, the changed test against
+// the repaired assignment, convergence and restarts follow the reference.
+// ===========================================================================
+constexpr int kWK = 16;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct WarpKm {
+  double cen[kWK], best_cen[kWK], sv[kWK];
+  double swx[kWK], sw[kWK], sx[kWK];
+  double fpart[32][3], lpart[32][3];
+  int so[kWK], rank_of[kWK], cnt[kWK];
+  int seg[kWK + 1], pseg[kWK + 1], pso[kWK];
+  int exc_pos[kWK], exc_q[kWK], pexc_pos[kWK], pexc_q[kWK];
+  int nexc, pnexc;
+  int fc[32], lc[32];
+  long long vkeys[2 * kWK], vvals[2 * kWK];
+  Rng rng;
+  int ncen;
+};
+
+struct WkParams {
+  const float* ws;     // rows x n, original order
+  const float* sw;     // rows x n, original order
+  const float* skeys;  // rows x n, sorted values
+  const int* svals;    // rows x n, original index of each sorted position
+  int64_t rows;
+  int n, C, k, init, max_iters, restarts;
+  float rel_tol;
+  uint64_t seed;
+  int64_t row_offset;
+  float* luts;
+  uint8_t* codes;
+  int* err;
+  int* row_counter;
+  double* d2scr;       // [total warps][C * 32] k-means++ D^2, lane-interleaved
+  int* bail_rows;      // rows handed to k_kmeans_rows
+  int* bail_n;
+  uint32_t warp_bytes;  // dynamic smem per warp
+  long long* dbg;       // debug counters [8] (ANYQ_KM_DEBUG), or null
+};
+
+__device__ __forceinline__ double w_sum(double v) {  // fixed tree to lane 0, broadcast
+  for (int off = 16; off; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(kFull, v, off));
+  return __shfl_sync(kFull, v, 0);
+}
+__device__ __forceinline__ double w_scan_excl(double v, int lane, double* total) {
+  double incl = v;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double o = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl = __dadd_rn(o, incl);
+  }
+  *total = __shfl_sync(kFull, incl, 31);
+  const double ex = __shfl_up_sync(kFull, incl, 1);
+  return lane == 0 ? 0.0 : ex;
+}
+__device__ __forceinline__ long long w_min_ll(long long v) {
+  for (int off = 16; off; off >>= 1) v = min(v, __shfl_xor_sync(kFull, v, off));
+  return v;
+}
+__device__ __forceinline__ long long w_max_ll(long long v) {
+  for (int off = 16; off; off >>= 1) v = max(v, __shfl_xor_sync(kFull, v, off));
+  return v;
+}
+__device__ __forceinline__ double w_bcast_rng(WarpKm& S, int lane) {
+  double u = 0.0;
+  if (lane == 0) u = S.rng.next_double();
+  return __shfl_sync(kFull, u, 0);
+}
+
+__device__ __forceinline__ void w_sort(WarpKm& S, int k, int lane) {
+  __syncwarp();
+  if (lane < k) {
+    const double v = S.cen[lane];
+    int r = 0;
+    for (int p = 0; p < k; ++p) {
+      const double u = S.cen[p];
+      r += (u < v) || (u == v && p < lane);
+    }
+    S.rank_of[lane] = r;
+    S.sv[r] = v;
+    S.so[r] = lane;
+  }
+  __syncwarp();
+}
+
+// Exact reference nearest centroid (ties to the smallest original index).
+__device__ __forceinline__ int w_nearest(double x, const WarpKm& S, int k) {
+  int lo = 0, hi = k;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (S.sv[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  const int p = lo;
+  const double cl = p > 0 ? dcost(x, S.sv[p - 1]) : INFINITY;
+  const double cr = p < k ? dcost(x, S.sv[p]) : INFINITY;
+  const double mc = cl < cr ? cl : cr;
+  int best = 1 << 30;
+  for (int r = p - 1; r >= 0; --r) {
+    const double c = (r == p - 1) ? cl : dcost(x, S.sv[r]);
+    if (!(c == mc)) break;
+    best = min(best, S.so[r]);
+  }
+  for (int r = p; r < k; ++r) {
+    const double c = (r == p) ? cr : dcost(x, S.sv[r]);
+    if (!(c == mc)) break;
+    best = min(best, S.so[r]);
+  }
+  return best;
+}
+
+// Row buffers of one warp: element j of lane l's contiguous chunk
+// [l*C, l*C + C) lives at j*33 + l (padded rows: bank (j + l) % 32) — conflict
+// free both for lanes walking their chunks in step and for coalesced whole-row
+// loads, and linear in j (immediate offsets in the unrolled loops).
+__device__ __forceinline__ int sw_idx(int l, int j) { return j * 33 + l; }
+
+struct WRow {
+  const float* xs;  // sorted samples (Lloyd) / original order (k-means++)
+  const float* wv;  // their weights
+  int n, C, lo, hi;
+  __device__ __forceinline__ float x_at(int p) const {
+    const int l = p / C;
+    return xs[sw_idx(l, p - l * C)];
+  }
+};
+
+// Whole-row load into the swizzled layout (coalesced global reads).
+template <typename F>
+__device__ __forceinline__ void w_load_row(int n, int C, int lane, F&& put) {
+  int l = 0, j = lane;
+  while (j >= C) {
+    j -= C;
+    ++l;
+  }
+  for (int p = lane; p < n; p += 32) {
+    put(p, sw_idx(l, j));
+    j += 32;
+    while (j >= C) {
+      j -= C;
+      ++l;
+    }
+  }
+}
+
+// label of sorted position p under segments seg/so
+__device__ __forceinline__ int w_label_seg(const int* seg, const int* so, int k, int p) {
+  int r = 0;
+  while (r < k - 1 && seg[r + 1] <= p) ++r;
+  return so[r];
+}
+
+// m-th distinct sorted sample value, cycling (pad_with_distinct); global sorted row
+__device__ double w_distinct_value(const float* sk, int n, int64_t m) {
+  int64_t nd = 0;
+  for (int j = 0; j < n; ++j)
+    if (j == 0 || !((double)sk[j] == (double)sk[j - 1])) ++nd;
+  int64_t want = m % nd, seen = -1;
+  for (int j = 0; j < n; ++j)
+    if (j == 0 || !((double)sk[j] == (double)sk[j - 1]))
+      if (++seen == want) return (double)sk[j];
+  return (double)sk[0];
+}
+
+// Cumulative-mass sampling (learner.cpp:64-75) over this lane's chunk of
+// ORIGINAL indices: first hit over lanes, else the last positive index.
+template <int kMode>  // 0: mass = w, 1: mass = w * d2, 2: mass = d2
+__device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, int lane, double excl,
+                                              double r) {
+  long long cand = LLONG_MAX, lastpos = -1;
+  double acc = excl;
+  const int cnt = R.hi - R.lo;
+  auto mass = [&](int j) {
+    if (kMode == 0) return (double)R.wv[sw_idx(lane, j)];
+    if (kMode == 1) return __dmul_rn((double)R.wv[sw_idx(lane, j)], d2[j * 32 + lane]);
+    return d2[j * 32 + lane];
+  };
+  for (int j0 = 0; j0 < cnt && cand == LLONG_MAX; j0 += 16) {
+    double mv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) mv[u] = (j0 + u < cnt) ? mass(j0 + u) : 0.0;  // loads first
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (cand != LLONG_MAX || !(mv[u] > 0.0)) continue;
+      acc = __dadd_rn(acc, mv[u]);
+      lastpos = R.lo + j0 + u;
+      if (r < acc) cand = R.lo + j0 + u;
+    }
+  }
+  if (cand != LLONG_MAX) {  // lastpos = last positive index of the chunk
+    for (int j = cnt - 1; j >= 0; --j)
+      if (mass(j) > 0.0) {
+        lastpos = R.lo + j;
+        break;
+      }
+  }
+  const long long c = w_min_ll(cand);
+  const long long lp = w_max_ll(lastpos);
+  return c != LLONG_MAX ? c : (lp >= 0 ? lp : 0);
+}
+
+// k-means++ (learner.cpp:132-174): R holds the row in ORIGINAL order; D^2 in
+// global scratch (lane-interleaved, coalesced).
+__device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& S, int k, int lane) {
+  const int cnt = R.hi - R.lo;
+  double part = 0.0, total;
+  for (int j = 0; j < cnt; ++j) {
+    const double m = (double)R.wv[sw_idx(lane, j)];
+    if (m > 0.0) part = __dadd_rn(part, m);
+  }
+  double excl = w_scan_excl(part, lane, &total);
+  double u = w_bcast_rng(S, lane);
+  long long pick = w_sample<0>(R, d2, lane, excl, __dmul_rn(u, total));
+  if (lane == 0) {
+    S.cen[0] = (double)R.x_at((int)pick);
+    S.ncen = 1;
+  }
+  for (int j = 0; j < cnt; ++j) d2[j * 32 + lane] = INFINITY;
+  __syncwarp();
+  while (S.ncen < k) {
+    const double c = S.cen[S.ncen - 1];
+    part = 0.0;
+    for (int j0 = 0; j0 < cnt; j0 += 16) {
+      double dv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) dv[u] = d2[min(j0 + u, cnt - 1) * 32 + lane];  // loads first
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (j0 + u >= cnt) break;
+        const int si = sw_idx(lane, j0 + u);
+        const double pc = dcost((double)R.xs[si], c);
+        const double d = (pc < dv[u]) ? pc : dv[u];
+        d2[(j0 + u) * 32 + lane] = d;
+        const double m = __dmul_rn((double)R.wv[si], d);
+        if (m > 0.0) part = __dadd_rn(part, m);
+      }
+    }
+    excl = w_scan_excl(part, lane, &total);
+    if (total > 0.0) {
+      u = w_bcast_rng(S, lane);
+      pick = w_sample<1>(R, d2, lane, excl, __dmul_rn(u, total));
+      if (lane == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
+      __syncwarp();
+      continue;
+    }
+    part = 0.0;
+    for (int j = 0; j < cnt; ++j) {
+      const double m = d2[j * 32 + lane];
+      if (m > 0.0) part = __dadd_rn(part, m);
+    }
+    excl = w_scan_excl(part, lane, &total);
+    if (total > 0.0) {
+      u = w_bcast_rng(S, lane);
+      pick = w_sample<2>(R, d2, lane, excl, __dmul_rn(u, total));
+      if (lane == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
+      __syncwarp();
+      continue;
+    }
+    if (lane == 0) {
+      int64_t cursor = 0;
+      while (S.ncen < k) S.cen[S.ncen++] = w_distinct_value(sk, R.n, cursor++);
+    }
+    __syncwarp();
+  }
+}
+
+// random_init (learner.cpp:86-103); R holds the row in ORIGINAL order.
+__device__ void w_init_random(const WRow& R, const float* sk, WarpKm& S, int k, int lane) {
+  if (lane == 0) {
+    const int64_t n = R.n;
+    if ((int64_t)k >= n) {
+      int c = 0;
+      for (int64_t j = 0; j < n; ++j) S.cen[c++] = (double)sk[j];
+      int64_t cursor = 0;
+      while (c < k) S.cen[c++] = w_distinct_value(sk, R.n, cursor++);
+    } else {
+      int used = 0;
+      auto get = [&](long long pos) -> long long {
+        for (int i = 0; i < used; ++i)
+          if (S.vkeys[i] == pos) return S.vvals[i];
+        return pos;
+      };
+      auto set = [&](long long pos, long long v) {
+        for (int i = 0; i < used; ++i)
+          if (S.vkeys[i] == pos) {
+            S.vvals[i] = v;
+            return;
+          }
+        S.vkeys[used] = pos;
+        S.vvals[used] = v;
+        ++used;
+      };
+      for (int t = 0; t < k; ++t) {
+        const long long pick = t + S.rng.next_index(n - t);
+        const long long vt = get(t), vp = get(pick);
+        set(t, vp);
+        set(pick, vt);
+        S.cen[t] = (double)R.x_at((int)vp);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// One Lloyd run (learner.cpp:207-312). Returns the final loss (or 0 when
+// not needed); *bail = 1 when the row must go to the CTA kernel.
+__device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int* svals_row,
+                          int lane, bool need_loss, int* bail) {
+  const int n = R.n, C = R.C, k = P.k, lo = R.lo, hi = R.hi;
+  // data range for the monotonicity guard
+  const double xmax = fmax(fabs((double)R.x_at(0)), fabs((double)R.x_at(n - 1)));
+  double prev = INFINITY;
+  for (int iter = 0; iter < P.max_iters; ++iter) {
+    long long tph = clock64();
+    // ---- E-step: segment boundaries by binary search on the nearest rank
+    w_sort(S, k, lane);
+    {
+      double cmax = 0.0;
+      bool near_dup = false;
+      for (int r = 0; r < k; ++r) cmax = fmax(cmax, fabs(S.sv[r]));
+      const double thresh = ldexp(xmax + cmax, -40);
+      for (int r = 0; r + 1 < k; ++r) {
+        const double g = __dsub_rn(S.sv[r + 1], S.sv[r]);
+        near_dup |= (g > 0.0 && g < thresh) || !(g >= 0.0);
+      }
+      if (near_dup) {
+        *bail = 1;
+        return 0.0;
+      }
+    }
+    if (lane >= 1 && lane < k) {
+      // seg[lane] = first sorted position whose nearest rank is >= lane
+      auto rank_at = [&](int p) { return S.rank_of[w_nearest((double)R.x_at(p), S, k)]; };
+      int a = 0, b = n;
+      bool done = false;
+      if (S.sv[lane - 1] < S.sv[lane]) {
+        // distinct neighbours: the switch sits at the midpoint up to rounding;
+        // locate it by value, then settle it with the exact predicate
+        const double mid = 0.5 * S.sv[lane - 1] + 0.5 * S.sv[lane];
+        // first chunk whose first sample is >= mid, then inside the chunk before it
+        const int nl = (n + C - 1) / C;
+        int la = 0, lb = nl;
+        while (la < lb) {
+          const int m = (la + lb) >> 1;
+          if ((double)R.xs[sw_idx(m, 0)] < mid) la = m + 1;
+          else lb = m;
+        }
+        int lo2 = 0;
+        if (la > 0) {
+          const int l = la - 1, cntl = min(C, n - l * C);
+          int ja = 0, jb = cntl;
+          while (ja < jb) {
+            const int m = (ja + jb) >> 1;
+            if ((double)R.xs[sw_idx(l, m)] < mid) ja = m + 1;
+            else jb = m;
+          }
+          lo2 = l * C + ja;
+        }
+        int p = lo2, steps = 0;
+        while (p > 0 && steps < 8 && rank_at(p - 1) >= lane) --p, ++steps;
+        while (p < n && steps < 8 && rank_at(p) < lane) ++p, ++steps;
+        if (steps < 8) {
+          a = p;
+          done = true;
+        }
+      }
+      if (!done) {
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (rank_at(mid) >= lane) b = mid;
+          else a = mid + 1;
+        }
+      }
+      S.seg[lane] = a;
+    }
+    if (lane == 0) {
+      S.seg[0] = 0;
+      S.seg[k] = n;
+    }
+    __syncwarp();
+    int changed = 0;
+    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[4], (unsigned long long)(tt - tph)); tph = tt; }
+    // ---- M-step: per-lane runs over the lane's chunk, combined in chunk order
+    {
+      // runs of the lane's chunk: [p, pend) inside segment r (label so[r])
+      int r = 0, nr = 0, fcq = -1, lcq = -1;
+      for (int p = lo; p < hi;) {
+        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
+        const int pend = min(hi, S.seg[r + 1]);
+        const int q = S.so[r];
+        // four interleaved partial sums per quantity (fixed order: ILP for the
+        // 8-cycle DADD chain), folded at the end of the run
+        double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0}, b2[4] = {0.0, 0.0, 0.0, 0.0};
+        int j = p - lo;
+        const int je = pend - lo;
+        for (; j + 8 <= je; j += 8) {  // loads first, then the sums
+          float xv[8], wq[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            xv[u] = R.xs[sw_idx(lane, j + u)];
+            wq[u] = R.wv[sw_idx(lane, j + u)];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double w = (double)wq[u], x = (double)xv[u];
+            b0[u & 3] = __dadd_rn(b0[u & 3], __dmul_rn(w, x));
+            b1[u & 3] = __dadd_rn(b1[u & 3], w);
+            b2[u & 3] = __dadd_rn(b2[u & 3], x);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // remainder (< 8), constant register indices
+          if (j + u < je) {
+            const double w = (double)R.wv[sw_idx(lane, j + u)], x = (double)R.xs[sw_idx(lane, j + u)];
+            b0[u & 3] = __dadd_rn(b0[u & 3], __dmul_rn(w, x));
+            b1[u & 3] = __dadd_rn(b1[u & 3], w);
+            b2[u & 3] = __dadd_rn(b2[u & 3], x);
+          }
+        }
+        const double a0 = __dadd_rn(__dadd_rn(b0[0], b0[1]), __dadd_rn(b0[2], b0[3]));
+        const double a1 = __dadd_rn(__dadd_rn(b1[0], b1[1]), __dadd_rn(b1[2], b1[3]));
+        const double a2 = __dadd_rn(__dadd_rn(b2[0], b2[1]), __dadd_rn(b2[2], b2[3]));
+        if (nr == 0) {
+          S.fpart[lane][0] = a0;
+          S.fpart[lane][1] = a1;
+          S.fpart[lane][2] = a2;
+          fcq = q;
+        } else if (pend < hi) {  // interior run: the whole cluster lies in this chunk
+          S.swx[q] = a0;
+          S.sw[q] = a1;
+          S.sx[q] = a2;
+        } else {
+          S.lpart[lane][0] = a0;
+          S.lpart[lane][1] = a1;
+          S.lpart[lane][2] = a2;
+          lcq = q;
+        }
+        ++nr;
+        p = pend;
+      }
+      S.fc[lane] = fcq;
+      S.lc[lane] = lcq;
+      __syncwarp();
+      if (lane < k) {
+        const int q = lane;
+        const int rq = S.rank_of[q];
+        const int a = S.seg[rq], z = S.seg[rq + 1];
+        S.cnt[q] = z - a;
+        if (z > a) {
+          const int t0 = a / C, t1 = (z - 1) / C;
+          const bool starts_chunk = a == t0 * C;
+          const bool ends_chunk = z == min(n, (t0 + 1) * C);
+          if (t0 == t1) {
+            if (starts_chunk) {
+              S.swx[q] = S.fpart[t0][0];
+              S.sw[q] = S.fpart[t0][1];
+              S.sx[q] = S.fpart[t0][2];
+            } else if (ends_chunk) {
+              S.swx[q] = S.lpart[t0][0];
+              S.sw[q] = S.lpart[t0][1];
+              S.sx[q] = S.lpart[t0][2];
+            }  // else: interior run, already complete
+          } else {
+            const double* f0 = starts_chunk ? S.fpart[t0] : S.lpart[t0];
+            double s0 = f0[0], s1 = f0[1], s2 = f0[2];
+            for (int t = t0 + 1; t <= t1; ++t) {
+              s0 = __dadd_rn(s0, S.fpart[t][0]);
+              s1 = __dadd_rn(s1, S.fpart[t][1]);
+              s2 = __dadd_rn(s2, S.fpart[t][2]);
+            }
+            S.swx[q] = s0;
+            S.sw[q] = s1;
+            S.sx[q] = s2;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < k && S.cnt[lane] > 0) {
+        const int q = lane;
+        if (S.sw[q] > 0.0) S.cen[q] = __ddiv_rn(S.swx[q], S.sw[q]);
+        else S.cen[q] = __ddiv_rn(S.sx[q], (double)S.cnt[q]);
+      }
+      __syncwarp();
+    }
+    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[5], (unsigned long long)(tt - tph)); tph = tt; }
+    // ---- empty-cluster repair (learner.cpp:260-274), in cluster order
+    if (lane == 0) S.nexc = 0;
+    __syncwarp();
+    const unsigned empties = __ballot_sync(kFull, lane < k && S.cnt[lane] == 0);
+    for (unsigned em = empties; em; em &= em - 1) {
+      const int q = __ffs(em) - 1;
+      double worst = -1.0;
+      int wp = -1;
+      long long wo_i = LLONG_MAX;
+      int r = 0;
+      while (r < k - 1 && S.seg[r + 1] <= lo) ++r;
+      for (int p = lo, j = 0; p < hi; ++p, ++j) {
+        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
+        int lab = S.so[r];
+        for (int e = 0; e < S.nexc; ++e)
+          if (S.exc_pos[e] == p) lab = S.exc_q[e];
+        const double err = __dmul_rn((double)R.wv[sw_idx(lane, j)], dcost((double)R.xs[sw_idx(lane, j)], S.cen[lab]));
+        if (err > worst) {
+          worst = err;
+          wp = p;
+          wo_i = LLONG_MAX;
+        } else if (err == worst) {
+          if (wo_i == LLONG_MAX) wo_i = svals_row[wp];
+          const long long oi = svals_row[p];
+          if (oi < wo_i) {
+            wp = p;
+            wo_i = oi;
+          }
+        }
+      }
+      if (wp >= 0 && wo_i == LLONG_MAX) wo_i = svals_row[wp];
+      // warp argmax (err), ties to the smallest original index
+      for (int off = 16; off; off >>= 1) {
+        const double oe = __shfl_down_sync(kFull, worst, off);
+        const long long oo = __shfl_down_sync(kFull, wo_i, off);
+        const int op = __shfl_down_sync(kFull, wp, off);
+        if (lane + off < 32 && (oe > worst || (oe == worst && oo < wo_i))) {
+          worst = oe;
+          wo_i = oo;
+          wp = op;
+        }
+      }
+      if (lane == 0) {
+        S.cen[q] = (double)R.x_at(wp);
+        int e = 0;
+        while (e < S.nexc && S.exc_pos[e] != wp) ++e;
+        S.exc_pos[e] = wp;
+        S.exc_q[e] = q;
+        if (e == S.nexc) ++S.nexc;
+      }
+      __syncwarp();
+    }
+    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[6], (unsigned long long)(tt - tph)); tph = tt; }
+    // ---- loss after the update (chunk order, then fixed tree)
+    double loss_m;
+    {
+      double lb[4] = {0.0, 0.0, 0.0, 0.0};
+      const int nexc = S.nexc;
+      int r = 0;
+      for (int p = lo; p < hi;) {
+        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
+        const int pend = min(hi, S.seg[r + 1]);
+        const double c = S.cen[S.so[r]];
+        int j = p - lo;
+        const int je = pend - lo;
+        if (nexc == 0) {
+          for (; j + 8 <= je; j += 8) {
+            float xv[8], wq[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              xv[u] = R.xs[sw_idx(lane, j + u)];
+              wq[u] = R.wv[sw_idx(lane, j + u)];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              lb[u & 3] = __dadd_rn(lb[u & 3], __dmul_rn((double)wq[u], dcost((double)xv[u], c)));
+          }
+        }
+        for (; j < je; j += 4) {  // remainder / exception path, constant register indices
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (j + u < je) {
+              double cc = c;
+              for (int e = 0; e < nexc; ++e)
+                if (S.exc_pos[e] == lo + j + u) cc = S.cen[S.exc_q[e]];
+              lb[u] = __dadd_rn(lb[u], __dmul_rn((double)R.wv[sw_idx(lane, j + u)],
+                                                 dcost((double)R.xs[sw_idx(lane, j + u)], cc)));
+            }
+          }
+        }
+        p = pend;
+      }
+      const double local = __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
+      loss_m = w_sum(local);
+    }
+    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[7], (unsigned long long)(tt - tph)); tph = tt; }
+    // ---- changed: new E-step labels vs the previous iteration's repaired
+    // assignment (lane 0; O(k^2))
+    int stop = 0;
+    if (lane == 0) {
+      changed = empties != 0;  // repairs count as changes
+      if (iter > 0 && !changed) {
+        // previous exceptions: the new label must equal the repair cluster
+        for (int e = 0; e < S.pnexc && !changed; ++e) {
+          const int p = S.pexc_pos[e];
+          if (w_label_seg(S.seg, S.so, k, p) != S.pexc_q[e]) changed = 1;
+        }
+        // segment labels elsewhere
+        int ro = 0, rn = 0, pos = 0;
+        while (pos < n && !changed) {
+          while (ro < k - 1 && S.pseg[ro + 1] <= pos) ++ro;
+          while (rn < k - 1 && S.seg[rn + 1] <= pos) ++rn;
+          const int end = min(S.pseg[ro + 1], S.seg[rn + 1]);
+          if (S.pso[ro] != S.so[rn]) {
+            if (end - pos > S.pnexc) {
+              changed = 1;
+            } else {
+              for (int p = pos; p < end && !changed; ++p) {
+                bool isexc = false;
+                for (int e = 0; e < S.pnexc; ++e) isexc |= S.pexc_pos[e] == p;
+                if (!isexc) changed = 1;
+              }
+            }
+          }
+          pos = end;
+        }
+      }
+      const bool stable = !changed && iter > 0;
+      const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
+      stop = stable || tol || loss_m == 0.0;
+      // this iteration's assignment becomes the previous one
+      for (int t = 0; t <= k; ++t) S.pseg[t] = S.seg[t];
+      for (int t = 0; t < k; ++t) S.pso[t] = S.so[t];
+      S.pnexc = S.nexc;
+      for (int e = 0; e < S.nexc; ++e) {
+        S.pexc_pos[e] = S.exc_pos[e];
+        S.pexc_q[e] = S.exc_q[e];
+      }
+    }
+    prev = loss_m;
+    if (P.dbg && lane == 0) {
+      atomicAdd((unsigned long long*)&P.dbg[2], 1ull);
+      if (empties) atomicAdd((unsigned long long*)&P.dbg[3], (unsigned long long)__popc(empties));
+    }
+    stop = __shfl_sync(kFull, stop, 0);
+    __syncwarp();
+    if (stop) break;
+  }
+  if (!need_loss) return 0.0;
+  // final reassignment and loss (learner.cpp:305-311)
+  w_sort(S, k, lane);
+  double local = 0.0;
+  for (int p = lo, j = 0; p < hi; ++p, ++j) {
+    const double x = (double)R.xs[sw_idx(lane, j)];
+    const int q = w_nearest(x, S, k);
+    local = __dadd_rn(local, __dmul_rn((double)R.wv[sw_idx(lane, j)], dcost(x, S.cen[q])));
+  }
+  return w_sum(local);
+}
+
+__global__ void __launch_bounds__(256) k_kmeans_warp(WkParams P) {
+  extern __shared__ __align__(16) uint8_t dsmem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* mine = dsmem + (size_t)warp * P.warp_bytes;
+  WarpKm& S = *reinterpret_cast<WarpKm*>(mine);
+  float* xs = reinterpret_cast<float*>(mine + ((sizeof(WarpKm) + 15) & ~size_t(15)));
+  float* wv = xs + (size_t)P.C * 33;
+  const int n = P.n, C = P.C, k = P.k;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+  double* d2 = P.d2scr + (size_t)gw * C * 32;
+  const WRow R{xs, wv, n, C, lane * C, min(n, lane * C + C)};
+  while (true) {
+    int row = 0;
+    if (lane == 0) row = atomicAdd(P.row_counter, 1);
+    row = __shfl_sync(kFull, row, 0);
+    if (row >= P.rows) break;
+    const int* sv_row = P.svals + (size_t)row * n;
+    const float* sk_row = P.skeys + (size_t)row * n;
+    const float* xo = P.ws + (size_t)row * n;
+    const float* wo = P.sw + (size_t)row * n;
+    int bad = 0;
+    for (int p = lane; p < n; p += 32) {
+      const float w = wo[p];
+      bad |= !(w >= 0.0f) || !isfinite(w);
+    }
+    if (__any_sync(kFull, bad)) {  // KmProblem::validate (learner.cpp:10-23)
+      if (lane == 0) dev_fail(P.err, ANYQ_ERR_STATS);
+      continue;
+    }
+    if (lane == 0) {
+      S.rng = Rng::for_row(P.seed, P.row_offset + row);
+      S.pnexc = 0;
+      S.nexc = 0;
+    }
+    __syncwarp();
+    double best = INFINITY;
+    int bail = 0;
+    for (int r = 0; r < P.restarts && !bail; ++r) {
+      const long long t0 = clock64();
+      if (P.init == ANYQ_INIT_KMPP || P.init == ANYQ_INIT_RANDOM) {
+        // seeding works on the row in ORIGINAL order
+        w_load_row(n, C, lane, [&](int p, int si) {
+          xs[si] = xo[p];
+          wv[si] = wo[p];
+        });
+        __syncwarp();
+        if (P.init == ANYQ_INIT_KMPP) w_init_kmpp(R, sk_row, d2, S, k, lane);
+        else w_init_random(R, sk_row, S, k, lane);
+        __syncwarp();
+      } else if (P.init == ANYQ_INIT_GRID) {
+        if (lane < k) S.cen[lane] = (double)(-(k / 2) + lane);
+      } else {
+        const float nf4[16] = {-1.0f, -0.6961928009986877f, -0.5250730514526367f,
+                               -0.39491748809814453f, -0.28444138169288635f,
+                               -0.18477343022823334f, -0.09105003625154495f, 0.0f,
+                               0.07958029955625534f, 0.16093020141124725f, 0.24611230194568634f,
+                               0.33791524171829224f, 0.44070982933044434f, 0.5626170039176941f,
+                               0.7229568362236023f, 1.0f};
+        if (lane < k) S.cen[lane] = (double)nf4[lane & 15];
+      }
+      // Lloyd works on the sorted row
+      w_load_row(n, C, lane, [&](int p, int si) {
+        xs[si] = sk_row[p];
+        wv[si] = wo[sv_row[p]];
+      });
+      __syncwarp();
+      const long long t1 = clock64();
+      const double loss = w_lloyd(P, R, S, sv_row, lane, P.restarts > 1, &bail);
+      if (P.dbg && lane == 0) {
+        atomicAdd((unsigned long long*)&P.dbg[0], (unsigned long long)(t1 - t0));
+        atomicAdd((unsigned long long*)&P.dbg[1], (unsigned long long)(clock64() - t1));
+      }
+      if (!bail && (P.restarts == 1 || loss < best)) {
+        best = loss;
+        if (lane < k) S.best_cen[lane] = S.cen[lane];
+      }
+      __syncwarp();
+    }
+    if (bail) {
+      if (lane == 0) P.bail_rows[atomicAdd(P.bail_n, 1)] = row;
+      continue;
+    }
+    // best centroids -> sorted LUT + rank-remapped codes (learner.cpp:343-369)
+    if (lane < k) S.cen[lane] = S.best_cen[lane];
+    w_sort(S, k, lane);
+    if (lane < k) P.luts[(size_t)row * k + lane] = (float)S.sv[lane];
+    for (int p = R.lo, j = 0; p < R.hi; ++p, ++j) {
+      const int q = w_nearest((double)xs[sw_idx(lane, j)], S, k);
+      P.codes[(size_t)row * n + sv_row[p]] = (uint8_t)S.rank_of[q];
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_fill_offsets(int* off, int64_t rows, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i <= rows) off[i] = (int)(i * n);
@@ -636,8 +1397,8 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
                    int* err, cudaStream_t s) {
   if (rows * cols >= (int64_t(1) << 31)) fail(ANYQ_ERR_SHAPE, "quantize batch too large; split rows");
   const int64_t total = rows * cols;
-  DevBuf<float> skeys(total);
-  DevBuf<int> idx(total), svals(total), offs(rows + 1), counter(1);
+  DevBuf<float> skeys(total, s);
+  DevBuf<int> idx(total, s), svals(total, s), offs(rows + 1, s), counter(1, s);
   k_fill_offsets<<<(unsigned)((rows + 256) / 256), 256, 0, s>>>(offs.p, rows, cols);
   ANYQ_LAUNCHED();
   k_iota_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(idx.p, rows, cols);
@@ -646,7 +1407,7 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
   ANYQ_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, temp_bytes, ws, skeys.p, idx.p,
                                                       svals.p, (int)total, (int)rows, offs.p,
                                                       offs.p + 1, s));
-  DevBuf<uint8_t> temp(temp_bytes);
+  DevBuf<uint8_t> temp(temp_bytes, s);
   ANYQ_CUDA(cub::DeviceSegmentedSort::StableSortPairs(temp.p, temp_bytes, ws, skeys.p, idx.p,
                                                       svals.p, (int)total, (int)rows, offs.p,
                                                       offs.p + 1, s));
@@ -673,16 +1434,91 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
   P.err = err;
   P.row_counter = counter.p;
 
-  // per-row scratch: xs, wv (fp32) + 2n doubles (d2/mass during init, asg after)
-  size_t need = (((sizeof(float) * 2 * cols) + 15) & ~size_t(15)) + sizeof(double) * 2 * cols;
   int dev = 0;
   ANYQ_CUDA(cudaGetDevice(&dev));
   int sms = 148, max_optin = 0;
   ANYQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   ANYQ_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  P.row_list = nullptr;
+  P.row_list_n = nullptr;
+
+  // Warp-per-row kernel for k <= 16 when a warp's row fits in shared memory;
+  // rows it cannot take (near-duplicate centroids) are finished by the CTA
+  // kernel below from the bail list.
+  DevBuf<double> d2scr;
+  DevBuf<int> bail(rows, s), bail_n(1, s), counter2(1, s);
+  const int64_t Cw = (cols + 31) / 32;
+  const uint32_t warp_bytes =
+      (uint32_t)(((sizeof(WarpKm) + 15) & ~size_t(15)) + ((2 * sizeof(float) * Cw * 33 + 15) & ~size_t(15)));
+  const int wpc = (int)std::min<int64_t>(8, (int64_t)max_optin / warp_bytes);
+  const bool use_warp = P.k <= kWK && !P.check_inv && wpc >= 1 && cols < (int64_t(1) << 30);
+  if (use_warp) {
+    WkParams W;
+    W.ws = ws;
+    W.sw = sw;
+    W.skeys = skeys.p;
+    W.svals = svals.p;
+    W.rows = rows;
+    W.n = (int)cols;
+    W.C = (int)Cw;
+    W.k = P.k;
+    W.init = P.init;
+    W.max_iters = P.max_iters;
+    W.restarts = P.restarts;
+    W.rel_tol = P.rel_tol;
+    W.seed = P.seed;
+    W.row_offset = row_offset;
+    W.luts = luts;
+    W.codes = codes;
+    W.err = err;
+    W.row_counter = counter.p;
+    W.warp_bytes = warp_bytes;
+    static const bool km_debug = std::getenv("ANYQ_KM_DEBUG") != nullptr;
+    DevBuf<long long> dbg;
+    W.dbg = nullptr;
+    if (km_debug) {
+      dbg.alloc(8, s);
+      ANYQ_CUDA(cudaMemsetAsync(dbg.p, 0, 8 * sizeof(long long), s));
+      W.dbg = dbg.p;
+    }
+    const int smem = (int)(wpc * warp_bytes);
+    ANYQ_CUDA(cudaFuncSetAttribute(k_kmeans_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per_sm = 0;
+    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_warp, wpc * 32, smem));
+    const int blocks = (int)std::min<int64_t>((rows + wpc - 1) / wpc, (int64_t)sms * std::max(1, per_sm));
+    d2scr.alloc((size_t)blocks * wpc * Cw * 32, s);
+    W.d2scr = d2scr.p;
+    W.bail_rows = bail.p;
+    W.bail_n = bail_n.p;
+    ANYQ_CUDA(cudaMemsetAsync(bail_n.p, 0, sizeof(int), s));
+    k_kmeans_warp<<<blocks, wpc * 32, smem, s>>>(W);
+    ANYQ_LAUNCHED();
+    if (km_debug) {
+      long long h[8];
+      ANYQ_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof h, cudaMemcpyDeviceToHost, s));
+      int nb = 0;
+      ANYQ_CUDA(cudaMemcpyAsync(&nb, bail_n.p, sizeof nb, cudaMemcpyDeviceToHost, s));
+      ANYQ_CUDA(cudaStreamSynchronize(s));
+      std::fprintf(stderr,
+                   "[kmeans warp] rows %lld n %lld warps/cta %d blocks %d: init %.0f cyc/row, lloyd %.0f "
+                   "cyc/row, iters/row %.2f, repairs %lld, bailed %d; per iter: E %.0f M %.0f rep %.0f loss %.0f\n",
+                   (long long)rows, (long long)cols, wpc, blocks, (double)h[0] / rows,
+                   (double)h[1] / rows, (double)h[2] / rows, h[3], nb, (double)h[4] / h[2], (double)h[5] / h[2],
+                   (double)h[6] / h[2], (double)h[7] / h[2]);
+    }
+    // the CTA kernel takes the bailed rows (exits at once when there are none)
+    ANYQ_CUDA(cudaMemsetAsync(counter2.p, 0, sizeof(int), s));
+    P.row_counter = counter2.p;
+    P.row_list = bail.p;
+    P.row_list_n = bail_n.p;
+  }
+
+  // per-row scratch: xs, wv (fp32) + 2n doubles (d2/mass during init, asg after)
+  size_t need = (((sizeof(float) * 2 * cols) + 15) & ~size_t(15)) + sizeof(double) * 2 * cols;
   size_t static_smem = sizeof(Shared) + 2 * 2 * kMaxK * sizeof(int64_t);
   DevBuf<uint8_t> gscratch;
   int blocks;
+  const int64_t cta_rows = use_warp ? std::min<int64_t>(rows, (int64_t)sms) : rows;
   if (need + static_smem <= (size_t)max_optin) {
     P.use_smem = 1;
     P.gscratch = nullptr;
@@ -691,20 +1527,20 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
                                    (int)need));
     int per_sm = 0;
     ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, kThreads, need));
-    blocks = (int)std::min<int64_t>(rows, (int64_t)sms * std::max(1, per_sm));
+    blocks = (int)std::min<int64_t>(cta_rows, (int64_t)sms * std::max(1, per_sm));
     k_kmeans_rows<<<blocks, kThreads, need, s>>>(P);
   } else {
     int per_sm = 0;
     ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, kThreads, 0));
-    blocks = (int)std::min<int64_t>(rows, (int64_t)sms * std::max(1, per_sm));
+    blocks = (int)std::min<int64_t>(cta_rows, (int64_t)sms * std::max(1, per_sm));
     P.use_smem = 0;
     P.scratch_stride = (need + 255) & ~size_t(255);
-    gscratch.alloc(P.scratch_stride * blocks);
+    gscratch.alloc(P.scratch_stride * blocks, s);
     P.gscratch = gscratch.p;
     k_kmeans_rows<<<blocks, kThreads, 0, s>>>(P);
   }
   ANYQ_LAUNCHED();
-  ANYQ_CUDA(cudaStreamSynchronize(s));  // scratch buffers are freed on return
+  // scratch buffers are released stream-ordered on return
 }
 
 }  // namespace anyq_b200
