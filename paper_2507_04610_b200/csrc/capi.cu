@@ -502,7 +502,7 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
   return guard([&] {
     const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
     if (path == ANYQ_PATH_AUTO)
-      path = (m <= 1 && lt && lt->gv_gshift >= 0) ? ANYQ_PATH_GEMV
+      path = lutgemv_fits(lt, m) ? ANYQ_PATH_GEMV
              : m <= 16                              ? ANYQ_PATH_TC
                                                     : ANYQ_PATH_DEQUANT;
     if (path == ANYQ_PATH_GEMV)

@@ -836,6 +836,21 @@ void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs,
   else launch_gv<2>(n, ts, xs, ys, y32s, waits, m, s);
 }
 
+bool lutgemv_fits(const LutTensor* t, int64_t m) {
+  if (!t || m < 1 || m > kMaxMP || t->gv_gshift < 0) return false;
+  const LutTensor* ts[1] = {t};
+  const void* xs[1] = {nullptr};
+  void* ys[1] = {nullptr};
+  GvParams P;
+  try {
+    if (m == 1) plan_chain<1>(1, ts, xs, ys, nullptr, nullptr, m, P);
+    else plan_chain<2>(1, ts, xs, ys, nullptr, nullptr, m, P);
+  } catch (const Failure&) {
+    return false;
+  }
+  return true;
+}
+
 void lutgemv_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y32,
                  cudaStream_t s) {
   if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");

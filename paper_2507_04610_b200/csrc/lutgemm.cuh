@@ -46,6 +46,7 @@ void lutgemv_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), o
 // waits[i] != 0 reads x_i only after all earlier problems completed.
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                        float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s);
+bool lutgemv_fits(const LutTensor* t, int64_t m);  // GEMV applies (m <= 2, shared memory)
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
 // M > 16: bf16 dequantization in row slices + cuBLAS GEMM (dequant_gemm.cu).

@@ -7,6 +7,6 @@ SMI=$!
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
 kill $SMI
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref exit $?" >> gpurun_out/bench_ref.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 40 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 8 --warmup 3 --quick --no-cpu > gpurun_out/bench_ncu.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_lutgemv -c 20 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 8 --warmup 3 --quick --no-cpu > gpurun_out/bench_ncu.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_lutgemv -s 2 -c 1 -o gpurun_out/chain_full python scripts/prof_chain.py > gpurun_out/ncu_chain.log 2>&1
 echo done

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-ANYQ_KM_DEBUG=1 timeout 300 python scripts/prof_kmeans.py 148 4096 > gpurun_out/prof_kmeans_dbg.txt 2>&1
+ANYQ_KM_DEBUG=1 timeout 300 python scripts/prof_kmeans.py 4096 4096x14336 14336x4096 > gpurun_out/prof_kmeans_dbg.txt 2>&1
 echo done

@@ -13,16 +13,16 @@ from paper_2507_04610_b200 import _abi, anyq  # noqa: E402
 
 
 def main():
-    rows_list = [int(a) for a in sys.argv[1:]] or [148, 296, 1024, 4096, 8192]
+    specs = sys.argv[1:] or ["148", "296", "1024", "4096", "8192"]
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev)
     g.manual_seed(1)
     cfg = _abi.default_config(codebook=_abi.CB_ANY)
-    w = torch.randn(max(rows_list), 4096, device=dev, generator=g)
-    anyq.dev_quantize_any(w[:256].contiguous(), cfg)
-    torch.cuda.synchronize()
-    for r in rows_list:
-        x = w[:r].contiguous()
+    for spec in specs:  # "ROWS" or "ROWSxCOLS"
+        r, c = (int(v) for v in spec.split("x")) if "x" in spec else (int(spec), 4096)
+        x = torch.randn(r, c, device=dev, generator=g)
+        anyq.dev_quantize_any(x, cfg)  # warm (scratch pool)
+        torch.cuda.synchronize()
         ts = []
         for _ in range(3):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -34,7 +34,7 @@ def main():
             ts.append((e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
         ev = min(t[0] for t in ts)
         wall = min(t[1] for t in ts)
-        print(f"rows {r:6d}: event {ev:8.2f} ms  wall {wall:8.2f} ms  -> {r / ev * 1e3:10.0f} rows/s")
+        print(f"rows {r:6d} x {c:5d}: event {ev:8.2f} ms  wall {wall:8.2f} ms  -> {r / ev * 1e3:10.0f} rows/s")
 
 
 if __name__ == "__main__":
