@@ -646,19 +646,24 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
 // ===========================================================================
 constexpr int kWK = 16;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxG = 8;
 
+// Per-row state of one row group (one CTA of G warps works one row at a time).
 struct WarpKm {
   double cen[kWK], best_cen[kWK], sv[kWK];
   double swx[kWK], sw[kWK], sx[kWK];
-  double fpart[32][3], lpart[32][3];
   int so[kWK], rank_of[kWK], cnt[kWK];
   int seg[kWK + 1], pseg[kWK + 1], pso[kWK];
   int exc_pos[kWK], exc_q[kWK], pexc_pos[kWK], pexc_q[kWK];
   int nexc, pnexc;
-  int fc[32], lc[32];
   long long vkeys[2 * kWK], vvals[2 * kWK];
   Rng rng;
   int ncen;
+  double redd[kMaxG];  // cross-warp reduction slots
+  long long redl[kMaxG];
+  int redi[kMaxG];
+  double bcd;  // broadcasts from thread 0
+  int bci;
 };
 
 struct WkParams {
@@ -675,55 +680,102 @@ struct WkParams {
   uint8_t* codes;
   int* err;
   int* row_counter;
-  double* d2scr;       // [total warps][C * 32] k-means++ D^2, lane-interleaved
-  int* bail_rows;      // rows handed to k_kmeans_rows
+  double* d2scr;        // [CTAs][C * T] k-means++ D^2, thread-interleaved
+  int* bail_rows;       // rows handed to k_kmeans_rows
   int* bail_n;
-  uint32_t warp_bytes;  // dynamic smem per warp
-  long long* dbg;       // debug counters [8] (ANYQ_KM_DEBUG), or null
+  uint32_t state_bytes;  // dynamic smem: WarpKm + fpart/lpart
+  long long* dbg;        // debug counters [8] (ANYQ_KM_DEBUG), or null
 };
 
-__device__ __forceinline__ double w_sum(double v) {  // fixed tree to lane 0, broadcast
+// The row group: thread t of T = 32*G owns the contiguous chunk [t*C, t*C + C)
+// of the row; element j of chunk t lives at j*(T+1) + t in shared memory (bank
+// (j + t) % 32: conflict free for a warp walking its chunks in step and for
+// coalesced whole-row loads; linear in j).
+struct Grp {
+  int t, lane, warp, G, T;
+};
+
+struct WRow {
+  const float* xs;  // sorted samples (Lloyd) / original order (k-means++)
+  const float* wv;  // their weights
+  int n, C, T, lo, hi, nch;
+  __device__ __forceinline__ int idx(int t, int j) const { return j * (T + 1) + t; }
+  __device__ __forceinline__ float x_at(int p) const {
+    const int t = p / C;
+    return xs[idx(t, p - t * C)];
+  }
+};
+
+// Deterministic group reductions (fixed shuffle tree, then warp order).
+__device__ __forceinline__ double g_sum(double v, WarpKm& S, const Grp& g) {
   for (int off = 16; off; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(kFull, v, off));
-  return __shfl_sync(kFull, v, 0);
+  if (g.G == 1) return __shfl_sync(kFull, v, 0);
+  if (g.lane == 0) S.redd[g.warp] = v;
+  __syncthreads();
+  double s = S.redd[0];
+  for (int w = 1; w < g.G; ++w) s = __dadd_rn(s, S.redd[w]);
+  __syncthreads();
+  return s;
 }
-__device__ __forceinline__ double w_scan_excl(double v, int lane, double* total) {
+__device__ __forceinline__ double g_scan_excl(double v, WarpKm& S, const Grp& g, double* total) {
   double incl = v;
   for (int off = 1; off < 32; off <<= 1) {
     const double o = __shfl_up_sync(kFull, incl, off);
-    if (lane >= off) incl = __dadd_rn(o, incl);
+    if (g.lane >= off) incl = __dadd_rn(o, incl);
   }
-  *total = __shfl_sync(kFull, incl, 31);
-  const double ex = __shfl_up_sync(kFull, incl, 1);
-  return lane == 0 ? 0.0 : ex;
+  const double wtot = __shfl_sync(kFull, incl, 31);
+  double ex = __shfl_up_sync(kFull, incl, 1);
+  if (g.lane == 0) ex = 0.0;
+  if (g.G == 1) {
+    *total = wtot;
+    return ex;
+  }
+  if (g.lane == 0) S.redd[g.warp] = wtot;
+  __syncthreads();
+  double base = 0.0, tot = S.redd[0];
+  for (int w = 1; w < g.G; ++w) tot = __dadd_rn(tot, S.redd[w]);
+  if (g.warp > 0) {
+    base = S.redd[0];
+    for (int w = 1; w < g.warp; ++w) base = __dadd_rn(base, S.redd[w]);
+  }
+  __syncthreads();
+  *total = tot;
+  return g.warp > 0 ? __dadd_rn(base, ex) : ex;
 }
-__device__ __forceinline__ long long w_min_ll(long long v) {
+__device__ __forceinline__ long long g_min_ll(long long v, WarpKm& S, const Grp& g) {
   for (int off = 16; off; off >>= 1) v = min(v, __shfl_xor_sync(kFull, v, off));
-  return v;
+  if (g.G == 1) return v;
+  if (g.lane == 0) S.redl[g.warp] = v;
+  __syncthreads();
+  long long m = S.redl[0];
+  for (int w = 1; w < g.G; ++w) m = min(m, S.redl[w]);
+  __syncthreads();
+  return m;
 }
-__device__ __forceinline__ long long w_max_ll(long long v) {
-  for (int off = 16; off; off >>= 1) v = max(v, __shfl_xor_sync(kFull, v, off));
-  return v;
+__device__ __forceinline__ long long g_max_ll(long long v, WarpKm& S, const Grp& g) {
+  return -g_min_ll(-v, S, g);
 }
-__device__ __forceinline__ double w_bcast_rng(WarpKm& S, int lane) {
-  double u = 0.0;
-  if (lane == 0) u = S.rng.next_double();
-  return __shfl_sync(kFull, u, 0);
+__device__ __forceinline__ double g_rng(WarpKm& S, const Grp& g) {
+  __syncthreads();
+  if (g.t == 0) S.bcd = S.rng.next_double();
+  __syncthreads();
+  return S.bcd;
 }
 
-__device__ __forceinline__ void w_sort(WarpKm& S, int k, int lane) {
-  __syncwarp();
-  if (lane < k) {
-    const double v = S.cen[lane];
+__device__ __forceinline__ void w_sort(WarpKm& S, int k, const Grp& g) {
+  __syncthreads();
+  if (g.t < k) {
+    const double v = S.cen[g.t];
     int r = 0;
     for (int p = 0; p < k; ++p) {
       const double u = S.cen[p];
-      r += (u < v) || (u == v && p < lane);
+      r += (u < v) || (u == v && p < g.t);
     }
-    S.rank_of[lane] = r;
+    S.rank_of[g.t] = r;
     S.sv[r] = v;
-    S.so[r] = lane;
+    S.so[r] = g.t;
   }
-  __syncwarp();
+  __syncthreads();
 }
 
 // Exact reference nearest centroid (ties to the smallest original index).
@@ -752,36 +804,16 @@ __device__ __forceinline__ int w_nearest(double x, const WarpKm& S, int k) {
   return best;
 }
 
-// Row buffers of one warp: element j of lane l's contiguous chunk
-// [l*C, l*C + C) lives at j*33 + l (padded rows: bank (j + l) % 32) — conflict
-// free both for lanes walking their chunks in step and for coalesced whole-row
-// loads, and linear in j (immediate offsets in the unrolled loops).
-__device__ __forceinline__ int sw_idx(int l, int j) { return j * 33 + l; }
-
-struct WRow {
-  const float* xs;  // sorted samples (Lloyd) / original order (k-means++)
-  const float* wv;  // their weights
-  int n, C, lo, hi;
-  __device__ __forceinline__ float x_at(int p) const {
-    const int l = p / C;
-    return xs[sw_idx(l, p - l * C)];
-  }
-};
-
-// Whole-row load into the swizzled layout (coalesced global reads).
+// Whole-row load into the chunked layout (coalesced global reads).
 template <typename F>
-__device__ __forceinline__ void w_load_row(int n, int C, int lane, F&& put) {
-  int l = 0, j = lane;
-  while (j >= C) {
-    j -= C;
-    ++l;
-  }
-  for (int p = lane; p < n; p += 32) {
-    put(p, sw_idx(l, j));
-    j += 32;
-    while (j >= C) {
-      j -= C;
-      ++l;
+__device__ __forceinline__ void w_load_row(const WRow& R, const Grp& g, F&& put) {
+  int t = g.t / R.C, j = g.t - (g.t / R.C) * R.C;
+  for (int p = g.t; p < R.n; p += R.T) {
+    put(p, R.idx(t, j));
+    j += R.T;
+    while (j >= R.C) {
+      j -= R.C;
+      ++t;
     }
   }
 }
@@ -805,18 +837,18 @@ __device__ double w_distinct_value(const float* sk, int n, int64_t m) {
   return (double)sk[0];
 }
 
-// Cumulative-mass sampling (learner.cpp:64-75) over this lane's chunk of
-// ORIGINAL indices: first hit over lanes, else the last positive index.
+// Cumulative-mass sampling (learner.cpp:64-75) over this thread's chunk of
+// ORIGINAL indices: first hit over the group, else the last positive index.
 template <int kMode>  // 0: mass = w, 1: mass = w * d2, 2: mass = d2
-__device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, int lane, double excl,
-                                              double r) {
+__device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, WarpKm& S,
+                                              const Grp& g, double excl, double r) {
   long long cand = LLONG_MAX, lastpos = -1;
   double acc = excl;
   const int cnt = R.hi - R.lo;
   auto mass = [&](int j) {
-    if (kMode == 0) return (double)R.wv[sw_idx(lane, j)];
-    if (kMode == 1) return __dmul_rn((double)R.wv[sw_idx(lane, j)], d2[j * 32 + lane]);
-    return d2[j * 32 + lane];
+    if (kMode == 0) return (double)R.wv[R.idx(g.t, j)];
+    if (kMode == 1) return __dmul_rn((double)R.wv[R.idx(g.t, j)], d2[j * R.T + g.t]);
+    return d2[j * R.T + g.t];
   };
   for (int j0 = 0; j0 < cnt && cand == LLONG_MAX; j0 += 16) {
     double mv[16];
@@ -837,79 +869,80 @@ __device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, i
         break;
       }
   }
-  const long long c = w_min_ll(cand);
-  const long long lp = w_max_ll(lastpos);
+  const long long c = g_min_ll(cand, S, g);
+  const long long lp = g_max_ll(lastpos, S, g);
   return c != LLONG_MAX ? c : (lp >= 0 ? lp : 0);
 }
 
 // k-means++ (learner.cpp:132-174): R holds the row in ORIGINAL order; D^2 in
-// global scratch (lane-interleaved, coalesced).
-__device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& S, int k, int lane) {
+// global scratch (thread-interleaved, coalesced).
+__device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& S, int k,
+                            const Grp& g) {
   const int cnt = R.hi - R.lo;
   double part = 0.0, total;
   for (int j = 0; j < cnt; ++j) {
-    const double m = (double)R.wv[sw_idx(lane, j)];
+    const double m = (double)R.wv[R.idx(g.t, j)];
     if (m > 0.0) part = __dadd_rn(part, m);
   }
-  double excl = w_scan_excl(part, lane, &total);
-  double u = w_bcast_rng(S, lane);
-  long long pick = w_sample<0>(R, d2, lane, excl, __dmul_rn(u, total));
-  if (lane == 0) {
+  double excl = g_scan_excl(part, S, g, &total);
+  double u = g_rng(S, g);
+  long long pick = w_sample<0>(R, d2, S, g, excl, __dmul_rn(u, total));
+  for (int j = 0; j < cnt; ++j) d2[j * R.T + g.t] = INFINITY;
+  if (g.t == 0) {
     S.cen[0] = (double)R.x_at((int)pick);
     S.ncen = 1;
   }
-  for (int j = 0; j < cnt; ++j) d2[j * 32 + lane] = INFINITY;
-  __syncwarp();
+  __syncthreads();
   while (S.ncen < k) {
     const double c = S.cen[S.ncen - 1];
     part = 0.0;
     for (int j0 = 0; j0 < cnt; j0 += 16) {
       double dv[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) dv[u] = d2[min(j0 + u, cnt - 1) * 32 + lane];  // loads first
+      for (int uu = 0; uu < 16; ++uu) dv[uu] = d2[min(j0 + uu, cnt - 1) * R.T + g.t];  // loads first
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        if (j0 + u >= cnt) break;
-        const int si = sw_idx(lane, j0 + u);
+      for (int uu = 0; uu < 16; ++uu) {
+        if (j0 + uu >= cnt) break;
+        const int si = R.idx(g.t, j0 + uu);
         const double pc = dcost((double)R.xs[si], c);
-        const double d = (pc < dv[u]) ? pc : dv[u];
-        d2[(j0 + u) * 32 + lane] = d;
+        const double d = (pc < dv[uu]) ? pc : dv[uu];
+        d2[(j0 + uu) * R.T + g.t] = d;
         const double m = __dmul_rn((double)R.wv[si], d);
         if (m > 0.0) part = __dadd_rn(part, m);
       }
     }
-    excl = w_scan_excl(part, lane, &total);
+    excl = g_scan_excl(part, S, g, &total);
     if (total > 0.0) {
-      u = w_bcast_rng(S, lane);
-      pick = w_sample<1>(R, d2, lane, excl, __dmul_rn(u, total));
-      if (lane == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
-      __syncwarp();
+      u = g_rng(S, g);
+      pick = w_sample<1>(R, d2, S, g, excl, __dmul_rn(u, total));
+      if (g.t == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
+      __syncthreads();
       continue;
     }
     part = 0.0;
     for (int j = 0; j < cnt; ++j) {
-      const double m = d2[j * 32 + lane];
+      const double m = d2[j * R.T + g.t];
       if (m > 0.0) part = __dadd_rn(part, m);
     }
-    excl = w_scan_excl(part, lane, &total);
+    excl = g_scan_excl(part, S, g, &total);
     if (total > 0.0) {
-      u = w_bcast_rng(S, lane);
-      pick = w_sample<2>(R, d2, lane, excl, __dmul_rn(u, total));
-      if (lane == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
-      __syncwarp();
+      u = g_rng(S, g);
+      pick = w_sample<2>(R, d2, S, g, excl, __dmul_rn(u, total));
+      if (g.t == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
+      __syncthreads();
       continue;
     }
-    if (lane == 0) {
+    if (g.t == 0) {
       int64_t cursor = 0;
       while (S.ncen < k) S.cen[S.ncen++] = w_distinct_value(sk, R.n, cursor++);
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
 // random_init (learner.cpp:86-103); R holds the row in ORIGINAL order.
-__device__ void w_init_random(const WRow& R, const float* sk, WarpKm& S, int k, int lane) {
-  if (lane == 0) {
+__device__ void w_init_random(const WRow& R, const float* sk, WarpKm& S, int k, const Grp& g) {
+  if (g.t == 0) {
     const int64_t n = R.n;
     if ((int64_t)k >= n) {
       int c = 0;
@@ -942,66 +975,74 @@ __device__ void w_init_random(const WRow& R, const float* sk, WarpKm& S, int k, 
       }
     }
   }
-  __syncwarp();
+  __syncthreads();
 }
+
+#define KM_PHASE(slot)                                                                  \
+  do {                                                                                  \
+    if (P.dbg && g.t == 0) {                                                            \
+      const long long tt = clock64();                                                   \
+      atomicAdd((unsigned long long*)&P.dbg[slot], (unsigned long long)(tt - tph));     \
+      tph = tt;                                                                         \
+    }                                                                                   \
+  } while (0)
 
 // One Lloyd run (learner.cpp:207-312). Returns the final loss (or 0 when
 // not needed); *bail = 1 when the row must go to the CTA kernel.
-__device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int* svals_row,
-                          int lane, bool need_loss, int* bail) {
+__device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* FP, double* LP,
+                          const int* svals_row, const Grp& g, bool need_loss, int* bail) {
   const int n = R.n, C = R.C, k = P.k, lo = R.lo, hi = R.hi;
-  // data range for the monotonicity guard
   const double xmax = fmax(fabs((double)R.x_at(0)), fabs((double)R.x_at(n - 1)));
   double prev = INFINITY;
   for (int iter = 0; iter < P.max_iters; ++iter) {
     long long tph = clock64();
-    // ---- E-step: segment boundaries by binary search on the nearest rank
-    w_sort(S, k, lane);
+    // ---- E-step: segment boundaries of the sorted row by the exact predicate
+    w_sort(S, k, g);
     {
       double cmax = 0.0;
       bool near_dup = false;
       for (int r = 0; r < k; ++r) cmax = fmax(cmax, fabs(S.sv[r]));
       const double thresh = ldexp(xmax + cmax, -40);
       for (int r = 0; r + 1 < k; ++r) {
-        const double g = __dsub_rn(S.sv[r + 1], S.sv[r]);
-        near_dup |= (g > 0.0 && g < thresh) || !(g >= 0.0);
+        const double gap = __dsub_rn(S.sv[r + 1], S.sv[r]);
+        near_dup |= (gap > 0.0 && gap < thresh) || !(gap >= 0.0);
       }
-      if (near_dup) {
+      if (near_dup) {  // uniform: every thread sees the same centroids
         *bail = 1;
         return 0.0;
       }
     }
-    if (lane >= 1 && lane < k) {
-      // seg[lane] = first sorted position whose nearest rank is >= lane
+    if (g.t >= 1 && g.t < k) {
+      // seg[t] = first sorted position whose nearest rank is >= t
+      const int t = g.t;
       auto rank_at = [&](int p) { return S.rank_of[w_nearest((double)R.x_at(p), S, k)]; };
       int a = 0, b = n;
       bool done = false;
-      if (S.sv[lane - 1] < S.sv[lane]) {
+      if (S.sv[t - 1] < S.sv[t]) {
         // distinct neighbours: the switch sits at the midpoint up to rounding;
-        // locate it by value, then settle it with the exact predicate
-        const double mid = 0.5 * S.sv[lane - 1] + 0.5 * S.sv[lane];
-        // first chunk whose first sample is >= mid, then inside the chunk before it
-        const int nl = (n + C - 1) / C;
-        int la = 0, lb = nl;
+        // locate it by value (chunk starts, then inside the chunk), then settle
+        // it with the exact predicate
+        const double mid = 0.5 * S.sv[t - 1] + 0.5 * S.sv[t];
+        int la = 0, lb = R.nch;
         while (la < lb) {
           const int m = (la + lb) >> 1;
-          if ((double)R.xs[sw_idx(m, 0)] < mid) la = m + 1;
+          if ((double)R.xs[R.idx(m, 0)] < mid) la = m + 1;
           else lb = m;
         }
-        int lo2 = 0;
+        int p = 0;
         if (la > 0) {
-          const int l = la - 1, cntl = min(C, n - l * C);
-          int ja = 0, jb = cntl;
+          const int c0 = la - 1, cntc = min(C, n - c0 * C);
+          int ja = 0, jb = cntc;
           while (ja < jb) {
             const int m = (ja + jb) >> 1;
-            if ((double)R.xs[sw_idx(l, m)] < mid) ja = m + 1;
+            if ((double)R.xs[R.idx(c0, m)] < mid) ja = m + 1;
             else jb = m;
           }
-          lo2 = l * C + ja;
+          p = c0 * C + ja;
         }
-        int p = lo2, steps = 0;
-        while (p > 0 && steps < 8 && rank_at(p - 1) >= lane) --p, ++steps;
-        while (p < n && steps < 8 && rank_at(p) < lane) ++p, ++steps;
+        int steps = 0;
+        while (p > 0 && steps < 8 && rank_at(p - 1) >= t) --p, ++steps;
+        while (p < n && steps < 8 && rank_at(p) < t) ++p, ++steps;
         if (steps < 8) {
           a = p;
           done = true;
@@ -1010,29 +1051,26 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
       if (!done) {
         while (a < b) {
           const int mid = (a + b) >> 1;
-          if (rank_at(mid) >= lane) b = mid;
+          if (rank_at(mid) >= t) b = mid;
           else a = mid + 1;
         }
       }
-      S.seg[lane] = a;
+      S.seg[t] = a;
     }
-    if (lane == 0) {
+    if (g.t == 0) {
       S.seg[0] = 0;
       S.seg[k] = n;
     }
-    __syncwarp();
-    int changed = 0;
-    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[4], (unsigned long long)(tt - tph)); tph = tt; }
-    // ---- M-step: per-lane runs over the lane's chunk, combined in chunk order
+    __syncthreads();
+    KM_PHASE(4);
+    // ---- M-step: per-thread runs over its chunk, combined in chunk order
     {
-      // runs of the lane's chunk: [p, pend) inside segment r (label so[r])
-      int r = 0, nr = 0, fcq = -1, lcq = -1;
+      int r = 0, nr = 0;
       for (int p = lo; p < hi;) {
         while (r < k - 1 && S.seg[r + 1] <= p) ++r;
         const int pend = min(hi, S.seg[r + 1]);
         const int q = S.so[r];
-        // four interleaved partial sums per quantity (fixed order: ILP for the
-        // 8-cycle DADD chain), folded at the end of the run
+        // four interleaved partial sums per quantity (fixed order), folded per run
         double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0}, b2[4] = {0.0, 0.0, 0.0, 0.0};
         int j = p - lo;
         const int je = pend - lo;
@@ -1040,8 +1078,8 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
           float xv[8], wq[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            xv[u] = R.xs[sw_idx(lane, j + u)];
-            wq[u] = R.wv[sw_idx(lane, j + u)];
+            xv[u] = R.xs[R.idx(g.t, j + u)];
+            wq[u] = R.wv[R.idx(g.t, j + u)];
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -1054,7 +1092,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
 #pragma unroll
         for (int u = 0; u < 8; ++u) {  // remainder (< 8), constant register indices
           if (j + u < je) {
-            const double w = (double)R.wv[sw_idx(lane, j + u)], x = (double)R.xs[sw_idx(lane, j + u)];
+            const double w = (double)R.wv[R.idx(g.t, j + u)], x = (double)R.xs[R.idx(g.t, j + u)];
             b0[u & 3] = __dadd_rn(b0[u & 3], __dmul_rn(w, x));
             b1[u & 3] = __dadd_rn(b1[u & 3], w);
             b2[u & 3] = __dadd_rn(b2[u & 3], x);
@@ -1064,28 +1102,24 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
         const double a1 = __dadd_rn(__dadd_rn(b1[0], b1[1]), __dadd_rn(b1[2], b1[3]));
         const double a2 = __dadd_rn(__dadd_rn(b2[0], b2[1]), __dadd_rn(b2[2], b2[3]));
         if (nr == 0) {
-          S.fpart[lane][0] = a0;
-          S.fpart[lane][1] = a1;
-          S.fpart[lane][2] = a2;
-          fcq = q;
+          FP[g.t * 3 + 0] = a0;
+          FP[g.t * 3 + 1] = a1;
+          FP[g.t * 3 + 2] = a2;
         } else if (pend < hi) {  // interior run: the whole cluster lies in this chunk
           S.swx[q] = a0;
           S.sw[q] = a1;
           S.sx[q] = a2;
         } else {
-          S.lpart[lane][0] = a0;
-          S.lpart[lane][1] = a1;
-          S.lpart[lane][2] = a2;
-          lcq = q;
+          LP[g.t * 3 + 0] = a0;
+          LP[g.t * 3 + 1] = a1;
+          LP[g.t * 3 + 2] = a2;
         }
         ++nr;
         p = pend;
       }
-      S.fc[lane] = fcq;
-      S.lc[lane] = lcq;
-      __syncwarp();
-      if (lane < k) {
-        const int q = lane;
+      __syncthreads();
+      if (g.t < k) {
+        const int q = g.t;
         const int rq = S.rank_of[q];
         const int a = S.seg[rq], z = S.seg[rq + 1];
         S.cnt[q] = z - a;
@@ -1095,21 +1129,21 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
           const bool ends_chunk = z == min(n, (t0 + 1) * C);
           if (t0 == t1) {
             if (starts_chunk) {
-              S.swx[q] = S.fpart[t0][0];
-              S.sw[q] = S.fpart[t0][1];
-              S.sx[q] = S.fpart[t0][2];
+              S.swx[q] = FP[t0 * 3 + 0];
+              S.sw[q] = FP[t0 * 3 + 1];
+              S.sx[q] = FP[t0 * 3 + 2];
             } else if (ends_chunk) {
-              S.swx[q] = S.lpart[t0][0];
-              S.sw[q] = S.lpart[t0][1];
-              S.sx[q] = S.lpart[t0][2];
+              S.swx[q] = LP[t0 * 3 + 0];
+              S.sw[q] = LP[t0 * 3 + 1];
+              S.sx[q] = LP[t0 * 3 + 2];
             }  // else: interior run, already complete
           } else {
-            const double* f0 = starts_chunk ? S.fpart[t0] : S.lpart[t0];
+            const double* f0 = starts_chunk ? &FP[t0 * 3] : &LP[t0 * 3];
             double s0 = f0[0], s1 = f0[1], s2 = f0[2];
             for (int t = t0 + 1; t <= t1; ++t) {
-              s0 = __dadd_rn(s0, S.fpart[t][0]);
-              s1 = __dadd_rn(s1, S.fpart[t][1]);
-              s2 = __dadd_rn(s2, S.fpart[t][2]);
+              s0 = __dadd_rn(s0, FP[t * 3 + 0]);
+              s1 = __dadd_rn(s1, FP[t * 3 + 1]);
+              s2 = __dadd_rn(s2, FP[t * 3 + 2]);
             }
             S.swx[q] = s0;
             S.sw[q] = s1;
@@ -1117,32 +1151,31 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
           }
         }
       }
-      __syncwarp();
-      if (lane < k && S.cnt[lane] > 0) {
-        const int q = lane;
+      __syncthreads();
+      if (g.t < k && S.cnt[g.t] > 0) {
+        const int q = g.t;
         if (S.sw[q] > 0.0) S.cen[q] = __ddiv_rn(S.swx[q], S.sw[q]);
         else S.cen[q] = __ddiv_rn(S.sx[q], (double)S.cnt[q]);
       }
-      __syncwarp();
+      if (g.t == 0) S.nexc = 0;
+      __syncthreads();
     }
-    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[5], (unsigned long long)(tt - tph)); tph = tt; }
+    KM_PHASE(5);
     // ---- empty-cluster repair (learner.cpp:260-274), in cluster order
-    if (lane == 0) S.nexc = 0;
-    __syncwarp();
-    const unsigned empties = __ballot_sync(kFull, lane < k && S.cnt[lane] == 0);
+    unsigned empties = 0;
+    for (int q = 0; q < k; ++q) empties |= (S.cnt[q] == 0 ? 1u : 0u) << q;
     for (unsigned em = empties; em; em &= em - 1) {
       const int q = __ffs(em) - 1;
       double worst = -1.0;
       int wp = -1;
       long long wo_i = LLONG_MAX;
       int r = 0;
-      while (r < k - 1 && S.seg[r + 1] <= lo) ++r;
       for (int p = lo, j = 0; p < hi; ++p, ++j) {
         while (r < k - 1 && S.seg[r + 1] <= p) ++r;
         int lab = S.so[r];
         for (int e = 0; e < S.nexc; ++e)
           if (S.exc_pos[e] == p) lab = S.exc_q[e];
-        const double err = __dmul_rn((double)R.wv[sw_idx(lane, j)], dcost((double)R.xs[sw_idx(lane, j)], S.cen[lab]));
+        const double err = __dmul_rn((double)R.wv[R.idx(g.t, j)], dcost((double)R.xs[R.idx(g.t, j)], S.cen[lab]));
         if (err > worst) {
           worst = err;
           wp = p;
@@ -1157,28 +1190,43 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
         }
       }
       if (wp >= 0 && wo_i == LLONG_MAX) wo_i = svals_row[wp];
-      // warp argmax (err), ties to the smallest original index
+      // argmax (err), ties to the smallest original index: warp tree, then warps in order
       for (int off = 16; off; off >>= 1) {
         const double oe = __shfl_down_sync(kFull, worst, off);
         const long long oo = __shfl_down_sync(kFull, wo_i, off);
         const int op = __shfl_down_sync(kFull, wp, off);
-        if (lane + off < 32 && (oe > worst || (oe == worst && oo < wo_i))) {
+        if (g.lane + off < 32 && (oe > worst || (oe == worst && oo < wo_i))) {
           worst = oe;
           wo_i = oo;
           wp = op;
         }
       }
-      if (lane == 0) {
-        S.cen[q] = (double)R.x_at(wp);
+      if (g.lane == 0) {
+        S.redd[g.warp] = worst;
+        S.redl[g.warp] = wo_i;
+        S.redi[g.warp] = wp;
+      }
+      __syncthreads();
+      if (g.t == 0) {
+        double be = S.redd[0];
+        long long bo = S.redl[0];
+        int bp = S.redi[0];
+        for (int w = 1; w < g.G; ++w)
+          if (S.redd[w] > be || (S.redd[w] == be && S.redl[w] < bo)) {
+            be = S.redd[w];
+            bo = S.redl[w];
+            bp = S.redi[w];
+          }
+        S.cen[q] = (double)R.x_at(bp);
         int e = 0;
-        while (e < S.nexc && S.exc_pos[e] != wp) ++e;
-        S.exc_pos[e] = wp;
+        while (e < S.nexc && S.exc_pos[e] != bp) ++e;
+        S.exc_pos[e] = bp;
         S.exc_q[e] = q;
         if (e == S.nexc) ++S.nexc;
       }
-      __syncwarp();
+      __syncthreads();
     }
-    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[6], (unsigned long long)(tt - tph)); tph = tt; }
+    KM_PHASE(6);
     // ---- loss after the update (chunk order, then fixed tree)
     double loss_m;
     {
@@ -1196,8 +1244,8 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
             float xv[8], wq[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              xv[u] = R.xs[sw_idx(lane, j + u)];
-              wq[u] = R.wv[sw_idx(lane, j + u)];
+              xv[u] = R.xs[R.idx(g.t, j + u)];
+              wq[u] = R.wv[R.idx(g.t, j + u)];
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -1211,29 +1259,24 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
               double cc = c;
               for (int e = 0; e < nexc; ++e)
                 if (S.exc_pos[e] == lo + j + u) cc = S.cen[S.exc_q[e]];
-              lb[u] = __dadd_rn(lb[u], __dmul_rn((double)R.wv[sw_idx(lane, j + u)],
-                                                 dcost((double)R.xs[sw_idx(lane, j + u)], cc)));
+              lb[u] = __dadd_rn(lb[u], __dmul_rn((double)R.wv[R.idx(g.t, j + u)],
+                                                 dcost((double)R.xs[R.idx(g.t, j + u)], cc)));
             }
           }
         }
         p = pend;
       }
       const double local = __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
-      loss_m = w_sum(local);
+      loss_m = g_sum(local, S, g);
     }
-    if (P.dbg && lane == 0) { const long long tt = clock64(); atomicAdd((unsigned long long*)&P.dbg[7], (unsigned long long)(tt - tph)); tph = tt; }
+    KM_PHASE(7);
     // ---- changed: new E-step labels vs the previous iteration's repaired
-    // assignment (lane 0; O(k^2))
-    int stop = 0;
-    if (lane == 0) {
-      changed = empties != 0;  // repairs count as changes
+    // assignment (thread 0; O(k^2)), convergence
+    if (g.t == 0) {
+      int changed = empties != 0;  // repairs count as changes
       if (iter > 0 && !changed) {
-        // previous exceptions: the new label must equal the repair cluster
-        for (int e = 0; e < S.pnexc && !changed; ++e) {
-          const int p = S.pexc_pos[e];
-          if (w_label_seg(S.seg, S.so, k, p) != S.pexc_q[e]) changed = 1;
-        }
-        // segment labels elsewhere
+        for (int e = 0; e < S.pnexc && !changed; ++e)
+          if (w_label_seg(S.seg, S.so, k, S.pexc_pos[e]) != S.pexc_q[e]) changed = 1;
         int ro = 0, rn = 0, pos = 0;
         while (pos < n && !changed) {
           while (ro < k - 1 && S.pseg[ro + 1] <= pos) ++ro;
@@ -1255,8 +1298,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
       }
       const bool stable = !changed && iter > 0;
       const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
-      stop = stable || tol || loss_m == 0.0;
-      // this iteration's assignment becomes the previous one
+      S.bci = stable || tol || loss_m == 0.0;
       for (int t = 0; t <= k; ++t) S.pseg[t] = S.seg[t];
       for (int t = 0; t < k; ++t) S.pso[t] = S.so[t];
       S.pnexc = S.nexc;
@@ -1264,79 +1306,86 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, const int
         S.pexc_pos[e] = S.exc_pos[e];
         S.pexc_q[e] = S.exc_q[e];
       }
+      if (P.dbg) {
+        atomicAdd((unsigned long long*)&P.dbg[2], 1ull);
+        if (empties) atomicAdd((unsigned long long*)&P.dbg[3], (unsigned long long)__popc(empties));
+      }
     }
     prev = loss_m;
-    if (P.dbg && lane == 0) {
-      atomicAdd((unsigned long long*)&P.dbg[2], 1ull);
-      if (empties) atomicAdd((unsigned long long*)&P.dbg[3], (unsigned long long)__popc(empties));
-    }
-    stop = __shfl_sync(kFull, stop, 0);
-    __syncwarp();
+    __syncthreads();
+    const int stop = S.bci;
+    __syncthreads();
     if (stop) break;
   }
   if (!need_loss) return 0.0;
   // final reassignment and loss (learner.cpp:305-311)
-  w_sort(S, k, lane);
+  w_sort(S, k, g);
   double local = 0.0;
   for (int p = lo, j = 0; p < hi; ++p, ++j) {
-    const double x = (double)R.xs[sw_idx(lane, j)];
+    const double x = (double)R.xs[R.idx(g.t, j)];
     const int q = w_nearest(x, S, k);
-    local = __dadd_rn(local, __dmul_rn((double)R.wv[sw_idx(lane, j)], dcost(x, S.cen[q])));
+    local = __dadd_rn(local, __dmul_rn((double)R.wv[R.idx(g.t, j)], dcost(x, S.cen[q])));
   }
-  return w_sum(local);
+  return g_sum(local, S, g);
 }
 
+// One CTA = one row group of G warps (blockDim.x = 32 G), persistent over rows.
 __global__ void __launch_bounds__(256) k_kmeans_warp(WkParams P) {
   extern __shared__ __align__(16) uint8_t dsmem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* mine = dsmem + (size_t)warp * P.warp_bytes;
-  WarpKm& S = *reinterpret_cast<WarpKm*>(mine);
-  float* xs = reinterpret_cast<float*>(mine + ((sizeof(WarpKm) + 15) & ~size_t(15)));
-  float* wv = xs + (size_t)P.C * 33;
+  Grp g;
+  g.t = threadIdx.x;
+  g.lane = threadIdx.x & 31;
+  g.warp = threadIdx.x >> 5;
+  g.G = blockDim.x >> 5;
+  g.T = blockDim.x;
+  WarpKm& S = *reinterpret_cast<WarpKm*>(dsmem);
+  double* FP = reinterpret_cast<double*>(dsmem + ((sizeof(WarpKm) + 15) & ~size_t(15)));
+  double* LP = FP + 3 * g.T;
+  float* xs = reinterpret_cast<float*>(dsmem + P.state_bytes);
   const int n = P.n, C = P.C, k = P.k;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
-  double* d2 = P.d2scr + (size_t)gw * C * 32;
-  const WRow R{xs, wv, n, C, lane * C, min(n, lane * C + C)};
+  float* wv = xs + (size_t)C * (g.T + 1);
+  double* d2 = P.d2scr + (size_t)blockIdx.x * C * g.T;
+  const WRow R{xs, wv, n, C, g.T, g.t * C, min(n, g.t * C + C), (n + C - 1) / C};
   while (true) {
-    int row = 0;
-    if (lane == 0) row = atomicAdd(P.row_counter, 1);
-    row = __shfl_sync(kFull, row, 0);
+    __syncthreads();
+    if (g.t == 0) S.bci = atomicAdd(P.row_counter, 1);
+    __syncthreads();
+    const int row = S.bci;
     if (row >= P.rows) break;
     const int* sv_row = P.svals + (size_t)row * n;
     const float* sk_row = P.skeys + (size_t)row * n;
     const float* xo = P.ws + (size_t)row * n;
     const float* wo = P.sw + (size_t)row * n;
     int bad = 0;
-    for (int p = lane; p < n; p += 32) {
+    for (int p = g.t; p < n; p += g.T) {
       const float w = wo[p];
       bad |= !(w >= 0.0f) || !isfinite(w);
     }
-    if (__any_sync(kFull, bad)) {  // KmProblem::validate (learner.cpp:10-23)
-      if (lane == 0) dev_fail(P.err, ANYQ_ERR_STATS);
+    if (__syncthreads_or(bad)) {  // KmProblem::validate (learner.cpp:10-23)
+      if (g.t == 0) dev_fail(P.err, ANYQ_ERR_STATS);
       continue;
     }
-    if (lane == 0) {
+    if (g.t == 0) {
       S.rng = Rng::for_row(P.seed, P.row_offset + row);
       S.pnexc = 0;
       S.nexc = 0;
     }
-    __syncwarp();
+    __syncthreads();
     double best = INFINITY;
     int bail = 0;
     for (int r = 0; r < P.restarts && !bail; ++r) {
       const long long t0 = clock64();
       if (P.init == ANYQ_INIT_KMPP || P.init == ANYQ_INIT_RANDOM) {
         // seeding works on the row in ORIGINAL order
-        w_load_row(n, C, lane, [&](int p, int si) {
+        w_load_row(R, g, [&](int p, int si) {
           xs[si] = xo[p];
           wv[si] = wo[p];
         });
-        __syncwarp();
-        if (P.init == ANYQ_INIT_KMPP) w_init_kmpp(R, sk_row, d2, S, k, lane);
-        else w_init_random(R, sk_row, S, k, lane);
-        __syncwarp();
+        __syncthreads();
+        if (P.init == ANYQ_INIT_KMPP) w_init_kmpp(R, sk_row, d2, S, k, g);
+        else w_init_random(R, sk_row, S, k, g);
       } else if (P.init == ANYQ_INIT_GRID) {
-        if (lane < k) S.cen[lane] = (double)(-(k / 2) + lane);
+        if (g.t < k) S.cen[g.t] = (double)(-(k / 2) + g.t);
       } else {
         const float nf4[16] = {-1.0f, -0.6961928009986877f, -0.5250730514526367f,
                                -0.39491748809814453f, -0.28444138169288635f,
@@ -1344,39 +1393,39 @@ __global__ void __launch_bounds__(256) k_kmeans_warp(WkParams P) {
                                0.07958029955625534f, 0.16093020141124725f, 0.24611230194568634f,
                                0.33791524171829224f, 0.44070982933044434f, 0.5626170039176941f,
                                0.7229568362236023f, 1.0f};
-        if (lane < k) S.cen[lane] = (double)nf4[lane & 15];
+        if (g.t < k) S.cen[g.t] = (double)nf4[g.t & 15];
       }
+      __syncthreads();
       // Lloyd works on the sorted row
-      w_load_row(n, C, lane, [&](int p, int si) {
+      w_load_row(R, g, [&](int p, int si) {
         xs[si] = sk_row[p];
         wv[si] = wo[sv_row[p]];
       });
-      __syncwarp();
+      __syncthreads();
       const long long t1 = clock64();
-      const double loss = w_lloyd(P, R, S, sv_row, lane, P.restarts > 1, &bail);
-      if (P.dbg && lane == 0) {
+      const double loss = w_lloyd(P, R, S, FP, LP, sv_row, g, P.restarts > 1, &bail);
+      if (P.dbg && g.t == 0) {
         atomicAdd((unsigned long long*)&P.dbg[0], (unsigned long long)(t1 - t0));
         atomicAdd((unsigned long long*)&P.dbg[1], (unsigned long long)(clock64() - t1));
       }
       if (!bail && (P.restarts == 1 || loss < best)) {
         best = loss;
-        if (lane < k) S.best_cen[lane] = S.cen[lane];
+        if (g.t < k) S.best_cen[g.t] = S.cen[g.t];
       }
-      __syncwarp();
+      __syncthreads();
     }
     if (bail) {
-      if (lane == 0) P.bail_rows[atomicAdd(P.bail_n, 1)] = row;
+      if (g.t == 0) P.bail_rows[atomicAdd(P.bail_n, 1)] = row;
       continue;
     }
     // best centroids -> sorted LUT + rank-remapped codes (learner.cpp:343-369)
-    if (lane < k) S.cen[lane] = S.best_cen[lane];
-    w_sort(S, k, lane);
-    if (lane < k) P.luts[(size_t)row * k + lane] = (float)S.sv[lane];
+    if (g.t < k) S.cen[g.t] = S.best_cen[g.t];
+    w_sort(S, k, g);
+    if (g.t < k) P.luts[(size_t)row * k + g.t] = (float)S.sv[g.t];
     for (int p = R.lo, j = 0; p < R.hi; ++p, ++j) {
-      const int q = w_nearest((double)xs[sw_idx(lane, j)], S, k);
+      const int q = w_nearest((double)xs[R.idx(g.t, j)], S, k);
       P.codes[(size_t)row * n + sv_row[p]] = (uint8_t)S.rank_of[q];
     }
-    __syncwarp();
   }
 }
 
@@ -1447,11 +1496,17 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
   // kernel below from the bail list.
   DevBuf<double> d2scr;
   DevBuf<int> bail(rows, s), bail_n(1, s), counter2(1, s);
-  const int64_t Cw = (cols + 31) / 32;
-  const uint32_t warp_bytes =
-      (uint32_t)(((sizeof(WarpKm) + 15) & ~size_t(15)) + ((2 * sizeof(float) * Cw * 33 + 15) & ~size_t(15)));
-  const int wpc = (int)std::min<int64_t>(8, (int64_t)max_optin / warp_bytes);
-  const bool use_warp = P.k <= kWK && !P.check_inv && wpc >= 1 && cols < (int64_t(1) << 30);
+  // row group size: ~64 samples per thread (more warps per row for long rows),
+  // ANYQ_KM_G overrides (1..8)
+  int G = (int)std::min<int64_t>(kMaxG, std::max<int64_t>(1, (cols + 2047) / 2048));
+  if (const char* e = std::getenv("ANYQ_KM_G")) G = std::max(1, std::min(kMaxG, std::atoi(e)));
+  const int T = 32 * G;
+  const int64_t Cw = (cols + T - 1) / T;
+  const uint32_t state_bytes =
+      (uint32_t)(((sizeof(WarpKm) + 15) & ~size_t(15)) + 2 * 3 * sizeof(double) * T);
+  const size_t cta_smem = state_bytes + ((2 * sizeof(float) * Cw * (T + 1) + 15) & ~size_t(15));
+  const bool use_warp = P.k <= kWK && !P.check_inv && cta_smem <= (size_t)max_optin &&
+                        cols < (int64_t(1) << 30);
   if (use_warp) {
     WkParams W;
     W.ws = ws;
@@ -1472,7 +1527,7 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
     W.codes = codes;
     W.err = err;
     W.row_counter = counter.p;
-    W.warp_bytes = warp_bytes;
+    W.state_bytes = state_bytes;
     static const bool km_debug = std::getenv("ANYQ_KM_DEBUG") != nullptr;
     DevBuf<long long> dbg;
     W.dbg = nullptr;
@@ -1481,17 +1536,17 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
       ANYQ_CUDA(cudaMemsetAsync(dbg.p, 0, 8 * sizeof(long long), s));
       W.dbg = dbg.p;
     }
-    const int smem = (int)(wpc * warp_bytes);
+    const int smem = (int)cta_smem;
     ANYQ_CUDA(cudaFuncSetAttribute(k_kmeans_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
-    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_warp, wpc * 32, smem));
-    const int blocks = (int)std::min<int64_t>((rows + wpc - 1) / wpc, (int64_t)sms * std::max(1, per_sm));
-    d2scr.alloc((size_t)blocks * wpc * Cw * 32, s);
+    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_warp, T, smem));
+    const int blocks = (int)std::min<int64_t>(rows, (int64_t)sms * std::max(1, per_sm));
+    d2scr.alloc((size_t)blocks * Cw * T, s);
     W.d2scr = d2scr.p;
     W.bail_rows = bail.p;
     W.bail_n = bail_n.p;
     ANYQ_CUDA(cudaMemsetAsync(bail_n.p, 0, sizeof(int), s));
-    k_kmeans_warp<<<blocks, wpc * 32, smem, s>>>(W);
+    k_kmeans_warp<<<blocks, T, smem, s>>>(W);
     ANYQ_LAUNCHED();
     if (km_debug) {
       long long h[8];
@@ -1500,9 +1555,9 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
       ANYQ_CUDA(cudaMemcpyAsync(&nb, bail_n.p, sizeof nb, cudaMemcpyDeviceToHost, s));
       ANYQ_CUDA(cudaStreamSynchronize(s));
       std::fprintf(stderr,
-                   "[kmeans warp] rows %lld n %lld warps/cta %d blocks %d: init %.0f cyc/row, lloyd %.0f "
+                   "[kmeans group] rows %lld n %lld warps/row %d blocks %d: init %.0f cyc/row, lloyd %.0f "
                    "cyc/row, iters/row %.2f, repairs %lld, bailed %d; per iter: E %.0f M %.0f rep %.0f loss %.0f\n",
-                   (long long)rows, (long long)cols, wpc, blocks, (double)h[0] / rows,
+                   (long long)rows, (long long)cols, G, blocks, (double)h[0] / rows,
                    (double)h[1] / rows, (double)h[2] / rows, h[3], nb, (double)h[4] / h[2], (double)h[5] / h[2],
                    (double)h[6] / h[2], (double)h[7] / h[2]);
     }
