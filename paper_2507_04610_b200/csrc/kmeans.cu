@@ -1330,7 +1330,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
 }
 
 // One CTA = one row group of G warps (blockDim.x = 32 G), persistent over rows.
-__global__ void __launch_bounds__(256) k_kmeans_warp(WkParams P) {
+__global__ void __launch_bounds__(256, 2) k_kmeans_warp(WkParams P) {
   extern __shared__ __align__(16) uint8_t dsmem[];
   Grp g;
   g.t = threadIdx.x;
@@ -1496,9 +1496,9 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
   // kernel below from the bail list.
   DevBuf<double> d2scr;
   DevBuf<int> bail(rows, s), bail_n(1, s), counter2(1, s);
-  // row group size: ~64 samples per thread (more warps per row for long rows),
-  // ANYQ_KM_G overrides (1..8)
-  int G = (int)std::min<int64_t>(kMaxG, std::max<int64_t>(1, (cols + 2047) / 2048));
+  // row group size: ~32 samples per thread (more warps per row for long rows;
+  // measured best on B200 for 4096-sample rows), ANYQ_KM_G overrides (1..8)
+  int G = (int)std::min<int64_t>(kMaxG, std::max<int64_t>(1, (cols + 1023) / 1024));
   if (const char* e = std::getenv("ANYQ_KM_G")) G = std::max(1, std::min(kMaxG, std::atoi(e)));
   const int T = 32 * G;
   const int64_t Cw = (cols + T - 1) / T;
