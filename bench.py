@@ -136,17 +136,28 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # synthetic any4 weights
 # ---------------------------------------------------------------------------
-def synthetic_qtensor(n, k, seed):
+def synthetic_qtensor(n, k, seed, fmt="any4"):
+    """Random-code tensor of a format: any4 / any3 (learned LUTs, sorted in the
+    scaled domain) or int4 / nf4 (the reference's fixed tables, asymmetric)."""
     from paper_2507_04610_b200 import _abi
     from paper_2507_04610_b200.qtensor import QuantizedTensor
 
     rng = np.random.default_rng(seed)
-    cfg = _abi.default_config(codebook=_abi.CB_ANY, group_size=GROUP)
+    cb = {"any4": _abi.CB_ANY, "any3": _abi.CB_ANY, "int4": 0, "nf4": 2}[fmt]
+    bits = 3 if fmt == "any3" else 4
+    cfg = _abi.default_config(codebook=cb, group_size=GROUP)
+    cfg.bits = bits
     qt = QuantizedTensor.empty(n, k, cfg)
-    qt.codes[:] = rng.integers(0, 256, qt.codes.size, dtype=np.uint8)
-    # any4 LUTs live in the scaled domain [0, 15], sorted (pack.hpp invariants)
-    lut = np.sort(rng.random((n, 16), dtype=np.float32) * 15.0, axis=1)
-    qt.luts[:] = lut.ravel()
+    if bits == 4:  # int4 / nf4 / any4: all 16 codes are valid
+        qt.codes[:] = rng.integers(0, 256, qt.codes.size, dtype=np.uint8)
+    else:  # any3: 3-bit packed codes
+        from paper_2507_04610_b200 import anyq
+
+        qt.codes[:] = anyq.pack_codes(rng.integers(0, 8, (n, k), dtype=np.uint8), bits).ravel()
+    if qt.luts is not None:
+        # learned LUTs live in the scaled domain [0, 15], sorted (pack.hpp invariants)
+        lut = np.sort(rng.random((n, 1 << bits), dtype=np.float32) * 15.0, axis=1)
+        qt.luts[:] = lut.ravel()
     qt.alphas[:] = (0.01 + 0.04 * rng.random(qt.alphas.size, dtype=np.float32))
     qt.betas[:] = -0.3 * rng.random(qt.betas.size, dtype=np.float32)
     return qt
@@ -479,6 +490,28 @@ def gpu_arm(args):
                                           "path": "gemv" if mm <= 2 else "tcgen05" if mm <= 16
                                           else "dequant+cublas"}
 
+    # ---- config 5 variants: int4 / nf4 (fixed tables) and any3 (3-bit codes on
+    # the 4-bit device layout) next to any4, q shape, AUTO path
+    variants = {}
+    if not args.quick and P == 1:
+        xq = {mm: torch.randn(mm, 4096, device=dev).to(torch.bfloat16) for mm in (1, 2, 16, 256)}
+        for fmt in ("any4", "int4", "nf4", "any3"):
+            vts = [anyq.DeviceTensor(synthetic_qtensor(4096, 4096, 77 + li, fmt)) for li in range(8)]
+            for mm in (1, 2, 16, 256):
+                yv = torch.empty(mm, 4096, device=dev, dtype=torch.bfloat16)
+
+                def onev():
+                    for vt in vts:
+                        vt.gemm_ptr(xq[mm].data_ptr(), mm, yv.data_ptr(), None, stream.cuda_stream)
+                us = time_graph(onev, 10) / len(vts)
+                bits = 3 if fmt == "any3" else 4
+                nb = algo_bytes(4096, 4096, mm, bits=bits)
+                variants[f"{fmt}_M{mm}"] = {"us": round(us, 3),
+                                            "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2),
+                                            "bits": bits}
+            for vt in vts:
+                vt.close()
+
     # ---- k-means quantizer throughput (config 1 / config 4): each rank quantizes
     # its 4096-row shard of a (4096*P) x 4096 gaussian matrix, device-resident,
     # rows keyed by global index (no collective); max time over ranks
@@ -510,6 +543,46 @@ def gpu_arm(args):
         kmeans = {"rows_per_s": round(4096 * P / secs, 1),
                   "matrix": f"{4096 * P}x4096 gaussian any4 g128, 4096 rows per GPU",
                   "seconds": round(secs, 4), "gpus": P}
+
+        # config 4, stratified: one Llama-3-8B layer's seven matrices (43,008 rows,
+        # 4,096 of them 14,336 long) with synthetic activation statistics, each
+        # matrix's rows partitioned over the ranks (row_offset keys the RNG by the
+        # matrix row); the full model is 32 such layers
+        from paper_2507_04610_b200.dist import row_range
+
+        mats = []
+        for i, (_, n, k) in enumerate(LAYER):
+            r0, r1 = row_range(n, P, rank)
+            gm = torch.Generator(device=dev)
+            gm.manual_seed(1 + i)
+            exj = torch.rand(k, device=dev, generator=gm) + 0.05
+            wm = torch.randn(max(r1 - r0, 1), k, device=dev, generator=gm)[: r1 - r0].contiguous()
+            mats.append((wm, exj, r0))
+        for wm, exj, r0 in mats:  # warm
+            if wm.shape[0]:
+                anyq.dev_quantize_any(wm, cfg, exj=exj, row_offset=r0)
+        torch.cuda.synchronize()
+        if P > 1:
+            dist.barrier()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
+        for wm, exj, r0 in mats:
+            if wm.shape[0]:
+                anyq.dev_quantize_any(wm, cfg, exj=exj, row_offset=r0)
+        k1.record()
+        torch.cuda.synchronize()
+        lsecs = k0.elapsed_time(k1) * 1e-3
+        if P > 1:
+            t = torch.tensor([lsecs], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            lsecs = float(t.item())
+        lrows = sum(n for (_, n, _) in LAYER)
+        kmeans["layer"] = {"rows_per_s": round(lrows / lsecs, 1), "rows": lrows,
+                           "weights": sum(n * k for (_, n, k) in LAYER),
+                           "seconds": round(lsecs, 4),
+                           "full_8b_model_seconds_extrapolated": round(32 * lsecs, 2),
+                           "stats": "synthetic E|x_j| ~ U(0.05, 1.05)",
+                           "shapes": "q,k,v,o,gate,up (K=4096), down (K=14336)"}
 
     # roofline of the dominant kernel: the step IS one k_lutgemv chain launch per
     # layer at M=1 (P=1), so its launch duration is the step time
@@ -573,6 +646,7 @@ def gpu_arm(args):
             "per_shape": per_shape,
             "m_sweep": sweep,
             "kmeans": kmeans,
+            "variants_q_shape": variants,
             "pct_hbm_peak_step": round(100 * value / peak, 2),
         }
         print(json.dumps(line), flush=True)

@@ -32,6 +32,8 @@
 //    order by the last-arriving CTA (deterministic, self-resetting counters).
 #include <cuda_bf16.h>
 
+#include <vector>
+
 #include "kernels.cuh"
 #include "lutgemm.cuh"
 
@@ -776,7 +778,9 @@ void launch_mp(const LutTensor* t, const void* x, int64_t m, void* y, float* y32
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt) {
   const anyq_config& c = qt->cfg;
-  if (c.bits != 4) fail(ANYQ_ERR_CONFIG, "tensor-core LUT GEMM needs 4-bit codes");
+  // 2/3/4-bit codes share the 4-bit device layout (a 2^bits-entry LUT padded to 16)
+  if (c.bits != 2 && c.bits != 3 && c.bits != 4)
+    fail(ANYQ_ERR_CONFIG, "device LUT GEMM needs codes of at most 4 bits");
   if (c.granularity != ANYQ_G_GROUP && c.granularity != ANYQ_G_ROW)
     fail(ANYQ_ERR_CONFIG, "tensor-core LUT GEMM needs rowwise or groupwise scales");
   if (c.granularity == ANYQ_G_GROUP && c.group_size % 128 != 0)
@@ -800,10 +804,10 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
     t->weight_bytes = rows * ((cols * 4 + 7) / 8) + ng * 4 + rows * 16 * 2;
 
     // logical row-major codes on device
-    const int64_t nb = rows * packed_bpr(cols, 4);
+    const int64_t nb = rows * packed_bpr(cols, c.bits);
     DevBuf<uint8_t> dp(nb), logical(rows * cols), tmp;
     dp.upload(qt->codes, nb);
-    launch_unpack(dp.p, rows, cols, 4, logical.p, 0);
+    launch_unpack(dp.p, rows, cols, c.bits, logical.p, 0);
     if (qt->layout == ANYQ_LAYOUT_KTILED) {
       tmp.alloc(rows * cols);
       launch_ktile(logical.p, rows, cols, qt->tile_k, 1, tmp.p, 0);
@@ -826,8 +830,12 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
 
     DevBuf<float> luts, table16(16), alphas(ng), betas(ng);
     if (c.codebook == ANYQ_CB_ANY) {
+      const int L = 1 << c.bits;
+      std::vector<float> l16((size_t)rows * 16, 0.0f);
+      for (int64_t r = 0; r < rows; ++r)
+        for (int i = 0; i < L; ++i) l16[(size_t)r * 16 + i] = qt->luts[(size_t)r * L + i];
       luts.alloc(rows * 16);
-      luts.upload(qt->luts, rows * 16);
+      luts.upload(l16.data(), rows * 16);
     }
     table16.upload(fixed.v, 16);
     // scales in [row][GR] order (rowwise: GR == 1 per row)

@@ -144,9 +144,10 @@ def tc_tolerance(orc, x, qt):
 
 
 @pytest.mark.parametrize("path", ["gemv", "tc"])
-@pytest.mark.parametrize("fmt", ["any4", "int4", "nf4", "fp4"])
+@pytest.mark.parametrize("fmt", ["any4", "int4", "nf4", "fp4", "any3", "any2"])
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8, 9, 16])
 def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m, path):
+    """any3 / any2 run on the 4-bit device layout (2^bits-entry LUT padded to 16)."""
     if path == "gemv" and m > 2:
         pytest.skip("the GEMV serves m <= 2")
     n, k = 200, 384  # ragged rows (not a multiple of 32), 3 chunks, 3 groups
