@@ -146,6 +146,21 @@ anyq_status anyq_narrow_inplace(anyq_qtensor* qt);
 anyq_status anyq_dequantize(const anyq_qtensor* qt, float* w_out);
 
 /* ---------------------------------------------------------------------------
+ * Scaling (host buffers). Group map: cfg->granularity / group_size / block_size
+ * (ScaleSet::group_of, scaling.hpp:36-45); alphas/betas hold num_groups entries.
+ * ------------------------------------------------------------------------- */
+/* scaling.hpp:52 compute_scales(w, cfg, qmin, qmax): per-group min/max -> alpha, beta. */
+anyq_status anyq_compute_scales(const float* w, int64_t rows, int64_t cols, const anyq_config* cfg,
+                                float qmin, float qmax, float* alphas, float* betas);
+/* scaling.hpp:56 scale_weights(w, s): ws = (w - beta_g) / alpha_g. */
+anyq_status anyq_scale_weights(const float* w, int64_t rows, int64_t cols, const anyq_config* cfg,
+                               const float* alphas, const float* betas, float* ws);
+/* scaling.hpp:60 dequantize(values, s): out = alpha_g * v + beta_g. */
+anyq_status anyq_dequantize_values(const float* v, int64_t rows, int64_t cols,
+                                   const anyq_config* cfg, const float* alphas,
+                                   const float* betas, float* out);
+
+/* ---------------------------------------------------------------------------
  * GEMM (host buffers)
  * ------------------------------------------------------------------------- */
 

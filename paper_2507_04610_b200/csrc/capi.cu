@@ -417,6 +417,50 @@ anyq_status anyq_narrow_inplace(anyq_qtensor* qt) {
   });
 }
 
+anyq_status anyq_compute_scales(const float* w, int64_t rows, int64_t cols, const anyq_config* cfg,
+                                float qmin, float qmax, float* alphas, float* betas) {
+  return guard([&] {
+    validate_config(*cfg, rows, cols);
+    if (!(qmax > qmin)) fail(ANYQ_ERR_CONFIG, "qmax must exceed qmin");
+    if (cfg->symmetric && !(qmax > 0)) fail(ANYQ_ERR_CONFIG, "symmetric scaling needs qmax > 0");
+    const int64_t ng = group_count(*cfg, rows, cols);
+    DevBuf<float> dw(rows * cols), da(ng), db(ng);
+    DevBuf<int> err(1);
+    err.zero();
+    dw.upload(w, rows * cols);
+    launch_check_finite(dw.p, rows * cols, err.p, ANYQ_ERR_NONFINITE, 0);
+    ANYQ_CUDA(cudaDeviceSynchronize());
+    check_device_error(err.p, "compute_scales");
+    launch_scales(dw.p, rows, cols, *cfg, qmin, qmax, da.p, db.p, 0);
+    da.download(alphas, ng);
+    db.download(betas, ng);
+  });
+}
+
+static anyq_status affine_host(const float* in, int64_t rows, int64_t cols, const anyq_config* cfg,
+                               const float* alphas, const float* betas, int inverse, float* out) {
+  return guard([&] {
+    const int64_t ng = group_count(*cfg, rows, cols);
+    DevBuf<float> din(rows * cols), dout(rows * cols), da(ng), db(ng);
+    din.upload(in, rows * cols);
+    da.upload(alphas, ng);
+    db.upload(betas, ng);
+    if (rows * cols > 0) launch_affine(din.p, rows, cols, *cfg, da.p, db.p, inverse, dout.p, 0);
+    dout.download(out, rows * cols);
+  });
+}
+
+anyq_status anyq_scale_weights(const float* w, int64_t rows, int64_t cols, const anyq_config* cfg,
+                               const float* alphas, const float* betas, float* ws) {
+  return affine_host(w, rows, cols, cfg, alphas, betas, 1, ws);
+}
+
+anyq_status anyq_dequantize_values(const float* v, int64_t rows, int64_t cols,
+                                   const anyq_config* cfg, const float* alphas,
+                                   const float* betas, float* out) {
+  return affine_host(v, rows, cols, cfg, alphas, betas, 0, out);
+}
+
 anyq_status anyq_dequantize(const anyq_qtensor* qt, float* w_out) {
   return guard([&] {
     check_qt(qt);

@@ -16,6 +16,9 @@ void launch_scales(const float* w, int64_t rows, int64_t cols, const anyq_config
 void launch_scale_rows(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg,
                        const float* alphas, const float* betas, const float* exj, float* ws,
                        float* sw, int* err, cudaStream_t s);
+void launch_affine(const float* in, int64_t rows, int64_t cols, const anyq_config& cfg,
+                   const float* alphas, const float* betas, int inverse, float* out,
+                   cudaStream_t s);
 void launch_round(const float* ws, int64_t n, const Table& t, uint8_t* codes, cudaStream_t s);
 void launch_pack(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
                  int* err, cudaStream_t s);

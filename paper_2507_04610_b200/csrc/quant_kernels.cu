@@ -376,6 +376,30 @@ void launch_scale_rows(const float* w, int64_t rows, int64_t cols, const anyq_co
   ANYQ_LAUNCHED();
 }
 
+// scale_weights (inverse = 1, scaling.cpp:72-83) / dequantize(values, s)
+// (inverse = 0, scaling.cpp:85-96), element-wise in the reference's order of
+// operations (no contraction).
+__global__ void k_affine(const float* __restrict__ in, int64_t rows, int64_t cols, GroupMap gm,
+                         const float* __restrict__ alphas, const float* __restrict__ betas,
+                         int inverse, float* __restrict__ out) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    const int64_t g = gm(i, j);
+    out[e] = inverse ? __fdiv_rn(__fsub_rn(in[e], betas[g]), alphas[g])
+                     : __fadd_rn(__fmul_rn(alphas[g], in[e]), betas[g]);
+  }
+}
+
+void launch_affine(const float* in, int64_t rows, int64_t cols, const anyq_config& cfg,
+                   const float* alphas, const float* betas, int inverse, float* out,
+                   cudaStream_t s) {
+  GroupMap gm = make_group_map(cfg, cols);
+  k_affine<<<grid_for(rows * cols), 256, 0, s>>>(in, rows, cols, gm, alphas, betas, inverse, out);
+  ANYQ_LAUNCHED();
+}
+
 void launch_round(const float* ws, int64_t n, const Table& t, uint8_t* codes, cudaStream_t s) {
   k_round_to_table<<<grid_for(n), 256, 0, s>>>(ws, n, t, codes);
   ANYQ_LAUNCHED();

@@ -10,6 +10,8 @@
 //   narrowed        pack.hpp:68        to_ktiled / from_ktiled  pack.hpp:86-87
 //   dequantize(qt)  pack.hpp:98        gemm_dense / gemm_reference / gemm_fused
 //                                                      qgemm.hpp:28-37
+//   compute_scales  scaling.hpp:52     scale_weights   scaling.hpp:56
+//   dequantize(values, s)  scaling.hpp:60
 //
 // Linking this object before the reference objects (tests/reftests/Makefile
 // weakens the latter) swaps the hot path of an unmodified reference build —
@@ -22,6 +24,7 @@
 #include "anyq/pack.hpp"
 #include "anyq/qgemm.hpp"
 #include "anyq/quantize.hpp"
+#include "anyq/scaling.hpp"
 #include "anyq_b200.h"
 
 namespace anyq {
@@ -136,7 +139,57 @@ QuantizedTensor quantize_impl(const Eigen::Ref<const Matf>& w, const QuantConfig
   return qt;
 }
 
+// The group map of a ScaleSet as a C config (granularity, group/block sizes).
+anyq_config group_cfg(const ScaleSet& s) {
+  anyq_config c;
+  anyq_config_default(&c);
+  c.granularity = static_cast<int32_t>(s.granularity);
+  if (s.group_size > 0) c.group_size = s.group_size;
+  if (s.block_size > 0) c.block_size = s.block_size;
+  c.symmetric = s.symmetric ? 1 : 0;
+  return c;
+}
+
+Matf affine(const Eigen::Ref<const Matf>& in, const ScaleSet& s, bool inverse) {
+  const anyq_config c = group_cfg(s);
+  const std::vector<float> f = flat(in);
+  Matf out(in.rows(), in.cols());
+  if (inverse)
+    check(anyq_scale_weights(f.data(), in.rows(), in.cols(), &c, s.alphas.data(), s.betas.data(),
+                             out.data()));
+  else
+    check(anyq_dequantize_values(f.data(), in.rows(), in.cols(), &c, s.alphas.data(),
+                                 s.betas.data(), out.data()));
+  return out;
+}
+
 }  // namespace
+
+ScaleSet compute_scales(const Eigen::Ref<const Matf>& w, const QuantConfig& cfg, Real qmin,
+                        Real qmax) {
+  const anyq_config c = to_c(cfg);
+  const int64_t ng = anyq_num_groups(&c, w.rows(), w.cols());
+  if (ng < 0) throw ConfigError("unknown granularity");
+  ScaleSet s = empty_scales(cfg, w.rows(), w.cols(), ng);
+  s.group_size = cfg.group_size;  // compute_scales records both sizes (scaling.cpp:40-41)
+  s.block_size = cfg.block_size;
+  const std::vector<float> f = flat(w);
+  check(anyq_compute_scales(f.data(), w.rows(), w.cols(), &c, qmin, qmax, s.alphas.data(),
+                            s.betas.data()));
+  return s;
+}
+
+Matf scale_weights(const Eigen::Ref<const Matf>& w, const ScaleSet& s) {
+  if (w.rows() != s.rows || w.cols() != s.cols)
+    throw ShapeError("scale_weights: matrix shape does not match scale set");
+  return affine(w, s, true);
+}
+
+Matf dequantize(const Eigen::Ref<const Matf>& values, const ScaleSet& s) {
+  if (values.rows() != s.rows || values.cols() != s.cols)
+    throw ShapeError("dequantize: matrix shape does not match scale set");
+  return affine(values, s, false);
+}
 
 QuantizedTensor quantize_any(const Eigen::Ref<const Matf>& w, const QuantConfig& cfg,
                              const Vecf* exj, int /*threads: the GPU ignores it; results are
