@@ -487,7 +487,7 @@ def gpu_arm(args):
                                           "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2),
                                           "TFLOPs": round(tf, 1),
                                           "pct_bf16_peak": round(100 * tf / tpeak, 2),
-                                          "path": "gemv" if mm <= 2 else "tcgen05" if mm <= 16
+                                          "path": "gemv" if mm <= 2 else "tcgen05" if mm <= 8
                                           else "dequant+cublas"}
 
     # ---- config 5 variants: int4 / nf4 (fixed tables) and any3 (3-bit codes on

@@ -546,8 +546,10 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
   return guard([&] {
     const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
     if (path == ANYQ_PATH_AUTO)
+      // measured crossovers on B200 (profiles/round1.md): the tcgen05 LUT GEMM
+      // wins for 3 <= m <= 8, dequant + cuBLAS from m = 16 on
       path = lutgemv_fits(lt, m) ? ANYQ_PATH_GEMV
-             : m <= 16                              ? ANYQ_PATH_TC
+             : m <= 8                               ? ANYQ_PATH_TC
                                                     : ANYQ_PATH_DEQUANT;
     if (path == ANYQ_PATH_GEMV)
       lutgemv_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);

@@ -17,63 +17,88 @@ namespace anyq_b200 {
 
 namespace {
 
-constexpr int64_t kSliceRows = 4096;  // row-block slice dequantized per GEMM (bounded workspace)
+constexpr int64_t kSliceRows = 8192;  // row-block slice dequantized per GEMM (bounded workspace)
 
-// One thread per (row, slab): 16 code bytes -> 32 bf16 weights at
-// k = 128c + 64h + 16q + 2j (+1), h = byte/8, j = byte%8 (layout of lutgemm.cu).
-__global__ void k_dequant_bf16(const uint4* __restrict__ codes, const uint4* __restrict__ lut,
-                               const __half2* __restrict__ ab, int rb0, int nrb, int C, int GR,
-                               int gshift_chunks, int64_t K, __nv_bfloat16* __restrict__ w) {
-  const int64_t total = (int64_t)nrb * C * 4 * 32;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int lane = (int)(i & 31);
-    const int q = (int)((i >> 5) & 3);
-    const int64_t cc = i >> 7;  // (row block, chunk)
-    const int c = (int)(cc % C);
-    const int rbl = (int)(cc / C);
+// One warp per (row block, 128-k chunk) item, lane L = row L. The lane's 16
+// dequantised values alpha_g * T[i] + beta_g (fp32, no contraction:
+// qgemm.cpp:98-111, rounded once to bf16) go to a per-warp table tbl[i][lane]
+// (bank = lane: conflict free); the chunk's 128 codes become 128 table reads.
+// Byte b of slab q holds k = 128c + 16q + 2b (+1) for b < 8 and
+// 128c + 64 + 16q + 2(b-8) (+1) for b >= 8 (layout of lutgemm.cu). The 32 x 128
+// bf16 tile is staged in shared memory (rows padded to 272 B: conflict free)
+// and written out as whole 256-B row segments (coalesced).
+constexpr int kDqWarps = 4;
+constexpr int kTileStride = 136;  // bf16 per staged row (128 + 8 pad)
+__global__ void __launch_bounds__(kDqWarps * 32) k_dequant_bf16(
+    const uint4* __restrict__ codes, const uint4* __restrict__ lut, const __half2* __restrict__ ab,
+    int rb0, int nrb, int C, int GR, int gshift_chunks, int64_t K, __nv_bfloat16* __restrict__ w) {
+  __shared__ uint32_t tbl_all[kDqWarps][16][32];
+  __shared__ __align__(16) __nv_bfloat16 tile_all[kDqWarps][32 * kTileStride];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t(*tbl)[32] = tbl_all[warp];
+  __nv_bfloat16* tile = tile_all[warp];
+  const bool vec = (K & 7) == 0;  // 16-B aligned rows
+  int cur_rb = -1;
+  float t[16];
+  for (int it = blockIdx.x * kDqWarps + warp; it < nrb * C; it += gridDim.x * kDqWarps) {
+    const int rbl = it / C, c = it - rbl * C;
     const int rb = rb0 + rbl;
-    const uint4 w4 = codes[((int64_t)rb * C + c) * 128 + q * 32 + lane];
     const int64_t row = (int64_t)rb * 32 + lane;
-    __half t[16];
-    {
+    if (rb != cur_rb) {
       const uint4 l0 = lut[row * 2], l1 = lut[row * 2 + 1];
       const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const __half2 h2 = *reinterpret_cast<const __half2*>(&lw[j]);
-        t[2 * j] = __low2half(h2);
-        t[2 * j + 1] = __high2half(h2);
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&lw[j]));
+        t[2 * j] = f.x;
+        t[2 * j + 1] = f.y;
       }
+      cur_rb = rb;
     }
     const int g = gshift_chunks >= 30 ? 0 : (c >> gshift_chunks);
     const float2 s = __half22float2(ab[((int64_t)rb * GR + g) * 32 + lane]);
-    const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
-    __nv_bfloat16 out[32];
+    const uint4* cp = codes + ((int64_t)rb * C + c) * 128 + lane;
+    uint4 w4[4];
 #pragma unroll
-    for (int b = 0; b < 16; ++b) {
-      const uint32_t byte = (wd[b >> 2] >> (8 * (b & 3))) & 0xffu;
-      // fp32 alpha * T + beta, no contraction (qgemm.cpp:98-111 order)
-      out[2 * b] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(s.x, __half2float(t[byte & 15])), s.y));
-      out[2 * b + 1] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(s.x, __half2float(t[byte >> 4])), s.y));
+    for (int q = 0; q < 4; ++q) w4[q] = cp[q * 32];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      tbl[i][lane] = (uint32_t)__bfloat16_as_ushort(
+          __float2bfloat16_rn(__fadd_rn(__fmul_rn(s.x, t[i]), s.y)));
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t wd[4] = {w4[q].x, w4[q].y, w4[q].z, w4[q].w};
+      uint32_t o[16];
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const uint32_t byte = (wd[b >> 2] >> (8 * (b & 3))) & 0xffu;
+        o[b] = tbl[byte & 15][lane] | (tbl[byte >> 4][lane] << 16);
+      }
+      uint4* trow = reinterpret_cast<uint4*>(tile + lane * kTileStride + q * 16);
+      trow[0] = make_uint4(o[0], o[1], o[2], o[3]);
+      trow[1] = make_uint4(o[4], o[5], o[6], o[7]);
+      trow[8] = make_uint4(o[8], o[9], o[10], o[11]);    // k + 64
+      trow[9] = make_uint4(o[12], o[13], o[14], o[15]);
     }
-    __nv_bfloat16* dst = w + (int64_t)rbl * 32 * K + (int64_t)lane * K + (int64_t)c * 128 + q * 16;
-    // bytes 0..7 -> k = 128c + 16q + [0,16); bytes 8..15 -> k = 128c + 64 + 16q + [0,16)
-    const int64_t k0 = (int64_t)c * 128 + q * 16;
-    const bool vec = (K & 7) == 0;  // 16-B aligned rows
-    if (vec && k0 + 16 <= K) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&out[0]);
-      *reinterpret_cast<uint4*>(dst + 8) = *reinterpret_cast<const uint4*>(&out[8]);
-    } else {
-      for (int j = 0; j < 16; ++j)
-        if (k0 + j < K) dst[j] = out[j];
-    }
-    if (vec && k0 + 64 + 16 <= K) {
-      *reinterpret_cast<uint4*>(dst + 64) = *reinterpret_cast<const uint4*>(&out[16]);
-      *reinterpret_cast<uint4*>(dst + 72) = *reinterpret_cast<const uint4*>(&out[24]);
-    } else {
-      for (int j = 0; j < 16; ++j)
-        if (k0 + 64 + j < K) dst[64 + j] = out[16 + j];
+    __syncwarp();
+    // write-out: 16 lanes per row (16 B each) -> 2 rows per instruction
+    const int64_t k0 = (int64_t)c * 128;
+    const int half = lane >> 4, seg = lane & 15;
+#pragma unroll 4
+    for (int r = 0; r < 32; r += 2) {
+      const int rr = r + half;
+      const uint4 v = *reinterpret_cast<const uint4*>(tile + rr * kTileStride + seg * 8);
+      __nv_bfloat16* dst = w + ((int64_t)rbl * 32 + rr) * K + k0 + seg * 8;
+      if (vec && k0 + seg * 8 + 8 <= K) {
+        *reinterpret_cast<uint4*>(dst) = v;
+      } else {
+        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < 8; ++j)
+          if (k0 + seg * 8 + j < K)
+            dst[j] = __ushort_as_bfloat16((unsigned short)(vv[j / 2] >> (16 * (j & 1))));
+      }
     }
   }
 }
@@ -117,16 +142,12 @@ void dequant_gemm_run(const LutTensor* t, const void* x, int64_t m, void* y, flo
   const int64_t K = t->cols, N = t->rows;
   const int slice_rb = (int)(kSliceRows / 32);
   const int64_t srows = std::min<int64_t>(kSliceRows, (int64_t)t->RB * 32);
-  // workspace kept on the tensor (first use sizes it; later calls are graph-capturable)
-  LutTensor* mt = const_cast<LutTensor*>(t);
-  if (!mt->dq_w) ANYQ_CUDA(cudaMalloc(&mt->dq_w, sizeof(__nv_bfloat16) * srows * K));
-  if (m * srows > mt->dq_acc_n) {
-    if (mt->dq_acc) ANYQ_CUDA(cudaFree(mt->dq_acc));
-    ANYQ_CUDA(cudaMalloc(&mt->dq_acc, sizeof(float) * m * srows));
-    mt->dq_acc_n = m * srows;
-  }
-  __nv_bfloat16* wbuf = reinterpret_cast<__nv_bfloat16*>(mt->dq_w);
-  float* accbuf = mt->dq_acc;
+  // stream-ordered workspace from the retained pool: no allocation on the hot
+  // path after the first call, and capturable into CUDA graphs (memory nodes)
+  DevBuf<__nv_bfloat16> wws(srows * K, s);
+  __nv_bfloat16* wbuf = wws.p;
+  DevBuf<float> accw;
+  if (y32) accw.alloc(m * srows, s);
   Blas& B = blas();
   std::lock_guard<std::mutex> lock(B.mu);
   if (!B.h) check_blas(cublasCreate(&B.h), "cublasCreate");
@@ -136,20 +157,32 @@ void dequant_gemm_run(const LutTensor* t, const void* x, int64_t m, void* y, flo
     const int nrb = std::min(slice_rb, t->RB - rb0);
     const int64_t row0 = (int64_t)rb0 * 32;
     const int64_t nrows = std::min<int64_t>((int64_t)nrb * 32, N - row0);
-    const int64_t items = (int64_t)nrb * t->C * 128;
-    k_dequant_bf16<<<(unsigned)std::min<int64_t>((items + 255) / 256, 148 * 16), 256, 0, s>>>(
+    const int items = nrb * t->C;
+    k_dequant_bf16<<<(unsigned)std::max(1, std::min((items + kDqWarps - 1) / kDqWarps, t->sms * 16)),
+                     kDqWarps * 32, 0, s>>>(
         reinterpret_cast<const uint4*>(t->codes), reinterpret_cast<const uint4*>(t->lut), t->ab,
         rb0, nrb, t->C, t->GR, gshift, K, wbuf);
     ANYQ_LAUNCHED();
-    // column-major view: acc^T[nrows x m] = W[nrows x K] (row-major = col-major K x nrows)^T * x^T
-    check_blas(cublasGemmEx(B.h, CUBLAS_OP_T, CUBLAS_OP_N, (int)nrows, (int)m, (int)K, &one, wbuf,
-                            CUDA_R_16BF, (int)K, x, CUDA_R_16BF, (int)K, &zero, accbuf, CUDA_R_32F,
-                            (int)nrows, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
-               "cublasGemmEx");
-    note_launch();
-    k_f32_to_outputs<<<(unsigned)std::min<int64_t>((m * nrows + 255) / 256, 148 * 8), 256, 0, s>>>(
-        accbuf, m, nrows, N, row0, reinterpret_cast<__nv_bfloat16*>(y), y32);
-    ANYQ_LAUNCHED();
+    // column-major view: y^T[nrows x m] (ld N, starting at column row0 of y) =
+    // W[nrows x K] (row-major = col-major K x nrows)^T * x^T; bf16 output
+    // straight from the GEMM (fp32 accumulation) unless fp32 y is requested
+    if (!y32) {
+      check_blas(cublasGemmEx(B.h, CUBLAS_OP_T, CUBLAS_OP_N, (int)nrows, (int)m, (int)K, &one, wbuf,
+                              CUDA_R_16BF, (int)K, x, CUDA_R_16BF, (int)K, &zero,
+                              reinterpret_cast<__nv_bfloat16*>(y) + row0, CUDA_R_16BF, (int)N,
+                              CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+                 "cublasGemmEx");
+      note_launch();
+    } else {
+      check_blas(cublasGemmEx(B.h, CUBLAS_OP_T, CUBLAS_OP_N, (int)nrows, (int)m, (int)K, &one, wbuf,
+                              CUDA_R_16BF, (int)K, x, CUDA_R_16BF, (int)K, &zero, accw.p, CUDA_R_32F,
+                              (int)nrows, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+                 "cublasGemmEx");
+      note_launch();
+      k_f32_to_outputs<<<(unsigned)std::min<int64_t>((m * nrows + 255) / 256, 148 * 8), 256, 0, s>>>(
+          accw.p, m, nrows, N, row0, reinterpret_cast<__nv_bfloat16*>(y), y32);
+      ANYQ_LAUNCHED();
+    }
   }
 }
 

@@ -258,6 +258,6 @@ def test_dequant_gemm_large_m(aq, orc, cuda, m, n, k, g):
     ref = orc.gemm_reference(x, nq)
     tol = 2.0 ** -8 * (np.abs(x) @ np.abs(orc.dequantize(nq)).T) + 1e-30
     assert np.all(np.abs(y32 - ref) <= tol)
-    if m > 16:  # AUTO picks this path above m = 16
+    if m > 8:  # AUTO picks this path above m = 8
         y32a, _ = tc_gemm(aq, cuda, qt, x, 0)
         assert bits_equal(y32a, y32)
