@@ -101,7 +101,9 @@ __device__ double block_sum(double v, Shared& sh) {
     sh.dbl_bcast = s;
   }
   __syncthreads();
-  return sh.dbl_bcast;
+  const double r = sh.dbl_bcast;
+  __syncthreads();  // the slot is rewritten by the next broadcast
+  return r;
 }
 
 __device__ long long block_min_ll(long long v, Shared& sh) {
@@ -116,7 +118,9 @@ __device__ long long block_min_ll(long long v, Shared& sh) {
     sh.ll_bcast = s;
   }
   __syncthreads();
-  return sh.ll_bcast;
+  const long long r = sh.ll_bcast;
+  __syncthreads();  // the slot is rewritten by the next broadcast
+  return r;
 }
 
 __device__ long long block_max_ll(long long v, Shared& sh) { return -block_min_ll(-v, sh); }
