@@ -304,7 +304,18 @@ def gpu_arm(args):
 
     # buffers: layer input x, per-layer local y shards, gathered y (TP)
     x_in = torch.randn(M, 4096, device=dev).to(torch.bfloat16)
-    ys = [[torch.empty(M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L] for L in layers]
+    # the seven outputs of a layer are views into one flat buffer (one D2H copy per step)
+    ybufs = [torch.empty(M * sum(ns for (_, ns, _, _) in L), device=dev, dtype=torch.bfloat16)
+             for L in layers]
+
+    def split_views(buf, L):
+        out, off = [], 0
+        for (_, ns, _, _) in L:
+            out.append(buf[off:off + M * ns].view(M, ns))
+            off += M * ns
+        return out
+
+    ys = [split_views(ybufs[li], L) for li, L in enumerate(layers)]
     # TP gather buffers: all_gather_into_tensor concatenates the [M, N/P] slices
     # along dim 0 -> [P*M, N/P]; for M = 1 that memory IS the [1, N] row
     yg = [[torch.empty(P * M, ns, device=dev, dtype=torch.bfloat16) for (_, ns, _, _) in L]
@@ -400,6 +411,7 @@ def gpu_arm(args):
     xh = torch.randn(M, 4096).to(torch.bfloat16).pin_memory()
     yh = [[torch.empty(M, ns * P, dtype=torch.bfloat16).pin_memory() for (_, ns, _, _) in L]
           for L in layers]
+    yhflat = [torch.empty(ybufs[li].numel(), dtype=torch.bfloat16).pin_memory() for li in range(len(layers))]
 
     def e2e_step(i, s):
         li = i % len(layers)
@@ -408,8 +420,11 @@ def gpu_arm(args):
             graphs[li].replay()
         else:
             run_layer(li, s)
-        for j in range(7):
-            yh[li][j].copy_(gathered(li, j) if P > 1 else ys[li][j], non_blocking=True)
+        if P > 1:
+            for j in range(7):
+                yh[li][j].copy_(gathered(li, j), non_blocking=True)
+        else:  # one D2H copy of the layer's seven outputs
+            yhflat[li].copy_(ybufs[li], non_blocking=True)
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
