@@ -657,7 +657,7 @@ struct WarpKm {
   double cen[kWK], best_cen[kWK], sv[kWK];
   double swx[kWK], sw[kWK], sx[kWK];
   int so[kWK], rank_of[kWK], cnt[kWK];
-  int seg[kWK + 1], pseg[kWK + 1], pso[kWK];
+  int seg[kWK + 1], pseg[kWK + 1], pso[kWK], prank[kWK];
   int exc_pos[kWK], exc_q[kWK], pexc_pos[kWK], pexc_q[kWK];
   int nexc, pnexc;
   long long vkeys[2 * kWK], vvals[2 * kWK];
@@ -771,9 +771,12 @@ __device__ __forceinline__ void w_sort(WarpKm& S, int k, const Grp& g) {
   if (g.t < k) {
     const double v = S.cen[g.t];
     int r = 0;
-    for (int p = 0; p < k; ++p) {
-      const double u = S.cen[p];
-      r += (u < v) || (u == v && p < g.t);
+#pragma unroll
+    for (int p = 0; p < kWK; ++p) {  // independent loads (k <= kWK)
+      if (p < k) {
+        const double u = S.cen[p];
+        r += (u < v) || (u == v && p < g.t);
+      }
     }
     S.rank_of[g.t] = r;
     S.sv[r] = v;
@@ -1002,14 +1005,22 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     long long tph = clock64();
     // ---- E-step: segment boundaries of the sorted row by the exact predicate
     w_sort(S, k, g);
+    KM_PHASE(8);
     {
+      double svr[kWK];
+#pragma unroll
+      for (int r = 0; r < kWK; ++r) svr[r] = r < k ? S.sv[r] : 0.0;  // independent loads
       double cmax = 0.0;
       bool near_dup = false;
-      for (int r = 0; r < k; ++r) cmax = fmax(cmax, fabs(S.sv[r]));
+#pragma unroll
+      for (int r = 0; r < kWK; ++r) cmax = fmax(cmax, fabs(svr[r]));
       const double thresh = ldexp(xmax + cmax, -40);
-      for (int r = 0; r + 1 < k; ++r) {
-        const double gap = __dsub_rn(S.sv[r + 1], S.sv[r]);
-        near_dup |= (gap > 0.0 && gap < thresh) || !(gap >= 0.0);
+#pragma unroll
+      for (int r = 0; r + 1 < kWK; ++r) {
+        if (r + 1 < k) {
+          const double gap = __dsub_rn(svr[r + 1], svr[r]);
+          near_dup |= (gap > 0.0 && gap < thresh) || !(gap >= 0.0);
+        }
       }
       if (near_dup) {  // uniform: every thread sees the same centroids
         *bail = 1;
@@ -1122,6 +1133,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
         p = pend;
       }
       __syncthreads();
+      KM_PHASE(9);
       if (g.t < k) {
         const int q = g.t;
         const int rq = S.rank_of[q];
@@ -1275,50 +1287,73 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     }
     KM_PHASE(7);
     // ---- changed: new E-step labels vs the previous iteration's repaired
-    // assignment (thread 0; O(k^2)), convergence
-    if (g.t == 0) {
+    // assignment, convergence (warp 0). Without repairs the labelings are equal
+    // iff every cluster keeps the same sample range (one lane per cluster);
+    // after repairs thread 0 walks the segment breakpoints (O(k^2)).
+    if (g.warp == 0) {
       int changed = empties != 0;  // repairs count as changes
       if (iter > 0 && !changed) {
-        for (int e = 0; e < S.pnexc && !changed; ++e)
-          if (w_label_seg(S.seg, S.so, k, S.pexc_pos[e]) != S.pexc_q[e]) changed = 1;
-        int ro = 0, rn = 0, pos = 0;
-        while (pos < n && !changed) {
-          while (ro < k - 1 && S.pseg[ro + 1] <= pos) ++ro;
-          while (rn < k - 1 && S.seg[rn + 1] <= pos) ++rn;
-          const int end = min(S.pseg[ro + 1], S.seg[rn + 1]);
-          if (S.pso[ro] != S.so[rn]) {
-            if (end - pos > S.pnexc) {
-              changed = 1;
-            } else {
-              for (int p = pos; p < end && !changed; ++p) {
-                bool isexc = false;
-                for (int e = 0; e < S.pnexc; ++e) isexc |= S.pexc_pos[e] == p;
-                if (!isexc) changed = 1;
+        if (S.pnexc == 0) {
+          bool diff = false;
+          if (g.lane < k) {
+            const int rn = S.rank_of[g.lane], ro = S.prank[g.lane];
+            const int an = S.seg[rn], bn = S.seg[rn + 1], ao = S.pseg[ro], bo = S.pseg[ro + 1];
+            diff = !((an == bn && ao == bo) || (an == ao && bn == bo));
+          }
+          changed = __ballot_sync(kFull, diff) != 0;
+        } else {
+          if (g.lane == 0) {
+            for (int e = 0; e < S.pnexc && !changed; ++e)
+              if (w_label_seg(S.seg, S.so, k, S.pexc_pos[e]) != S.pexc_q[e]) changed = 1;
+            int ro = 0, rn = 0, pos = 0;
+            while (pos < n && !changed) {
+              while (ro < k - 1 && S.pseg[ro + 1] <= pos) ++ro;
+              while (rn < k - 1 && S.seg[rn + 1] <= pos) ++rn;
+              const int end = min(S.pseg[ro + 1], S.seg[rn + 1]);
+              if (S.pso[ro] != S.so[rn]) {
+                if (end - pos > S.pnexc) {
+                  changed = 1;
+                } else {
+                  for (int p = pos; p < end && !changed; ++p) {
+                    bool isexc = false;
+                    for (int e = 0; e < S.pnexc; ++e) isexc |= S.pexc_pos[e] == p;
+                    if (!isexc) changed = 1;
+                  }
+                }
               }
+              pos = end;
             }
           }
-          pos = end;
+          changed = __shfl_sync(kFull, changed, 0);
         }
       }
-      const bool stable = !changed && iter > 0;
-      const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
-      S.bci = stable || tol || loss_m == 0.0;
-      for (int t = 0; t <= k; ++t) S.pseg[t] = S.seg[t];
-      for (int t = 0; t < k; ++t) S.pso[t] = S.so[t];
-      S.pnexc = S.nexc;
-      for (int e = 0; e < S.nexc; ++e) {
-        S.pexc_pos[e] = S.exc_pos[e];
-        S.pexc_q[e] = S.exc_q[e];
+      __syncwarp();
+      if (g.lane == 0) {
+        const bool stable = !changed && iter > 0;
+        const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
+        S.bci = stable || tol || loss_m == 0.0;
+        S.pnexc = S.nexc;
+        for (int e = 0; e < S.nexc; ++e) {
+          S.pexc_pos[e] = S.exc_pos[e];
+          S.pexc_q[e] = S.exc_q[e];
+        }
+        if (P.dbg) {
+          atomicAdd((unsigned long long*)&P.dbg[2], 1ull);
+          if (empties) atomicAdd((unsigned long long*)&P.dbg[3], (unsigned long long)__popc(empties));
+        }
       }
-      if (P.dbg) {
-        atomicAdd((unsigned long long*)&P.dbg[2], 1ull);
-        if (empties) atomicAdd((unsigned long long*)&P.dbg[3], (unsigned long long)__popc(empties));
+      // this iteration's assignment becomes the previous one
+      if (g.lane <= k) S.pseg[g.lane] = S.seg[g.lane];
+      if (g.lane < k) {
+        S.pso[g.lane] = S.so[g.lane];
+        S.prank[g.lane] = S.rank_of[g.lane];
       }
     }
     prev = loss_m;
     __syncthreads();
     const int stop = S.bci;
     __syncthreads();
+    KM_PHASE(10);
     if (stop) break;
   }
   if (!need_loss) return 0.0;
@@ -1536,8 +1571,8 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
     DevBuf<long long> dbg;
     W.dbg = nullptr;
     if (km_debug) {
-      dbg.alloc(8, s);
-      ANYQ_CUDA(cudaMemsetAsync(dbg.p, 0, 8 * sizeof(long long), s));
+      dbg.alloc(16, s);
+      ANYQ_CUDA(cudaMemsetAsync(dbg.p, 0, 16 * sizeof(long long), s));
       W.dbg = dbg.p;
     }
     const int smem = (int)cta_smem;
@@ -1553,17 +1588,19 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
     k_kmeans_warp<<<blocks, T, smem, s>>>(W);
     ANYQ_LAUNCHED();
     if (km_debug) {
-      long long h[8];
+      long long h[16];
       ANYQ_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof h, cudaMemcpyDeviceToHost, s));
       int nb = 0;
       ANYQ_CUDA(cudaMemcpyAsync(&nb, bail_n.p, sizeof nb, cudaMemcpyDeviceToHost, s));
       ANYQ_CUDA(cudaStreamSynchronize(s));
       std::fprintf(stderr,
                    "[kmeans group] rows %lld n %lld warps/row %d blocks %d: init %.0f cyc/row, lloyd %.0f "
-                   "cyc/row, iters/row %.2f, repairs %lld, bailed %d; per iter: E %.0f M %.0f rep %.0f loss %.0f\n",
+                   "cyc/row, iters/row %.2f, repairs %lld, bailed %d; per iter: E %.0f M %.0f rep %.0f loss %.0f "
+                   "[sort %.0f, M-runs %.0f, changed+stop %.0f]\n",
                    (long long)rows, (long long)cols, G, blocks, (double)h[0] / rows,
                    (double)h[1] / rows, (double)h[2] / rows, h[3], nb, (double)h[4] / h[2], (double)h[5] / h[2],
-                   (double)h[6] / h[2], (double)h[7] / h[2]);
+                   (double)h[6] / h[2], (double)h[7] / h[2], (double)h[8] / h[2], (double)h[9] / h[2],
+                   (double)h[10] / h[2]);
     }
     // the CTA kernel takes the bailed rows (exits at once when there are none)
     ANYQ_CUDA(cudaMemsetAsync(counter2.p, 0, sizeof(int), s));
