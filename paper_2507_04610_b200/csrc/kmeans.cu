@@ -857,12 +857,12 @@ __device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, W
     if (kMode == 1) return __dmul_rn((double)R.wv[R.idx(g.t, j)], d2[j * R.T + g.t]);
     return d2[j * R.T + g.t];
   };
-  for (int j0 = 0; j0 < cnt && cand == LLONG_MAX; j0 += 16) {
-    double mv[16];
+  for (int j0 = 0; j0 < cnt && cand == LLONG_MAX; j0 += 8) {
+    double mv[8];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) mv[u] = (j0 + u < cnt) ? mass(j0 + u) : 0.0;  // loads first
+    for (int u = 0; u < 8; ++u) mv[u] = (j0 + u < cnt) ? mass(j0 + u) : 0.0;  // loads first
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
+    for (int u = 0; u < 8; ++u) {
       if (cand != LLONG_MAX || !(mv[u] > 0.0)) continue;
       acc = __dadd_rn(acc, mv[u]);
       lastpos = R.lo + j0 + u;
@@ -903,12 +903,12 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
   while (S.ncen < k) {
     const double c = S.cen[S.ncen - 1];
     part = 0.0;
-    for (int j0 = 0; j0 < cnt; j0 += 16) {
-      double dv[16];
+    for (int j0 = 0; j0 < cnt; j0 += 8) {
+      double dv[8];
 #pragma unroll
-      for (int uu = 0; uu < 16; ++uu) dv[uu] = d2[min(j0 + uu, cnt - 1) * R.T + g.t];  // loads first
+      for (int uu = 0; uu < 8; ++uu) dv[uu] = d2[min(j0 + uu, cnt - 1) * R.T + g.t];  // loads first
 #pragma unroll
-      for (int uu = 0; uu < 16; ++uu) {
+      for (int uu = 0; uu < 8; ++uu) {
         if (j0 + uu >= cnt) break;
         const int si = R.idx(g.t, j0 + uu);
         const double pc = dcost((double)R.xs[si], c);
@@ -1104,14 +1104,11 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
             b2[u & 3] = __dadd_rn(b2[u & 3], x);
           }
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {  // remainder (< 8), constant register indices
-          if (j + u < je) {
-            const double w = (double)R.wv[R.idx(g.t, j + u)], x = (double)R.xs[R.idx(g.t, j + u)];
-            b0[u & 3] = __dadd_rn(b0[u & 3], __dmul_rn(w, x));
-            b1[u & 3] = __dadd_rn(b1[u & 3], w);
-            b2[u & 3] = __dadd_rn(b2[u & 3], x);
-          }
+        for (; j < je; ++j) {  // remainder (< 8) into the first partials: small code
+          const double w = (double)R.wv[R.idx(g.t, j)], x = (double)R.xs[R.idx(g.t, j)];
+          b0[0] = __dadd_rn(b0[0], __dmul_rn(w, x));
+          b1[0] = __dadd_rn(b1[0], w);
+          b2[0] = __dadd_rn(b2[0], x);
         }
         const double a0 = __dadd_rn(__dadd_rn(b0[0], b0[1]), __dadd_rn(b0[2], b0[3]));
         const double a1 = __dadd_rn(__dadd_rn(b1[0], b1[1]), __dadd_rn(b1[2], b1[3]));
@@ -1268,17 +1265,12 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
               lb[u & 3] = __dadd_rn(lb[u & 3], __dmul_rn((double)wq[u], dcost((double)xv[u], c)));
           }
         }
-        for (; j < je; j += 4) {  // remainder / exception path, constant register indices
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (j + u < je) {
-              double cc = c;
-              for (int e = 0; e < nexc; ++e)
-                if (S.exc_pos[e] == lo + j + u) cc = S.cen[S.exc_q[e]];
-              lb[u] = __dadd_rn(lb[u], __dmul_rn((double)R.wv[R.idx(g.t, j + u)],
-                                                 dcost((double)R.xs[R.idx(g.t, j + u)], cc)));
-            }
-          }
+        for (; j < je; ++j) {  // remainder / exception path into the first partial
+          double cc = c;
+          for (int e = 0; e < nexc; ++e)
+            if (S.exc_pos[e] == lo + j) cc = S.cen[S.exc_q[e]];
+          lb[0] = __dadd_rn(lb[0], __dmul_rn((double)R.wv[R.idx(g.t, j)],
+                                             dcost((double)R.xs[R.idx(g.t, j)], cc)));
         }
         p = pend;
       }
