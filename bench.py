@@ -279,6 +279,7 @@ def cpu_baseline_sample():
 # q,k,v read the layer input; o reads y_q; gate/up read y_o; down reads y_up
 # (the GEMMs of a Llama decoder layer with the non-GEMM ops between them elided)
 X_SRC = [-1, -1, -1, 0, 3, 3, 5]
+DEPS = X_SRC  # each problem waits only for the problem its x comes from
 WAITS = [0, 0, 0, 1, 1, 0, 1]
 BATCHES = [[0, 1, 2], [3], [4, 5], [6]]
 
@@ -335,7 +336,7 @@ def gpu_arm(args):
         L = layers[li]
         if P == 1 and use_chain:
             anyq.gemm_chain_ptrs([d for (_, _, _, d) in L], [x_of(li, j).data_ptr() for j in range(7)],
-                                 [y.data_ptr() for y in ys[li]], M, s.cuda_stream, WAITS)
+                                 [y.data_ptr() for y in ys[li]], M, s.cuda_stream, deps=DEPS)
             return
         for bt in BATCHES:  # TP: one launch per batch, all-gather of the slices read next
             if use_chain:

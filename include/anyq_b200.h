@@ -222,6 +222,14 @@ anyq_status anyq_dev_gemm_chain(int32_t n, const anyq_dev_tensor* const* t,
                                 const void* const* x_bf16, void* const* y_bf16,
                                 float* const* y_f32, const int32_t* wait_prev, int64_t m,
                                 void* stream);
+/* Same, with one dependency per problem: deps[i] = index of the earlier
+ * problem whose y problem i reads as its x (it starts once every CTA finished
+ * that problem), or -1. Independent problems (e.g. k/v next to o in a decoder
+ * layer) run while others wait. */
+anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
+                                     const void* const* x_bf16, void* const* y_bf16,
+                                     float* const* y_f32, const int32_t* deps, int64_t m,
+                                     void* stream);
 
 /* Device quantize: rows [row_offset, row_offset+rows) of a matrix, fp32 in,
  * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device. */

@@ -132,6 +132,8 @@ def lib() -> C.CDLL:
         "anyq_dev_gemm_bf16_path": (st, [vp, vp, i64, vp, vp, i32, vp]),
         "anyq_dev_gemm_chain": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                      C.POINTER(vp), C.POINTER(i32), i64, vp]),
+        "anyq_dev_gemm_chain_deps": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                          C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -150,7 +152,8 @@ EXPORTED_SYMBOLS = (
     "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
     "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
     "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
-    "anyq_dev_quantize_any", "anyq_launch_count",
+    "anyq_dev_gemm_chain_deps", "anyq_dev_quantize_any", "anyq_launch_count",
+    "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
 )
 
 
@@ -397,11 +400,14 @@ class DeviceTensor:
         return y
 
 
-def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None, y32_ptrs=None):
-    """One launch of y_i = x_i W_i^T for a list of DeviceTensors (anyq_dev_gemm_chain).
+def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None, y32_ptrs=None,
+                    deps=None):
+    """One launch of y_i = x_i W_i^T for a list of DeviceTensors.
 
-    wait_prev[i] = 1 makes problem i read x_i only after all earlier problems
-    completed (x_i may be an earlier y). Pointers are raw device addresses.
+    deps[i] = j (< i) makes problem i read x_i only after problem j completed
+    (x_i is y_j); -1 = no dependency (anyq_dev_gemm_chain_deps). The older
+    wait_prev[i] = 1 waits for every earlier problem (anyq_dev_gemm_chain).
+    Pointers are raw device addresses.
     """
     n = len(tensors)
     VP = C.c_void_p * n
@@ -409,11 +415,15 @@ def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None
     xs = VP(*x_ptrs)
     ys = VP(*y_ptrs)
     y32 = VP(*[p or 0 for p in y32_ptrs]) if y32_ptrs is not None else None
+    if deps is not None:
+        d = (C.c_int32 * n)(*deps)
+        _check(lib().anyq_dev_gemm_chain_deps(n, t, xs, ys, y32, d, m, C.c_void_p(stream)))
+        return
     w = (C.c_int32 * n)(*(wait_prev or [0] * n))
     _check(lib().anyq_dev_gemm_chain(n, t, xs, ys, y32, w, m, C.c_void_p(stream)))
 
 
-def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None):
+def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None, deps=None):
     """gemm_chain_ptrs on torch CUDA tensors; returns the list of y (bf16)."""
     import torch
 
@@ -423,7 +433,7 @@ def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
     gemm_chain_ptrs(tensors, [x.data_ptr() for x in xs], [y.data_ptr() for y in ys], m,
                     s.cuda_stream, wait_prev,
-                    [y.data_ptr() for y in y32s] if y32s is not None else None)
+                    [y.data_ptr() for y in y32s] if y32s is not None else None, deps)
     return ys
 
 

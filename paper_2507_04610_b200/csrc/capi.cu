@@ -568,8 +568,22 @@ anyq_status anyq_dev_gemm_chain(int32_t n, const anyq_dev_tensor* const* t,
                                 void* stream) {
   return guard([&] {
     if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
-    lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32,
-                      wait_prev, m, (cudaStream_t)stream);
+    // "after every earlier problem" == after problem i-1 (problems are released in order)
+    int32_t deps[8];
+    for (int i = 0; i < n; ++i) deps[i] = (wait_prev && i > 0 && wait_prev[i]) ? i - 1 : -1;
+    lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
+                      m, (cudaStream_t)stream);
+  });
+}
+
+anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
+                                     const void* const* x_bf16, void* const* y_bf16,
+                                     float* const* y_f32, const int32_t* deps, int64_t m,
+                                     void* stream) {
+  return guard([&] {
+    if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
+    lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
+                      m, (cudaStream_t)stream);
   });
 }
 

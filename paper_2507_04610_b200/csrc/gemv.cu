@@ -12,11 +12,13 @@
 // (tolerance 1e-5 * sum|x*w|, tests/test_gpu_gemm.py).
 //
 // One persistent CTA per SM: 16 compute warps, 1 writer warp, 1 producer warp.
-//  * Work items are whole 32-row blocks. A launch runs a chain of GEMMs split
-//    into batches (runs of problems without a dependency); the row blocks of a
-//    batch, concatenated in problem order, are dealt round-robin to the CTAs.
-//    An item is computed by one CTA only, so y needs no cross-CTA combine and
-//    the result is deterministic.
+//  * Work items are whole 32-row blocks. A launch runs a chain of up to 8
+//    GEMMs; problem i may depend on one earlier problem dep[i] (its x is that
+//    problem's y). The chain's row blocks, concatenated in problem order, are
+//    dealt round-robin to the CTAs and every CTA walks its items in order, so
+//    independent problems fill the time other CTAs spend waiting on a
+//    dependency. An item is computed by one CTA only, so y needs no cross-CTA
+//    combine and the result is deterministic.
 //  * The producer warp (one lane) streams every item of the CTA: its 32 LUT
 //    rows (1 KB) and its codes in STAGES of 16 consecutive 128-k chunks
 //    (32 rows x 128 k = 2 KB each, contiguous in the prepacked layout
@@ -32,16 +34,16 @@
 //    and ONE LDS dequantises two weights. Two buffers, handed between warps
 //    with mbarriers (warps drift by up to one item instead of meeting at a CTA
 //    barrier).
-//  * x enters once per batch: raw bf16 rows by cp.async.bulk, converted in
+//  * x enters once per image: raw bf16 rows by cp.async.bulk, converted in
 //    place to the permuted fp16 image the code bytes index, plus per-chunk
-//    (2^-e, sum x). Problems of a batch that read the same x share the image;
-//    batches alternate between two image banks.
-//  * The writer warp reduces the 16 warp partials of an item in a fixed order
-//    and stores y; after a batch it releases it grid-wide (done[batch end]).
-//    It also stages x: for a dependent batch it first waits until every CTA
-//    released the batch before (x_i may be an earlier y_j), while the weights
-//    of the batch already stream in. The grid is co-resident (cooperative
-//    launch), so the waits cannot deadlock.
+//    (2^-e, sum x). Consecutive problems that read the same x share the image;
+//    images alternate between two banks.
+//  * The writer warp reduces the 16 warp partials of an item in a fixed order,
+//    stores y, and after its items of a problem releases that problem
+//    grid-wide (done[p], in problem order). It also stages x: for a dependent
+//    problem it first waits until every CTA released the problem x comes from,
+//    while the weights already stream in. The grid is co-resident (cooperative
+//    launch) and dependencies point backwards, so the waits cannot deadlock.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -93,24 +95,24 @@ struct GvProb {
   uint32_t xh, xs;       // dynamic-smem offsets of this problem's x image / chunk scales
   int N, K, C, GR, RB;
   int gshift;            // chunk -> scale group: g = c >> gshift
-  int wait;              // 1: read x only after all earlier problems completed
-  int dup;               // x image shared with an earlier problem of the same batch
+  int dep;               // problem whose output x is (must be complete first), or -1
+  int img;               // x image index (problems in a row with the same x share one)
+  int newimg;            // first problem of its image
   int tma;               // x rows staged by cp.async.bulk into the image region
-  int bstart, bend;      // batch of this problem: problems [bstart, bend]
-  int rboff;             // first item of this problem within its batch
-  int btot;              // items (row blocks) of the whole batch
+  int rboff;             // first item of this problem in the chain's item sequence
 };
 
 struct GvParams {
   GvProb p[kMaxProb];
   int np, M, ncta;
+  int tot;               // items (row blocks) of the whole chain
   int nring;             // code ring stages (2..kMaxRing)
   uint32_t red;          // dynamic-smem offset of the reduction buffer [2][kW][MP][32]
   uint32_t bars;         // dynamic-smem offset of the mbarriers
   uint32_t ring[kMaxRing];  // dynamic-smem offsets of the code ring stages [16 chunks][2048]
   uint32_t abring;       // dynamic-smem offset of the (alpha, beta) ring [nring][16][128]
   uint32_t lutbuf;       // dynamic-smem offset of the LUT rows [2][32][32 B]
-  int* done;             // [kMaxProb] batch release counters (self-resetting)
+  int* done;             // [kMaxProb] per-problem release counters (self-resetting)
   int* err;              // device error word
   long long* trace;      // debug: [ncta][64] globaltimer stamps, or null
 };
@@ -224,36 +226,31 @@ __device__ __forceinline__ long long gtimer() {
   } while (0)
 
 // ---------------------------------------------------------------------------
-// Work items: (problem, row block), dealt round-robin per batch
+// Work items: (problem, row block). The chain's row blocks, concatenated in
+// problem order, are dealt round-robin to the CTAs (item j -> CTA j % ncta);
+// every CTA walks its items in sequence order, so a problem's dependency
+// (always an earlier problem) can never wait on a later item.
 // ---------------------------------------------------------------------------
 struct Item {
-  int p, rb, j;  // p == np: end; j = item index within the batch
+  int p, rb, j;  // p == np: end; j = item index in the chain sequence
 };
 
-// Resolve item index it.j of the batch holding problem it.p; past the batch's
-// end move to the next batch (starting again at this CTA's index b).
-__device__ __forceinline__ void locate(const GvParams& P, int b, Item& it) {
-  while (it.p < P.np) {
-    const GvProb& h = P.p[P.p[it.p].bstart];
-    if (it.j < h.btot) {
-      int p = h.bstart;
-      while (it.j >= P.p[p].rboff + P.p[p].RB) ++p;
-      it.p = p;
-      it.rb = it.j - P.p[p].rboff;
-      return;
-    }
-    it.p = h.bend + 1;
-    it.j = b;
+__device__ __forceinline__ void locate(const GvParams& P, Item& it) {
+  if (it.j >= P.tot) {
+    it.p = P.np;
+    return;
   }
+  while (it.j >= P.p[it.p].rboff + P.p[it.p].RB) ++it.p;
+  it.rb = it.j - P.p[it.p].rboff;
 }
 __device__ __forceinline__ Item item_begin(const GvParams& P, int b) {
   Item it{0, 0, b};
-  locate(P, b, it);
+  locate(P, it);
   return it;
 }
-__device__ __forceinline__ void item_next(const GvParams& P, int b, Item& it) {
+__device__ __forceinline__ void item_next(const GvParams& P, int /*b*/, Item& it) {
   it.j += P.ncta;
-  locate(P, b, it);
+  locate(P, it);
 }
 struct Chunk {
   uint4 w[4];
@@ -385,43 +382,41 @@ __device__ __forceinline__ void prep_x(const GvProb& q, int M, uint8_t* smem, in
   }
 }
 
-// Writer warp: stages x per batch (after the batch it depends on was
-// released by every CTA), then per item reduces the kW warp partials (fixed
-// order) and stores y; after a batch releases it grid-wide.
+// Writer warp, per problem in order: stages the problem's x image when this
+// CTA has items of it and the image is new to this CTA (first waiting until
+// every CTA released the problem x comes from: x may be an earlier y), reduces
+// the kW warp partials of each item in a fixed order and stores y, then
+// releases the problem grid-wide (done[p]; in order, so done[p] == ncta
+// implies every earlier problem is complete too).
 template <int MP>
 __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red, uint32_t bars,
                                             uint32_t sbase, int b, int lane) {
   const uint32_t bar_full = bars + kBarRedFull, bar_empty = bars + kBarRedEmpty;
   const uint32_t bar_x = bars + kBarX;
   Item it = item_begin(P, b);
-  int g = 0;
-  for (int p0 = 0; p0 < P.np;) {
-    const int p1 = P.p[p0].bend;
-    if (it.p <= p1) {  // this CTA has items in the batch: stage its x rows
+  int g = 0, staged = -1;
+  for (int p = 0; p < P.np; ++p) {
+    const GvProb& q = P.p[p];
+    if (it.p == p && q.img != staged) {  // this CTA needs image q.img next
       if (lane == 0) {
-        if (P.p[p0].wait && p0 > 0) {
-          GV_TRACE_W(16 + p0);
-          wait_geq(&P.done[p0 - 1], P.ncta);
-          GV_TRACE_W(24 + p0);
+        if (q.dep >= 0) {
+          GV_TRACE_W(16 + p);
+          wait_geq(&P.done[q.dep], P.ncta);
+          GV_TRACE_W(24 + p);
         }
         // y of other CTAs (generic stores) is read below by the async proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        uint32_t bytes = 0;
-        for (int pp = p0; pp <= p1; ++pp)
-          if (P.p[pp].tma && !P.p[pp].dup) bytes += (uint32_t)P.M * P.p[pp].K * 2;
+        const uint32_t bytes = q.tma ? (uint32_t)P.M * q.K * 2 : 0u;
         mbar_expect_tx(bar_x, bytes);
-        for (int pp = p0; pp <= p1; ++pp) {
-          const GvProb& r = P.p[pp];
-          if (!r.tma || r.dup) continue;
+        if (q.tma)
           for (int m = 0; m < P.M; ++m)
-            bulk_g2s(sbase + r.xh + (uint32_t)m * r.K * 2, r.x + (size_t)m * r.K, (uint32_t)r.K * 2,
+            bulk_g2s(sbase + q.xh + (uint32_t)m * q.K * 2, q.x + (size_t)m * q.K, (uint32_t)q.K * 2,
                      bar_x);
-        }
       }
       __syncwarp();
+      staged = q.img;
     }
-    while (it.p <= p1) {
-      const GvProb& q = P.p[it.p];
+    while (it.p == p) {
       const int par = g & 1;
       mbar_wait_sleep(bar_full + 8 * par, (uint32_t)((g >> 1) & 1));
       const float* rp = red + (size_t)par * kW * MP * 32;
@@ -451,12 +446,11 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
     __syncwarp();
     if (lane == 0) {
       __threadfence();
-      const int old = atomicAdd(&P.done[p1], 1);
-      if (p1 == P.np - 1 && old == P.ncta - 1)  // last CTA of the last batch: reset
+      const int old = atomicAdd(&P.done[p], 1);
+      if (p == P.np - 1 && old == P.ncta - 1)  // last CTA of the last problem: reset
         for (int r = 0; r < P.np; ++r) P.done[r] = 0;
     }
     __syncwarp();
-    p0 = p1 + 1;
   }
 }
 
@@ -577,29 +571,22 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
   if (s.p < P.np) table(0);
   GV_TRACE(1);
 
-  int xbatch = 0;     // x batches staged so far (parity of bar_x)
-  int xready = -1;    // x images are ready for problems <= xready
+  int xbatch = 0;     // x images staged so far (parity of bar_x)
+  int cur_img = -1;   // x image the compute warps hold
   int g = 0;          // items processed by this CTA
   int slot = 0;       // ring stage
   uint32_t round = 0;
   while (s.p < P.np) {
     const int p = s.p;
     const GvProb& q = P.p[p];
-    if (p > xready) {  // first item of a new batch: convert its x rows
-      const int p0 = q.bstart, p1 = q.bend;
+    if (q.img != cur_img) {  // first item on a new x image: convert the staged rows
       mbar_wait(bars + kBarX, (uint32_t)(xbatch & 1));
       ++xbatch;
-      int base = 0;  // conversion tasks of the batch dealt round-robin to the warps
-      for (int pp = p0; pp <= p1; ++pp) {
-        if (P.p[pp].dup) continue;
-        const int nt = MP * ((P.p[pp].C + 3) >> 2);
-        for (int task = (warp - base % kW + kW) % kW; task < nt; task += kW)
-          prep_x<MP>(P.p[pp], P.M, smem, task, lane);
-        base += nt;
-      }
-      xready = p1;
+      const int nt = MP * ((q.C + 3) >> 2);
+      for (int task = warp; task < nt; task += kW) prep_x<MP>(q, P.M, smem, task, lane);
+      cur_img = q.img;
       cw_sync();
-      GV_TRACE(2 + (p0 & 7));
+      GV_TRACE(2 + (q.img & 7));
     }
     const uint32_t tb = kTblAddr | ((uint32_t)(g & 1) << 7) | laneoff;
     mbar_wait(tready + 8 * (g & 1), (uint32_t)((g >> 1) & 1));
@@ -658,7 +645,7 @@ long long* g_gv_trace = nullptr;
 // dynamic shared memory bytes.
 template <int MP>
 uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
-                    float* const* y32s, const int32_t* waits, int64_t m, GvParams& P) {
+                    float* const* y32s, const int32_t* deps, int64_t m, GvParams& P) {
   if (n < 1 || n > kMaxProb) fail(ANYQ_ERR_SHAPE, "LUT GEMV chain: 1..8 problems");
   P.np = n;
   P.M = (int)m;
@@ -666,7 +653,8 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
   P.err = ts[0]->gv_err;
   P.done = ts[0]->gv_done;
   P.trace = g_gv_trace;
-  // batches and x-image sharing
+  // dependencies, x images and the chain's item sequence
+  int tot = 0;
   for (int i = 0; i < n; ++i) {
     const LutTensor* t = ts[i];
     if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");
@@ -686,45 +674,26 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
     q.GR = t->GR;
     q.RB = t->RB;
     q.gshift = t->gv_gshift;
-    q.wait = (waits && i > 0) ? (waits[i] != 0) : 0;
+    q.dep = deps ? deps[i] : -1;
+    if (q.dep < -1 || q.dep >= i) fail(ANYQ_ERR_SHAPE, "chain dependency must name an earlier problem");
     // raw x rows are staged in place of their image: needs K = 128 * C
     q.tma = (q.K % 128 == 0) && ((reinterpret_cast<uintptr_t>(xs[i]) & 15) == 0);
-    q.bstart = (i == 0 || q.wait) ? i : P.p[i - 1].bstart;
-    q.rboff = (q.bstart == i) ? 0 : P.p[i - 1].rboff + P.p[i - 1].RB;
-    q.dup = 0;
-    for (int j = q.bstart; j < i; ++j) {
-      if (P.p[j].x == q.x && P.p[j].K == q.K && !P.p[j].dup) {
-        q.dup = 1 + j;  // (index of the owner) + 1, resolved below
-        break;
-      }
-    }
+    // a problem shares the previous problem's x image when it reads the same x
+    // after the same dependency
+    q.newimg = !(i > 0 && P.p[i - 1].x == q.x && P.p[i - 1].K == q.K && P.p[i - 1].dep == q.dep);
+    q.img = i == 0 ? 0 : P.p[i - 1].img + q.newimg;
+    q.rboff = tot;
+    tot += q.RB;
   }
-  for (int i = n - 1; i >= 0; --i) {
-    GvProb& q = P.p[i];
-    q.bend = (i == n - 1 || P.p[i + 1].wait) ? i : P.p[i + 1].bend;
-  }
-  for (int i = 0; i < n; ++i) {
-    GvProb& q = P.p[i];
-    q.btot = P.p[q.bend].rboff + P.p[q.bend].RB;
-  }
-  // x images: batches alternate between two banks (batch b+2 is staged only
-  // after every CTA released batch b+1, so nobody still reads batch b's bank)
+  P.tot = tot;
+  // x images alternate between two banks: image i+2 is staged only after this
+  // CTA's items on image i are done, so nobody still reads it
   auto img_bytes = [&](const GvProb& q) {
     return (((uint32_t)MP * q.C * 8 + 255u) & ~255u) + (((uint32_t)MP * q.C * 256 + 255u) & ~255u);
   };
   uint32_t bank_need[2] = {0, 0};
-  int bidx[kMaxProb];
-  for (int i = 0, bi = -1; i < n; ++i) {
-    if (P.p[i].bstart == i) ++bi;
-    bidx[i] = bi;
-  }
-  for (int i = 0; i < n; ++i) {
-    if (P.p[i].bstart != i) continue;
-    uint32_t need = 0;
-    for (int j = i; j <= P.p[i].bend; ++j)
-      if (!P.p[j].dup) need += img_bytes(P.p[j]);
-    bank_need[bidx[i] & 1] = std::max(bank_need[bidx[i] & 1], need);
-  }
+  for (int i = 0; i < n; ++i)
+    if (P.p[i].newimg) bank_need[P.p[i].img & 1] = std::max(bank_need[P.p[i].img & 1], img_bytes(P.p[i]));
   // placement: pieces go in front of the 64-KB table while they fit, else behind it
   uint32_t front = kParamOff + (((uint32_t)sizeof(GvParams) + 255u) & ~255u);
   uint32_t back = kPre + kTblBytes;
@@ -745,23 +714,13 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
   uint32_t bank_off[2];
   for (int k = 0; k < 2; ++k) bank_off[k] = bank_need[k] ? place(bank_need[k]) : 0;
   for (int i = 0; i < n; ++i) {
-    if (P.p[i].bstart != i) continue;
-    uint32_t o = bank_off[bidx[i] & 1];
-    for (int j = i; j <= P.p[i].bend; ++j) {
-      GvProb& q = P.p[j];
-      if (q.dup) continue;
-      q.xs = o;
-      q.xh = o + (((uint32_t)MP * q.C * 8 + 255u) & ~255u);
-      o += img_bytes(q);
-    }
-  }
-  for (int i = 0; i < n; ++i) {
     GvProb& q = P.p[i];
-    if (q.dup) {
-      const GvProb& own = P.p[q.dup - 1];
-      q.xs = own.xs;
-      q.xh = own.xh;
-      q.dup = 1;
+    if (q.newimg) {
+      q.xs = bank_off[q.img & 1];
+      q.xh = q.xs + (((uint32_t)MP * q.C * 8 + 255u) & ~255u);
+    } else {
+      q.xs = P.p[i - 1].xs;
+      q.xh = P.p[i - 1].xh;
     }
   }
   // the code ring takes what is left: as many 32-KB stages as fit (2..4),
@@ -790,9 +749,9 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
 
 template <int MP>
 void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
-               float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s) {
+               float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
   GvParams P;
-  const uint32_t smem_bytes = plan_chain<MP>(n, ts, xs, ys, y32s, waits, m, P);
+  const uint32_t smem_bytes = plan_chain<MP>(n, ts, xs, ys, y32s, deps, m, P);
   static uint32_t configured = 0;
   if (smem_bytes > configured) {
     ANYQ_CUDA(cudaFuncSetAttribute(k_lutgemv<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -833,11 +792,11 @@ void lutgemv_setup(LutTensor* t) {
 }
 
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
-                       float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s) {
+                       float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
   if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "LUT GEMV supports 1 <= m <= 2");
   if (n < 1 || !ts) fail(ANYQ_ERR_SHAPE, "empty GEMM chain");
-  if (m == 1) launch_gv<1>(n, ts, xs, ys, y32s, waits, m, s);
-  else launch_gv<2>(n, ts, xs, ys, y32s, waits, m, s);
+  if (m == 1) launch_gv<1>(n, ts, xs, ys, y32s, deps, m, s);
+  else launch_gv<2>(n, ts, xs, ys, y32s, deps, m, s);
 }
 
 bool lutgemv_fits(const LutTensor* t, int64_t m) {

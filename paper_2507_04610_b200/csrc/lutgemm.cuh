@@ -44,8 +44,10 @@ void lutgemv_setup(LutTensor* t);
 void lutgemv_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
 // A chain of n <= 8 GEMMs (same m <= 2) in one launch; problem i > 0 with
 // waits[i] != 0 reads x_i only after all earlier problems completed.
+// deps[i]: index of the earlier problem whose y problem i reads as x, or -1
+// (null = no dependencies)
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
-                       float* const* y32s, const int32_t* waits, int64_t m, cudaStream_t s);
+                       float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
 bool lutgemv_fits(const LutTensor* t, int64_t m);  // GEMV applies (m <= 2, shared memory)
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);

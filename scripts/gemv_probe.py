@@ -134,7 +134,7 @@ def main():
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
                 for l in range(nl):
-                    anyq.gemm_chain(tens[l], xs, ys, wait_prev=waits, stream=stream)
+                    anyq.gemm_chain(tens[l], xs, ys, deps=[-1, -1, -1, 0, 3, 3, 5], stream=stream)
             reps = 20
             with torch.cuda.stream(stream):
                 for _ in range(3):

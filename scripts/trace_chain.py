@@ -30,12 +30,12 @@ def main():
     t_end = time.time() + 0.3
     while time.time() < t_end:
         for _ in range(20):
-            anyq.gemm_chain(tens, xs, ys, wait_prev=waits)
+            anyq.gemm_chain(tens, xs, ys, deps=[-1, -1, -1, 0, 3, 3, 5])
         torch.cuda.synchronize()
     L.anyq_debug_set_gemv_trace(C.c_void_p(tr.data_ptr()))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    anyq.gemm_chain(tens, xs, ys, wait_prev=waits)
+    anyq.gemm_chain(tens, xs, ys, deps=[-1, -1, -1, 0, 3, 3, 5])
     e1.record()
     torch.cuda.synchronize()
     L.anyq_debug_set_gemv_trace(None)

@@ -244,6 +244,40 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         d.close()
 
 
+def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):
+    """anyq_dev_gemm_chain_deps: a decoder-layer pattern (q, k, v, o <- q,
+    gate <- o, up <- o, down <- up) in one launch, each problem waiting only for
+    the problem its x comes from, equals the single launches bit for bit."""
+    import torch
+
+    K0 = 256
+    shapes = [(256, K0), (64, K0), (64, K0), (K0, 256), (640, K0), (640, K0), (K0, 640)]
+    deps = [-1, -1, -1, 0, 3, 3, 5]
+    dts, qts = [], []
+    for i, (n, k) in enumerate(shapes):
+        qt = aq.quantize_any(orc.gaussian(n, k, 110 + i), cfg(codebook=3, max_iters=4, seed=i))
+        qts.append(qt)
+        dts.append(aq.DeviceTensor(qt))
+    for m in (1, 2):
+        x0 = torch.from_numpy(bf16(orc.gaussian(m, K0, 120 + m))).cuda().to(torch.bfloat16)
+        ys = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for n, _ in shapes]
+        y32 = [torch.empty(m, n, device="cuda", dtype=torch.float32) for n, _ in shapes]
+        xs = [x0 if d < 0 else ys[d] for d in deps]
+        for _ in range(3):  # repeated launches reuse the self-resetting counters
+            aq.gemm_chain(dts, xs, ys, y32s=y32, deps=deps)
+        torch.cuda.synchronize()
+        for i, d in enumerate(dts):
+            xi = (x0 if deps[i] < 0 else ys[deps[i]]).clone()
+            r = torch.empty(m, shapes[i][0], device="cuda", dtype=torch.float32)
+            d.gemm(xi, None, r, path=1)
+            torch.cuda.synchronize()
+            assert torch.equal(r, y32[i]), i
+    with pytest.raises(aq.ShapeError):  # a dependency must point backwards
+        aq.gemm_chain(dts[:2], [x0, x0], ys[:2], deps=[-1, 1])
+    for d in dts:
+        d.close()
+
+
 @pytest.mark.parametrize("m", [1, 17, 64, 300])
 @pytest.mark.parametrize("n,k,g", [(200, 384, 128), (4096, 1024, 256), (96, 1280, 1280), (70, 200, 128)])
 def test_dequant_gemm_large_m(aq, orc, cuda, m, n, k, g):
