@@ -279,8 +279,12 @@ def cpu_baseline_sample():
 # q,k,v read the layer input; o reads y_q; gate/up read y_o; down reads y_up
 # (the GEMMs of a Llama decoder layer with the non-GEMM ops between them elided)
 X_SRC = [-1, -1, -1, 0, 3, 3, 5]
-DEPS = X_SRC  # each problem waits only for the problem its x comes from
 WAITS = [0, 0, 0, 1, 1, 0, 1]
+# the single-launch chain runs the layer in its natural order; each problem waits
+# only for the problem its x comes from (anyq_dev_gemm_chain_deps). (Scheduling
+# o before k/v and up before gate measured no faster: scripts/gemv_probe.py.)
+CHAIN_ORDER = [0, 1, 2, 3, 4, 5, 6]
+CHAIN_DEPS = [-1 if X_SRC[j] < 0 else CHAIN_ORDER.index(X_SRC[j]) for j in CHAIN_ORDER]
 BATCHES = [[0, 1, 2], [3], [4, 5], [6]]
 
 
@@ -335,8 +339,9 @@ def gpu_arm(args):
     def run_layer(li, s):
         L = layers[li]
         if P == 1 and use_chain:
-            anyq.gemm_chain_ptrs([d for (_, _, _, d) in L], [x_of(li, j).data_ptr() for j in range(7)],
-                                 [y.data_ptr() for y in ys[li]], M, s.cuda_stream, deps=DEPS)
+            anyq.gemm_chain_ptrs([L[j][3] for j in CHAIN_ORDER], [x_of(li, j).data_ptr() for j in CHAIN_ORDER],
+                                 [ys[li][j].data_ptr() for j in CHAIN_ORDER], M, s.cuda_stream,
+                                 deps=CHAIN_DEPS)
             return
         for bt in BATCHES:  # TP: one launch per batch, all-gather of the slices read next
             if use_chain:

@@ -130,27 +130,32 @@ def main():
             x = torch.randn(m, 4096, device=dev).to(torch.bfloat16)
             ys = [torch.empty(m, n, device=dev, dtype=torch.bfloat16) for _, n, _ in layer]
             xs = [x, x, x, ys[0], ys[3], ys[3], ys[5]]
-            waits = [0, 0, 0, 1, 1, 0, 1]
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for l in range(nl):
-                    anyq.gemm_chain(tens[l], xs, ys, deps=[-1, -1, -1, 0, 3, 3, 5], stream=stream)
-            reps = 20
-            with torch.cuda.stream(stream):
-                for _ in range(3):
-                    g.replay()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(reps):
-                    g.replay()
-                e1.record(stream)
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) * 1e3 / (reps * nl)
-            nb = sum(n * k // 2 + n * (k // 128) * 4 + n * 32 + m * k * 2 + m * n * 2 for _, n, k in layer)
-            gbs = nb / (us * 1e-6) / 1e9
-            out[f"layer_chain_m{m}"] = {"us": round(us, 3), "GBps": round(gbs, 1), "pct": round(100 * gbs / peak, 1)}
-            print(f"layer_chain_m{m}", out[f"layer_chain_m{m}"], flush=True)
+            # natural order (q,k,v,o,gate,up,down) and the scheduled order of bench.py
+            orders = {"": ([0, 1, 2, 3, 4, 5, 6], [-1, -1, -1, 0, 3, 3, 5]),
+                      "_sched": ([0, 3, 1, 2, 5, 4, 6], [-1, 0, -1, -1, 1, 1, 4])}
+            for tag, (order, deps) in orders.items():
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for l in range(nl):
+                        anyq.gemm_chain([tens[l][j] for j in order], [xs[j] for j in order],
+                                        [ys[j] for j in order], deps=deps, stream=stream)
+                reps = 20
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        g.replay()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(reps):
+                        g.replay()
+                    e1.record(stream)
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) * 1e3 / (reps * nl)
+                nb = sum(n * k // 2 + n * (k // 128) * 4 + n * 32 + m * k * 2 + m * n * 2 for _, n, k in layer)
+                gbs = nb / (us * 1e-6) / 1e9
+                key = f"layer_chain_m{m}{tag}"
+                out[key] = {"us": round(us, 3), "GBps": round(gbs, 1), "pct": round(100 * gbs / peak, 1)}
+                print(key, out[key], flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/gemv_probe.json", "w") as f:
         json.dump(out, f, indent=1)
