@@ -130,6 +130,7 @@ def lib() -> C.CDLL:
         "anyq_dev_tensor_cols": (i64, [vp]),
         "anyq_dev_gemm_bf16": (st, [vp, vp, i64, vp, vp, vp]),
         "anyq_dev_gemm_bf16_path": (st, [vp, vp, i64, vp, vp, i32, vp]),
+        "anyq_dev_gemm_auto_path": (i32, [vp, i64]),
         "anyq_dev_gemm_chain": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                      C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_gemm_chain_deps": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
@@ -152,7 +153,8 @@ EXPORTED_SYMBOLS = (
     "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
     "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
     "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
-    "anyq_dev_gemm_chain_deps", "anyq_dev_quantize_any", "anyq_launch_count",
+    "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_auto_path", "anyq_dev_quantize_any",
+    "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
 )
 
@@ -378,6 +380,10 @@ class DeviceTensor:
             self.close()
         except Exception:
             pass
+
+    def auto_path(self, m: int) -> int:
+        """The kernel PATH_AUTO runs at m rows of x (PATH_GEMV / PATH_TC / PATH_DEQUANT)."""
+        return int(lib().anyq_dev_gemm_auto_path(self._h, m))
 
     def gemm_ptr(self, x_ptr: int, m: int, y_ptr: int, y32_ptr: int | None, stream: int,
                  path: int = 0):

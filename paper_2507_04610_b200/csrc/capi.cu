@@ -541,16 +541,23 @@ int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t) {
   return reinterpret_cast<const LutTensor*>(t)->cols;
 }
 
+int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
+  // measured crossovers on B200 (profiles/round1.md): the GEMV while its x
+  // image fits shared memory (m <= 4), the tcgen05 LUT GEMM up to m = 8,
+  // dequant + cuBLAS from m = 16 on
+  const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
+  try {
+    if (lutgemv_fits(lt, m)) return ANYQ_PATH_GEMV;
+  } catch (...) {
+  }
+  return m <= 8 ? ANYQ_PATH_TC : ANYQ_PATH_DEQUANT;
+}
+
 anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                     void* y_bf16, float* y_f32, int32_t path, void* stream) {
   return guard([&] {
     const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
-    if (path == ANYQ_PATH_AUTO)
-      // measured crossovers on B200 (profiles/round1.md): the tcgen05 LUT GEMM
-      // wins for 3 <= m <= 8, dequant + cuBLAS from m = 16 on
-      path = lutgemv_fits(lt, m) ? ANYQ_PATH_GEMV
-             : m <= 8                               ? ANYQ_PATH_TC
-                                                    : ANYQ_PATH_DEQUANT;
+    if (path == ANYQ_PATH_AUTO) path = anyq_dev_gemm_auto_path(t, m);
     if (path == ANYQ_PATH_GEMV)
       lutgemv_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else if (path == ANYQ_PATH_TC)

@@ -60,7 +60,7 @@ constexpr int kW = 16;                // compute warps per CTA (one table slice 
 constexpr int kWriterWarp = kW;
 constexpr int kProducerWarp = kW + 1;
 constexpr int kT = (kW + 2) * 32;
-constexpr int kMaxMP = 2;
+constexpr int kMaxMP = 4;
 constexpr int kStageChunks = kW;      // chunks per ring stage: one per compute warp
 constexpr uint32_t kStageBytes = kStageChunks * 2048u;
 constexpr uint32_t kStageAb = kStageChunks * 128u;
@@ -793,10 +793,11 @@ void lutgemv_setup(LutTensor* t) {
 
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                        float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
-  if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "LUT GEMV supports 1 <= m <= 2");
+  if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "LUT GEMV supports 1 <= m <= 4");
   if (n < 1 || !ts) fail(ANYQ_ERR_SHAPE, "empty GEMM chain");
   if (m == 1) launch_gv<1>(n, ts, xs, ys, y32s, deps, m, s);
-  else launch_gv<2>(n, ts, xs, ys, y32s, deps, m, s);
+  else if (m == 2) launch_gv<2>(n, ts, xs, ys, y32s, deps, m, s);
+  else launch_gv<4>(n, ts, xs, ys, y32s, deps, m, s);
 }
 
 bool lutgemv_fits(const LutTensor* t, int64_t m) {
@@ -807,7 +808,8 @@ bool lutgemv_fits(const LutTensor* t, int64_t m) {
   GvParams P;
   try {
     if (m == 1) plan_chain<1>(1, ts, xs, ys, nullptr, nullptr, m, P);
-    else plan_chain<2>(1, ts, xs, ys, nullptr, nullptr, m, P);
+    else if (m == 2) plan_chain<2>(1, ts, xs, ys, nullptr, nullptr, m, P);
+    else plan_chain<4>(1, ts, xs, ys, nullptr, nullptr, m, P);
   } catch (const Failure&) {
     return false;
   }

@@ -3,7 +3,7 @@
 * anyq_gemm_fused (exact path): bit-identical to the reference gemm_fused /
   gemm_reference for every format, layout and M (test_qgemm.cpp:53-160).
 * device LUT GEMM paths (bf16 x, exact fp16 x fp16 products, fp32
-  accumulation): the CUDA-core GEMV (m <= 2, gemv.cu) and the tcgen05 LUT GEMM
+  accumulation): the CUDA-core GEMV (m <= 4, gemv.cu) and the tcgen05 LUT GEMM
   (m <= 16, lutgemm.cu), each within
   |dy| <= 1e-5 * sum_j |x_j| * (|alpha*T| + |beta|) of
   gemm_reference(bf16(x), narrowed(qt)) computed by the oracle in fp32.
@@ -148,8 +148,8 @@ def tc_tolerance(orc, x, qt):
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 8, 9, 16])
 def test_tc_gemm_matches_reference(aq, orc, cuda, fmt, m, path):
     """any3 / any2 run on the 4-bit device layout (2^bits-entry LUT padded to 16)."""
-    if path == "gemv" and m > 2:
-        pytest.skip("the GEMV serves m <= 2")
+    if path == "gemv" and m > 4:
+        pytest.skip("the GEMV serves m <= 4")
     n, k = 200, 384  # ragged rows (not a multiple of 32), 3 chunks, 3 groups
     w = orc.gaussian(n, k, 31)
     c = cfg(granularity=3, group_size=128, seed=2)
@@ -175,7 +175,7 @@ def test_tc_gemm_shapes(aq, orc, cuda, n, k, g, path):
     gran = 1 if g == k else 3
     c = cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=8)
     qt = aq.quantize_any(w, c)
-    x = bf16(orc.gaussian(2 if path == "gemv" else 3, k, 43))
+    x = bf16(orc.gaussian(3, k, 43))
     y32, _ = tc_gemm(aq, cuda, qt, x, PATHS[path])
     ref = orc.gemm_reference(x, orc.narrowed(qt))
     tol = tc_tolerance(orc, x, qt)
@@ -187,7 +187,7 @@ def test_tc_gemm_is_deterministic_and_rowwise_consistent(aq, orc, cuda, path):
     w = orc.gaussian(512, 1024, 5)
     qt = aq.quantize_any(w, cfg(codebook=3, max_iters=5))
     x1 = bf16(orc.gaussian(1, 1024, 6))
-    mm = 2 if path == "gemv" else 16
+    mm = 4 if path == "gemv" else 16
     xm = np.repeat(x1, mm, axis=0)
     a, _ = tc_gemm(aq, cuda, qt, x1, PATHS[path])
     b, _ = tc_gemm(aq, cuda, qt, x1, PATHS[path])
@@ -220,7 +220,7 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         qt = aq.quantize_any(orc.gaussian(n, k, 70 + i), cfg(codebook=3, max_iters=4, seed=i))
         qts.append(qt)
         dts.append(aq.DeviceTensor(qt))
-    for m in (1, 2):
+    for m in (1, 2, 4):
         x0 = torch.from_numpy(bf16(orc.gaussian(m, 384, 80 + m))).cuda().to(torch.bfloat16)
         x2 = torch.from_numpy(bf16(orc.gaussian(m, 256, 90 + m))).cuda().to(torch.bfloat16)
         # chain: y0 = x0 W0, y1 = x0 W1 (independent), y2 = x2 W2, y3 = y2 W3 (waits on y2)
@@ -258,7 +258,7 @@ def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):
         qt = aq.quantize_any(orc.gaussian(n, k, 110 + i), cfg(codebook=3, max_iters=4, seed=i))
         qts.append(qt)
         dts.append(aq.DeviceTensor(qt))
-    for m in (1, 2):
+    for m in (1, 2, 3):
         x0 = torch.from_numpy(bf16(orc.gaussian(m, K0, 120 + m))).cuda().to(torch.bfloat16)
         ys = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for n, _ in shapes]
         y32 = [torch.empty(m, n, device="cuda", dtype=torch.float32) for n, _ in shapes]
