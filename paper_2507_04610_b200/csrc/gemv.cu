@@ -293,7 +293,11 @@ __device__ __forceinline__ void consume(const Chunk& ch, const uint32_t tb, cons
     uint32_t t[16];
 #pragma unroll
     for (int b = 0; b < 16; ++b)
+#ifdef GV_NOLOOKUP  // experiment build: the table address without the shared-memory read
+      t[b] = __byte_perm(wd[b >> 2], tb, 0x7604u | ((uint32_t)(b & 3) << 4));
+#else
       t[b] = lds32(__byte_perm(wd[b >> 2], tb, 0x7604u | ((uint32_t)(b & 3) << 4)));
+#endif
 #pragma unroll
     for (int m = 0; m < MP; ++m) {
       const uint32_t xq = xa + m * xstride + q * 64;
