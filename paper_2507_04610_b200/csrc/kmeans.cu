@@ -668,6 +668,7 @@ struct WarpKm {
   int redi[kMaxG];
   double bcd;  // broadcasts from thread 0
   int bci;
+  int chg;     // changed flag of the current iteration
 };
 
 struct WkParams {
@@ -996,14 +997,21 @@ __device__ void w_init_random(const WRow& R, const float* sk, WarpKm& S, int k, 
 
 // One Lloyd run (learner.cpp:207-312). Returns the final loss (or 0 when
 // not needed); *bail = 1 when the row must go to the CTA kernel.
+//
+// Iteration i: M-step sums of the E-step segments seg_i -> centroid update ->
+// empty-cluster repair -> changed_i -> loss_i -> stop test. loss_i needs the
+// updated centroids and the repaired labels of iteration i, so it shares one
+// pass over the row with the M-step sums of iteration i+1: the E-step of
+// iteration i+1 (a pure function of the updated centroids) runs first,
+// speculatively; when the stop test then fires, its results are simply not
+// used. Rows with repairs in the iteration take separate passes.
 __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* FP, double* LP,
                           const int* svals_row, const Grp& g, bool need_loss, int* bail) {
   const int n = R.n, C = R.C, k = P.k, lo = R.lo, hi = R.hi;
   const double xmax = fmax(fabs((double)R.x_at(0)), fabs((double)R.x_at(n - 1)));
-  double prev = INFINITY;
-  for (int iter = 0; iter < P.max_iters; ++iter) {
+  // ---- E-step: segment boundaries of the sorted row by the exact predicate
+  auto estep = [&]() -> bool {
     long long tph = clock64();
-    // ---- E-step: segment boundaries of the sorted row by the exact predicate
     w_sort(S, k, g);
     KM_PHASE(8);
     {
@@ -1024,7 +1032,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
       }
       if (near_dup) {  // uniform: every thread sees the same centroids
         *bail = 1;
-        return 0.0;
+        return false;
       }
     }
     if (g.t >= 1 && g.t < k) {
@@ -1078,8 +1086,29 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     }
     __syncthreads();
     KM_PHASE(4);
-    // ---- M-step: per-thread runs over its chunk, combined in chunk order
-    {
+    return true;
+  };
+  // ---- M-step sums over seg/so (per-thread runs, combined later in chunk
+  // order); with fused = true also the loss of the previous labels pseg/pso
+  // under the current centroids (no exceptions), returned as this thread's part
+  auto mpass = [&](bool fused) -> double {
+    long long tph = clock64();
+    double lb[4] = {0.0, 0.0, 0.0, 0.0};
+    int ro = 0, end_o = 0;
+    double c_o = 0.0;
+    if (fused) {
+      while (ro < k - 1 && S.pseg[ro + 1] <= lo) ++ro;
+      end_o = S.pseg[ro + 1];
+      c_o = S.cen[S.pso[ro]];
+    }
+    auto loss_term = [&](int pp, double w, double x, int u) {
+      while (pp >= end_o) {  // next run of the previous labels
+        ++ro;
+        end_o = S.pseg[ro + 1];
+        c_o = S.cen[S.pso[ro]];
+      }
+      lb[u] = __dadd_rn(lb[u], __dmul_rn(w, dcost(x, c_o)));
+    };
       int r = 0, nr = 0;
       for (int p = lo; p < hi;) {
         while (r < k - 1 && S.seg[r + 1] <= p) ++r;
@@ -1102,6 +1131,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
             b0[u & 3] = __dadd_rn(b0[u & 3], __dmul_rn(w, x));
             b1[u & 3] = __dadd_rn(b1[u & 3], w);
             b2[u & 3] = __dadd_rn(b2[u & 3], x);
+            if (fused) loss_term(lo + j + u, w, x, u & 3);
           }
         }
         for (; j < je; ++j) {  // remainder (< 8) into the first partials: small code
@@ -1109,6 +1139,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
           b0[0] = __dadd_rn(b0[0], __dmul_rn(w, x));
           b1[0] = __dadd_rn(b1[0], w);
           b2[0] = __dadd_rn(b2[0], x);
+          if (fused) loss_term(lo + j, w, x, 0);
         }
         const double a0 = __dadd_rn(__dadd_rn(b0[0], b0[1]), __dadd_rn(b0[2], b0[3]));
         const double a1 = __dadd_rn(__dadd_rn(b1[0], b1[1]), __dadd_rn(b1[2], b1[3]));
@@ -1130,7 +1161,53 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
         p = pend;
       }
       __syncthreads();
-      KM_PHASE(9);
+    KM_PHASE(9);
+    return __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
+  };
+  // ---- loss of the labels pseg/pso (+ the exceptions pexc) under the current
+  // centroids (chunk order, then fixed tree)
+  auto losspass = [&]() -> double {
+    double lb[4] = {0.0, 0.0, 0.0, 0.0};
+    const int nexc = S.pnexc;
+    int r = 0;
+    for (int p = lo; p < hi;) {
+      while (r < k - 1 && S.pseg[r + 1] <= p) ++r;
+      const int pend = min(hi, S.pseg[r + 1]);
+      const double c = S.cen[S.pso[r]];
+      int j = p - lo;
+      const int je = pend - lo;
+      if (nexc == 0) {
+        for (; j + 8 <= je; j += 8) {
+          float xv[8], wq[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            xv[u] = R.xs[R.idx(g.t, j + u)];
+            wq[u] = R.wv[R.idx(g.t, j + u)];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            lb[u & 3] = __dadd_rn(lb[u & 3], __dmul_rn((double)wq[u], dcost((double)xv[u], c)));
+        }
+      }
+      for (; j < je; ++j) {  // remainder / exception path into the first partial
+        double cc = c;
+        for (int e = 0; e < nexc; ++e)
+          if (S.pexc_pos[e] == lo + j) cc = S.cen[S.pexc_q[e]];
+        lb[0] = __dadd_rn(lb[0], __dmul_rn((double)R.wv[R.idx(g.t, j)],
+                                           dcost((double)R.xs[R.idx(g.t, j)], cc)));
+      }
+      p = pend;
+    }
+    return __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
+  };
+
+  if (!estep()) return 0.0;
+  mpass(false);
+  double prev = INFINITY;
+  for (int iter = 0; iter < P.max_iters; ++iter) {
+    long long tph = clock64();
+    // ---- M-step: combine the chunk partials, update the centroids
+    {
       if (g.t < k) {
         const int q = g.t;
         const int rq = S.rank_of[q];
@@ -1240,48 +1317,10 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
       __syncthreads();
     }
     KM_PHASE(6);
-    // ---- loss after the update (chunk order, then fixed tree)
-    double loss_m;
-    {
-      double lb[4] = {0.0, 0.0, 0.0, 0.0};
-      const int nexc = S.nexc;
-      int r = 0;
-      for (int p = lo; p < hi;) {
-        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
-        const int pend = min(hi, S.seg[r + 1]);
-        const double c = S.cen[S.so[r]];
-        int j = p - lo;
-        const int je = pend - lo;
-        if (nexc == 0) {
-          for (; j + 8 <= je; j += 8) {
-            float xv[8], wq[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              xv[u] = R.xs[R.idx(g.t, j + u)];
-              wq[u] = R.wv[R.idx(g.t, j + u)];
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              lb[u & 3] = __dadd_rn(lb[u & 3], __dmul_rn((double)wq[u], dcost((double)xv[u], c)));
-          }
-        }
-        for (; j < je; ++j) {  // remainder / exception path into the first partial
-          double cc = c;
-          for (int e = 0; e < nexc; ++e)
-            if (S.exc_pos[e] == lo + j) cc = S.cen[S.exc_q[e]];
-          lb[0] = __dadd_rn(lb[0], __dmul_rn((double)R.wv[R.idx(g.t, j)],
-                                             dcost((double)R.xs[R.idx(g.t, j)], cc)));
-        }
-        p = pend;
-      }
-      const double local = __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
-      loss_m = g_sum(local, S, g);
-    }
-    KM_PHASE(7);
-    // ---- changed: new E-step labels vs the previous iteration's repaired
-    // assignment, convergence (warp 0). Without repairs the labelings are equal
-    // iff every cluster keeps the same sample range (one lane per cluster);
-    // after repairs thread 0 walks the segment breakpoints (O(k^2)).
+    // ---- changed: this iteration's E-step labels vs the previous iteration's
+    // repaired assignment (warp 0). Without repairs the labelings are equal iff
+    // every cluster keeps the same sample range (one lane per cluster); after
+    // repairs thread 0 walks the segment breakpoints (O(k^2)).
     if (g.warp == 0) {
       int changed = empties != 0;  // repairs count as changes
       if (iter > 0 && !changed) {
@@ -1320,10 +1359,10 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
         }
       }
       __syncwarp();
+      // this iteration's (repaired) assignment becomes the previous one: the
+      // labels of this iteration's loss and of the next changed test
       if (g.lane == 0) {
-        const bool stable = !changed && iter > 0;
-        const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
-        S.bci = stable || tol || loss_m == 0.0;
+        S.chg = changed;
         S.pnexc = S.nexc;
         for (int e = 0; e < S.nexc; ++e) {
           S.pexc_pos[e] = S.exc_pos[e];
@@ -1334,18 +1373,35 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
           if (empties) atomicAdd((unsigned long long*)&P.dbg[3], (unsigned long long)__popc(empties));
         }
       }
-      // this iteration's assignment becomes the previous one
       if (g.lane <= k) S.pseg[g.lane] = S.seg[g.lane];
       if (g.lane < k) {
         S.pso[g.lane] = S.so[g.lane];
         S.prank[g.lane] = S.rank_of[g.lane];
       }
     }
+    __syncthreads();
+    KM_PHASE(10);
+    // ---- loss of this iteration, fused with the next iteration's E/M-step
+    const bool last = iter + 1 >= P.max_iters;
+    if (!last && !estep()) return 0.0;
+    double local;
+    if (!last && S.pnexc == 0) {
+      local = mpass(true);
+    } else {
+      local = losspass();
+      if (!last) mpass(false);
+    }
+    const double loss_m = g_sum(local, S, g);
+    KM_PHASE(7);
+    if (g.t == 0) {
+      const bool stable = !S.chg && iter > 0;
+      const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
+      S.bci = stable || tol || loss_m == 0.0;
+    }
     prev = loss_m;
     __syncthreads();
     const int stop = S.bci;
     __syncthreads();
-    KM_PHASE(10);
     if (stop) break;
   }
   if (!need_loss) return 0.0;
