@@ -244,6 +244,34 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         d.close()
 
 
+def test_auto_path_choice_and_agreement(aq, orc, cuda):
+    """AUTO: GEMV while its x image fits shared memory (m <= 4), tcgen05 up to
+    m = 8, dequant + cuBLAS above; a long-K tensor leaves the GEMV at m = 3.
+    AUTO's output equals the explicit path's output bit for bit."""
+    import torch
+
+    qt = aq.quantize_any(orc.gaussian(96, 512, 7), cfg(codebook=3, max_iters=4))
+    dt = aq.DeviceTensor(qt)
+    expect = {1: aq.PATH_GEMV, 2: aq.PATH_GEMV, 3: aq.PATH_GEMV, 4: aq.PATH_GEMV,
+              5: aq.PATH_TC, 8: aq.PATH_TC, 9: aq.PATH_DEQUANT, 64: aq.PATH_DEQUANT}
+    for m, path in expect.items():
+        assert dt.auto_path(m) == path, m
+        x = torch.from_numpy(bf16(orc.gaussian(m, 512, 8 + m))).cuda().to(torch.bfloat16)
+        ya = torch.empty(m, 96, device="cuda", dtype=torch.float32)
+        ye = torch.empty(m, 96, device="cuda", dtype=torch.float32)
+        dt.gemm(x, None, ya)
+        dt.gemm(x, None, ye, path=path)
+        torch.cuda.synchronize()
+        assert torch.equal(ya, ye), m
+    dt.close()
+    # K = 14336 at m = 3: the x image (3 x 14336 bf16 -> fp16) no longer fits next to the table
+    # and the weight ring, so AUTO hands it to the tcgen05 kernel
+    long_k = aq.DeviceTensor(aq.quantize_any(orc.gaussian(64, 14336, 9), cfg(codebook=3, max_iters=2)))
+    assert long_k.auto_path(1) == aq.PATH_GEMV
+    assert long_k.auto_path(3) == aq.PATH_TC
+    long_k.close()
+
+
 def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):
     """anyq_dev_gemm_chain_deps: a decoder-layer pattern (q, k, v, o <- q,
     gate <- o, up <- o, down <- up) in one launch, each problem waiting only for
