@@ -17,7 +17,7 @@ namespace anyq_b200 {
 
 namespace {
 
-constexpr int64_t kSliceRows = 8192;  // row-block slice dequantized per GEMM (bounded workspace)
+constexpr int64_t kSliceRows = 16384;  // row-block slice dequantized per GEMM (bounded workspace)
 
 // One warp per (row block, 128-k chunk) item, lane L = row L. The lane's 16
 // dequantised values alpha_g * T[i] + beta_g (fp32, no contraction:
