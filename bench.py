@@ -508,7 +508,8 @@ def gpu_arm(args):
                                           "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2),
                                           "TFLOPs": round(tf, 1),
                                           "pct_bf16_peak": round(100 * tf / tpeak, 2),
-                                          "path": {1: "gemv", 2: "tcgen05", 3: "dequant+cublas"}[
+                                          "path": {1: "gemv", 2: "tcgen05", 3: "dequant+cublas",
+                                                   4: "fused-mma"}[
                                               layers[0][j][3].auto_path(mm)]}
 
     # ---- config 5 variants: int4 / nf4 (fixed tables) and any3 (3-bit codes on

@@ -543,13 +543,16 @@ int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t) {
 
 int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
   // measured crossovers on B200 (profiles/round1.md): the GEMV while its x
-  // image fits shared memory (m <= 4), the tcgen05 LUT GEMM up to m = 8,
-  // dequant + cuBLAS from m = 16 on
+  // image fits shared memory (m <= 4; else the tcgen05 kernel), the fused
+  // dequant-to-shared-memory mma.sync kernel for 5 <= m <= 32, dequant +
+  // cuBLAS above
   const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
   try {
     if (lutgemv_fits(lt, m)) return ANYQ_PATH_GEMV;
   } catch (...) {
   }
+  if (m <= 4) return ANYQ_PATH_TC;
+  if (m <= 32 && lutmma_supports(lt, m)) return ANYQ_PATH_MMA;
   return m <= 8 ? ANYQ_PATH_TC : ANYQ_PATH_DEQUANT;
 }
 
@@ -564,6 +567,8 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
       lutgemm_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else if (path == ANYQ_PATH_DEQUANT)
       dequant_gemm_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_MMA)
+      lutmma_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else
       fail(ANYQ_ERR_CONFIG, "unknown GEMM path");
   });

@@ -51,6 +51,10 @@ void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs,
 bool lutgemv_fits(const LutTensor* t, int64_t m);  // GEMV applies (m <= 2, shared memory)
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
+// 1 <= M <= 64: fused dequant-to-shared-memory + mma.sync LUT GEMM (lutmma.cu).
+bool lutmma_supports(const LutTensor* t, int64_t m);
+void lutmma_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
+                cudaStream_t s);
 // M > 16: bf16 dequantization in row slices + cuBLAS GEMM (dequant_gemm.cu).
 void dequant_gemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                       cudaStream_t s);

@@ -107,7 +107,7 @@ def bf16(x):
     return bf16_round(x)
 
 
-PATHS = {"gemv": 1, "tc": 2, "dequant": 3}
+PATHS = {"gemv": 1, "tc": 2, "dequant": 3, "mma": 4}
 
 
 def tc_gemm(aq, cuda, qt, x, path=2):
@@ -244,16 +244,41 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         d.close()
 
 
+@pytest.mark.parametrize("m", [1, 3, 8, 16, 33, 64])
+@pytest.mark.parametrize("n,k,g", [(200, 384, 128), (4096, 1024, 256), (96, 1280, 1280), (70, 200, 128),
+                                   (1024, 4096, 128)])
+def test_fused_mma_path(aq, orc, cuda, m, n, k, g):
+    """Fused dequant-to-shared-memory + mma.sync path (lutmma.cu): bf16 weights
+    as the dequant path, within 2^-8 * sum|x*w| of gemm_reference(bf16(x),
+    narrowed(qt)), deterministic (fixed-order split-K combine)."""
+    w = orc.gaussian(n, k, 61)
+    gran = 1 if g == k else 3
+    qt = aq.quantize_any(w, cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=6))
+    x = bf16(orc.gaussian(m, k, 62))
+    y32, ybf = tc_gemm(aq, cuda, qt, x, PATHS["mma"])
+    y32b, _ = tc_gemm(aq, cuda, qt, x, PATHS["mma"])
+    assert bits_equal(y32, y32b)
+    nq = orc.narrowed(qt)
+    ref = orc.gemm_reference(x, nq)
+    tol = 2.0 ** -8 * (np.abs(x) @ np.abs(orc.dequantize(nq)).T) + 1e-30
+    assert np.all(np.abs(y32 - ref) <= tol), float(np.max(np.abs(y32 - ref) / tol))
+    # same bf16 weights and fp32 accumulation as the dequant + cuBLAS path
+    yd, _ = tc_gemm(aq, cuda, qt, x, PATHS["dequant"])
+    assert np.all(np.abs(y32 - yd) <= tol)
+
+
 def test_auto_path_choice_and_agreement(aq, orc, cuda):
-    """AUTO: GEMV while its x image fits shared memory (m <= 4), tcgen05 up to
-    m = 8, dequant + cuBLAS above; a long-K tensor leaves the GEMV at m = 3.
-    AUTO's output equals the explicit path's output bit for bit."""
+    """AUTO: GEMV while its x image fits shared memory (m <= 4), the fused mma
+    kernel for 5 <= m <= 32, dequant + cuBLAS above; a long-K tensor leaves
+    the GEMV at m = 3 for tcgen05. AUTO's output equals the explicit path's
+    output bit for bit."""
     import torch
 
     qt = aq.quantize_any(orc.gaussian(96, 512, 7), cfg(codebook=3, max_iters=4))
     dt = aq.DeviceTensor(qt)
     expect = {1: aq.PATH_GEMV, 2: aq.PATH_GEMV, 3: aq.PATH_GEMV, 4: aq.PATH_GEMV,
-              5: aq.PATH_TC, 8: aq.PATH_TC, 9: aq.PATH_DEQUANT, 64: aq.PATH_DEQUANT}
+              5: aq.PATH_MMA, 8: aq.PATH_MMA, 32: aq.PATH_MMA, 33: aq.PATH_DEQUANT,
+              64: aq.PATH_DEQUANT}
     for m, path in expect.items():
         assert dt.auto_path(m) == path, m
         x = torch.from_numpy(bf16(orc.gaussian(m, 512, 8 + m))).cuda().to(torch.bfloat16)
@@ -320,6 +345,6 @@ def test_dequant_gemm_large_m(aq, orc, cuda, m, n, k, g):
     ref = orc.gemm_reference(x, nq)
     tol = 2.0 ** -8 * (np.abs(x) @ np.abs(orc.dequantize(nq)).T) + 1e-30
     assert np.all(np.abs(y32 - ref) <= tol)
-    if m > 8:  # AUTO picks this path above m = 8
+    if m > 32:  # AUTO picks this path above m = 32
         y32a, _ = tc_gemm(aq, cuda, qt, x, 0)
         assert bits_equal(y32a, y32)
