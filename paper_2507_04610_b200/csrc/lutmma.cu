@@ -113,20 +113,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_lutmma(const MmaArgs A) {
   // codes of the next chunk are loaded one iteration ahead (global latency)
   uint4 wn[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0),
                  make_uint4(0, 0, 0, 0)};
+  __half2 abn = __floats2half2_rn(0.0f, 0.0f);
+  auto ab_of = [&](int c) {
+    const int g = A.gshift >= 30 ? 0 : (c >> A.gshift);
+    return A.ab[((int64_t)rb * A.GR + g) * 32 + lane];
+  };
   if (live && c0 < c1) {
     const uint4* cp = A.codes + ((int64_t)rb * A.C + c0) * 128 + lane;
 #pragma unroll
     for (int q = 0; q < 4; ++q) wn[q] = cp[q * 32];
+    abn = ab_of(c0);
   }
-  for (int c = c0; c < c1; ++c) {
-    // ---- x chunk -> xs[n][physical k] (rows >= M and k >= K are zero)
-    __syncthreads();  // previous chunk's B reads are done
-    for (int task = threadIdx.x; task < NT * 8 * 8; task += kMmaWarps * 32) {
-      const int n = task >> 3, run = task & 7;  // run = (q, h): 16 bf16
+  // x chunk staging: this thread's 16-bf16 runs, loaded one chunk ahead
+  constexpr int kXTasks = (NT * 8 * 8 + kMmaWarps * 32 - 1) / (kMmaWarps * 32);
+  uint4 xv[kXTasks][2];
+  auto load_x = [&](int c) {
+#pragma unroll
+    for (int u = 0; u < kXTasks; ++u) {
+      const int task = threadIdx.x + u * kMmaWarps * 32;
+      uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+      const int n = task >> 3, run = task & 7;
       const int q = run >> 1, h = run & 1;
       const int64_t k0 = (int64_t)c * 128 + 16 * q + 64 * h;
-      uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
-      if (n < A.M) {
+      if (task < NT * 64 && n < A.M) {
         const __nv_bfloat16* src = A.x + (int64_t)n * A.K + k0;
         if (((A.K & 7) == 0) && k0 + 16 <= A.K) {
           v0 = *reinterpret_cast<const uint4*>(src);
@@ -140,14 +149,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_lutmma(const MmaArgs A) {
                           s[14] | (s[15] << 16));
         }
       }
-      uint4* dst = reinterpret_cast<uint4*>(xs + n * kTileStride + 32 * q + 16 * h);
-      dst[0] = v0;
-      dst[1] = v1;
+      xv[u][0] = v0;
+      xv[u][1] = v1;
     }
+  };
+  if (c0 < c1) load_x(c0);
+  for (int c = c0; c < c1; ++c) {
+    // ---- x chunk -> xs[n][physical k] (rows >= M and k >= K are zero)
+    __syncthreads();  // previous chunk's B reads are done
+#pragma unroll
+    for (int u = 0; u < kXTasks; ++u) {
+      const int task = threadIdx.x + u * kMmaWarps * 32;
+      if (task < NT * 64) {
+        const int n = task >> 3, run = task & 7;
+        const int q = run >> 1, h = run & 1;
+        uint4* dst = reinterpret_cast<uint4*>(xs + n * kTileStride + 32 * q + 16 * h);
+        dst[0] = xv[u][0];
+        dst[1] = xv[u][1];
+      }
+    }
+    if (c + 1 < c1) load_x(c + 1);
     // ---- this warp's 32 x 128 weight tile
     if (live) {
-      const int g = A.gshift >= 30 ? 0 : (c >> A.gshift);
-      const float2 s = __half22float2(A.ab[((int64_t)rb * A.GR + g) * 32 + lane]);
+      const float2 s = __half22float2(abn);
       uint4 w4[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) w4[q] = wn[q];
@@ -155,6 +179,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_lutmma(const MmaArgs A) {
         const uint4* cp = A.codes + ((int64_t)rb * A.C + c + 1) * 128 + lane;
 #pragma unroll
         for (int q = 0; q < 4; ++q) wn[q] = cp[q * 32];
+        abn = ab_of(c + 1);
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i)

@@ -13,5 +13,5 @@ dt = anyq.DeviceTensor(bench.synthetic_qtensor(14336, 4096, 5))
 x = torch.randn(m, 4096, device="cuda").to(torch.bfloat16)
 y = torch.empty(m, 14336, device="cuda", dtype=torch.bfloat16)
 for _ in range(3):
-    dt.gemm(x, y, None, path=2)
+    dt.gemm(x, y, None, path=int(sys.argv[2]) if len(sys.argv) > 2 else 2)
 torch.cuda.synchronize()
