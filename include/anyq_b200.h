@@ -216,7 +216,7 @@ int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m);
 
 /* A chain of small-M GEMMs in ONE persistent launch (e.g. the projections of a
  * decoder layer): y_i[m x rows_i] = x_i[m x cols_i] * dequant(W_i)^T for
- * i < n (n <= 8, the same 1 <= m <= 2 for all; CUDA-core GEMV path). Problem
+ * i < n (n <= 8, the same 1 <= m <= 4 for all; CUDA-core GEMV path). Problem
  * i > 0 with wait_prev[i] != 0 reads x_i only after every earlier problem has
  * completed grid-wide, so x_i may be (or depend on) an earlier y_j; the
  * weights of later problems stream in while it waits. y32 may be NULL (or any

@@ -1,4 +1,4 @@
-// K1a — CUDA-core any4 LUT GEMV for M <= 2 (the memory-bound decode path), sm_100a.
+// K1a — CUDA-core any4 LUT GEMV for M <= 4 (the memory-bound decode path), sm_100a.
 //
 //   y[m][n] = sum_k x[m][k] * (alpha[n][g(k)] * T_n[c[n][k]] + beta[n][g(k)])
 //

@@ -886,8 +886,6 @@ void lutgemm_destroy(LutTensor* t) {
   cudaFree(t->counters);
   cudaFree(t->gv_err);
   cudaFree(t->gv_done);
-  cudaFree(t->dq_w);
-  cudaFree(t->dq_acc);
   delete t;
 }
 

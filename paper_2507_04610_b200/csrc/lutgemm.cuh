@@ -30,32 +30,26 @@ struct LutTensor {
   int* gv_err = nullptr;      // device error word of the GEMV
   int* gv_done = nullptr;     // [8] chain completion counters (self-resetting)
   int gv_ncta = 0, gv_gshift = -1;
-  // large-M dequant + cuBLAS path (dequant_gemm.cu): lazily sized workspace
-  void* dq_w = nullptr;      // [<= 4096 rows][K] bf16
-  float* dq_acc = nullptr;   // [m][<= 4096] fp32
-  int64_t dq_acc_n = 0;
 };
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt);
 void lutgemm_destroy(LutTensor* t);
 void lutgemm_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
-// K1a CUDA-core GEMV (m <= 2) over the same prepacked tensor (gemv.cu).
+// K1a CUDA-core GEMV (m <= 4) over the same prepacked tensor (gemv.cu).
 void lutgemv_setup(LutTensor* t);
 void lutgemv_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
-// A chain of n <= 8 GEMMs (same m <= 2) in one launch; problem i > 0 with
-// waits[i] != 0 reads x_i only after all earlier problems completed.
-// deps[i]: index of the earlier problem whose y problem i reads as x, or -1
-// (null = no dependencies)
+// A chain of n <= 8 GEMMs (same m <= 4) in one launch. deps[i]: index of the
+// earlier problem whose y problem i reads as x, or -1 (null = no dependencies).
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                        float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
-bool lutgemv_fits(const LutTensor* t, int64_t m);  // GEMV applies (m <= 2, shared memory)
+bool lutgemv_fits(const LutTensor* t, int64_t m);  // GEMV applies (m <= 4, shared memory)
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
 // 1 <= M <= 64: fused dequant-to-shared-memory + mma.sync LUT GEMM (lutmma.cu).
 bool lutmma_supports(const LutTensor* t, int64_t m);
 void lutmma_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                 cudaStream_t s);
-// M > 16: bf16 dequantization in row slices + cuBLAS GEMM (dequant_gemm.cu).
+// Large M: bf16 dequantization in row slices + cuBLAS GEMM (dequant_gemm.cu).
 void dequant_gemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                       cudaStream_t s);
 void lutgemm_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
