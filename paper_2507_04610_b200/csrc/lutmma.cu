@@ -306,7 +306,8 @@ void lutmma_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y3
     A.part = nullptr;
   }
   const int blocks = groups * S;
-  if (m <= 16) launch_mma<2>(A, blocks, s);
+  if (m <= 8) launch_mma<1>(A, blocks, s);
+  else if (m <= 16) launch_mma<2>(A, blocks, s);
   else if (m <= 32) launch_mma<4>(A, blocks, s);
   else launch_mma<8>(A, blocks, s);
   if (S > 1) {
