@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32) k_lutmma(const MmaArgs A) {
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
           const uint32_t byte = (wd[b >> 2] >> (8 * (b & 3))) & 0xffu;
-          o[b] = tbl[byte & 15][lane] | (tbl[byte >> 4][lane] << 16);
+          o[b] = __byte_perm(tbl[byte & 15][lane], tbl[byte >> 4][lane], 0x5410);
         }
         uint4* trow = reinterpret_cast<uint4*>(wt + lane * kTileStride + 32 * q);
         trow[0] = make_uint4(o[0], o[1], o[2], o[3]);
