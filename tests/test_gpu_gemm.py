@@ -244,6 +244,20 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         d.close()
 
 
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+@pytest.mark.parametrize("n,k", [(70, 200), (33, 130), (300, 1000)])
+def test_gemv_ragged_k(aq, orc, cuda, m, n, k):
+    """K not a multiple of 128: the GEMV loads x directly (no bulk copy) and the
+    zero-padded tail chunk contributes nothing; within the exact-product
+    tolerance of gemm_reference(bf16(x), narrowed(qt))."""
+    w = orc.gaussian(n, k, 71)
+    qt = aq.quantize_any(w, cfg(codebook=3, granularity=1, seed=3, max_iters=5))
+    x = bf16(orc.gaussian(m, k, 72))
+    y32, _ = tc_gemm(aq, cuda, qt, x, PATHS["gemv"])
+    ref = orc.gemm_reference(x, orc.narrowed(qt))
+    assert np.all(np.abs(y32 - ref) <= tc_tolerance(orc, x, qt))
+
+
 @pytest.mark.parametrize("m", [1, 3, 8, 16, 33, 64])
 @pytest.mark.parametrize("n,k,g", [(200, 384, 128), (4096, 1024, 256), (96, 1280, 1280), (70, 200, 128),
                                    (1024, 4096, 128)])
