@@ -1063,9 +1063,19 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
           }
           p = c0 * C + ja;
         }
+        // with no near-duplicate centroids only the bracketing pair can win,
+        // so "nearest rank >= t" is the reference predicate on that pair alone
+        // (fl((x - c)^2), ties to the smaller original index)
+        const double clo = S.sv[t - 1], chi = S.sv[t];
+        const bool hi_wins_ties = S.so[t] < S.so[t - 1];
+        auto at_least_t = [&](int pp) {
+          const double x = (double)R.x_at(pp);
+          const double dl = dcost(x, clo), dh = dcost(x, chi);
+          return dh < dl || (dh == dl && hi_wins_ties);
+        };
         int steps = 0;
-        while (p > 0 && steps < 8 && rank_at(p - 1) >= t) --p, ++steps;
-        while (p < n && steps < 8 && rank_at(p) < t) ++p, ++steps;
+        while (p > 0 && steps < 8 && at_least_t(p - 1)) --p, ++steps;
+        while (p < n && steps < 8 && !at_least_t(p)) ++p, ++steps;
         if (steps < 8) {
           a = p;
           done = true;
