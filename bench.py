@@ -486,6 +486,30 @@ def gpu_arm(args):
                                "GBps": round(nb / (us * 1e-6) / 1e9, 1),
                                "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
 
+    # ---- config 3 shapes (Llama-3-70B) at M=1 on one GPU: the per-GPU slice of
+    # the TP config at P=1 (weights rotated over 2 copies > L2)
+    per_shape_70b = {}
+    if not args.quick and P == 1:
+        LAYER70 = [("q", 8192, 8192), ("k", 1024, 8192), ("v", 1024, 8192), ("o", 8192, 8192),
+                   ("gate", 28672, 8192), ("up", 28672, 8192), ("down", 8192, 28672)]
+        x70 = {k: torch.randn(M, k, device=dev).to(torch.bfloat16) for k in (8192, 28672)}
+        for j, (name, n, k) in enumerate(LAYER70):
+            if name in ("k", "up"):  # same shapes as v / gate
+                continue
+            ts70 = [anyq.DeviceTensor(synthetic_qtensor(n, k, 500 + 10 * j + c)) for c in range(2)]
+            y70 = torch.empty(M, n, device=dev, dtype=torch.bfloat16)
+
+            def one70():
+                for d in ts70:
+                    d.gemm_ptr(x70[k].data_ptr(), M, y70.data_ptr(), None, stream.cuda_stream)
+            us = time_graph(one70, 20) / len(ts70)
+            nb = algo_bytes(n, k, M)
+            per_shape_70b[name] = {"N": n, "K": k, "us": round(us, 3),
+                                   "GBps": round(nb / (us * 1e-6) / 1e9, 1),
+                                   "pct_hbm_peak": round(100 * nb / (us * 1e-6) / 1e9 / peak, 2)}
+            for d in ts70:
+                d.close()
+
     # ---- M sweep (per-GEMM launches, AUTO path: GEMV for m = 1, tcgen05 above)
     sweep = {}
     tpeak = hbm_peak_tflops()
@@ -666,6 +690,7 @@ def gpu_arm(args):
             "launches_counted_host": anyq.launch_count() - launches0,
             "clocks": clk.summary(),
             "per_shape": per_shape,
+            "per_shape_70b_m1": per_shape_70b,
             "m_sweep": sweep,
             "kmeans": kmeans,
             "variants_q_shape": variants,

@@ -35,6 +35,11 @@ def main():
           "|---|---|---|---|---|---|"]
     for k, v in b["per_shape"].items():
         L.append(f"| {k} | {v['N']} | {v['K']} | {v['us']} | {v['GBps']} | {v['pct_hbm_peak']} |")
+    if b.get("per_shape_70b_m1"):
+        L += ["", "## Llama-3-70B shapes (config 3 slice at P=1), M=1", "", "| shape | N | K | µs | GB/s | % HBM |",
+              "|---|---|---|---|---|---|"]
+        for k, v in b["per_shape_70b_m1"].items():
+            L.append(f"| {k} | {v['N']} | {v['K']} | {v['us']} | {v['GBps']} | {v['pct_hbm_peak']} |")
     L += ["", "## M sweep (AUTO path)", "", "| shape, M | µs | % HBM | TFLOP/s | path |",
           "|---|---|---|---|---|"]
     for k, v in b.get("m_sweep", {}).items():
