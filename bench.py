@@ -39,8 +39,11 @@ sys.path.insert(0, ROOT)
 LAYER = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
          ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
 GROUP = 128
+MODEL = "8b"
 METRIC = "any4 GEMM µs and % HBM peak at M=1–16 (Llama-3 shapes); k-means rows/s"
 UNIT = "GB/s"
+LAYER_70B = [("q", 8192, 8192), ("k", 1024, 8192), ("v", 1024, 8192), ("o", 8192, 8192),
+             ("gate", 28672, 8192), ("up", 28672, 8192), ("down", 8192, 28672)]
 
 
 def algo_bytes(n, k, m, bits=4, group=GROUP):
@@ -245,10 +248,10 @@ def reference_arm(args):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": "llama3-8b-layer-gemms", "M": m, "group_size": GROUP,
+        "config": {"workload": f"llama3-{MODEL}-layer-gemms", "M": m, "group_size": GROUP,
                    "shapes": [[n, k] for (_, n, k) in LAYER]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": "one Llama-3-8B layer (7 GEMMs) at M=1, reference gemm_fused "
+                         "sample": f"one Llama-3-{MODEL} layer (7 GEMMs) at M=1, reference gemm_fused "
                                    f"(qgemm.cpp:71) over {threads} row slices (harness-parallel)",
                          "library": os.path.relpath(REF_SO, ROOT) if kind == "reference" else
                          "oracle/_build/liboracle.so"},
@@ -308,7 +311,8 @@ def gpu_arm(args):
     stream = torch.cuda.Stream(dev)
 
     # buffers: layer input x, per-layer local y shards, gathered y (TP)
-    x_in = torch.randn(M, 4096, device=dev).to(torch.bfloat16)
+    D = LAYER[0][2]  # model dim (K of q/k/v/gate/up)
+    x_in = torch.randn(M, D, device=dev).to(torch.bfloat16)
     # the seven outputs of a layer are views into one flat buffer (one D2H copy per step)
     ybufs = [torch.empty(M * sum(ns for (_, ns, _, _) in L), device=dev, dtype=torch.bfloat16)
              for L in layers]
@@ -427,7 +431,7 @@ def gpu_arm(args):
 
     # ---- e2e through the public API with host buffers: H2D of the layer input
     # (pinned) + D2H of all seven outputs, every step, inside the timed region
-    xh = torch.randn(M, 4096).to(torch.bfloat16).pin_memory()
+    xh = torch.randn(M, D).to(torch.bfloat16).pin_memory()
     yh = [[torch.empty(M, ns * P, dtype=torch.bfloat16).pin_memory() for (_, ns, _, _) in L]
           for L in layers]
     yhflat = [torch.empty(ybufs[li].numel(), dtype=torch.bfloat16).pin_memory() for li in range(len(layers))]
@@ -463,7 +467,7 @@ def gpu_arm(args):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    h2d = M * 4096 * 2
+    h2d = M * D * 2
     d2h = sum(M * n * 2 for (_, n, _) in LAYER)
 
     # ---- per-shape single-GEMM timing (graph of the rotated layers' copies)
@@ -486,7 +490,8 @@ def gpu_arm(args):
         return a.elapsed_time(b) / reps * 1e3  # us per replay
 
     per_shape = {}
-    xk = {4096: x_in, 14336: torch.randn(M, 14336, device=dev).to(torch.bfloat16)}
+    FF = LAYER[6][2]  # FFN dim (K of down)
+    xk = {D: x_in, FF: torch.randn(M, FF, device=dev).to(torch.bfloat16)}
     if P == 1:
         for j, (name, n, k) in enumerate(LAYER):
             def one():
@@ -528,7 +533,7 @@ def gpu_arm(args):
     tpeak = hbm_peak_tflops()
     if not args.quick and P == 1:
         for mm in (1, 2, 4, 8, 16, 64, 256, 1024, 4096):
-            xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in (4096, 14336)}
+            xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in (D, FF)}
             for j, (name, n, k) in enumerate(LAYER):
                 if name not in ("q", "gate", "down"):
                     continue
@@ -676,7 +681,7 @@ def gpu_arm(args):
             "dtype": "f16",
             "data": "synthetic",
             "config": {
-                "workload": "llama3-8b decoder-layer GEMMs (q,k,v,o,gate,up,down) any4 g128, "
+                "workload": f"llama3-{MODEL} decoder-layer GEMMs (q,k,v,o,gate,up,down) any4 g128, "
                             "decoder data dependencies (o<-q, gate/up<-o, down<-up)",
                 "M": M,
                 "group_size": GROUP,
@@ -727,7 +732,14 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--quick", action="store_true", help="skip the M sweep and k-means extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--model", default="8b", choices=["8b", "70b"],
+                    help="layer shapes of the step: Llama-3-8B (default, config 2) or -70B "
+                         "(config 3; with --gpus N the layer is row-sharded over N GPUs)")
     args = ap.parse_args()
+    if args.model == "70b":
+        global LAYER, MODEL
+        LAYER = LAYER_70B
+        MODEL = "70b"
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
