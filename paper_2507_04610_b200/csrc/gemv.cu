@@ -321,15 +321,13 @@ __device__ __forceinline__ void consume(const Chunk& ch, const uint32_t tb, cons
   }
 }
 
-// x of problem q -> permuted fp16 image + per-chunk (2^-e, sum x). A warp task
-// covers (m, 4 consecutive chunks): lanes 8u..8u+7 own chunk c0+u, 16
-// consecutive k each (k = 128c + 16*sub + t), so the max/sum trees are 3
-// shuffles deep. Image position of k = 128c + 64h + 16s + 2j (+1): slab s,
+// x of problem q -> permuted fp16 image + per-chunk (2^-e, sum x) for chunk c
+// of x row m: the 8 lanes of a lane group own 16 consecutive k each
+// (k = 128c + 16*sub + t), so the max/sum trees are 3 shuffles deep. Image position of k = 128c + 64h + 16s + 2j (+1): slab s,
 // pair 8h + j -> a lane's 16 values are pairs 8*(sub/4) .. +7 of slab sub%4.
 template <int MP>
-__device__ __forceinline__ void prep_x(const GvProb& q, int M, uint8_t* smem, int task, int lane) {
-  const int cq = (q.C + 3) >> 2;
-  const int m = task / cq, c = (task % cq) * 4 + (lane >> 3), sub = lane & 7;
+__device__ __forceinline__ void prep_x(const GvProb& q, int M, uint8_t* smem, int m, int c, int lane) {
+  const int sub = lane & 7;
   const int k0 = c * 128 + sub * 16;
   float v[16];
 #pragma unroll
@@ -586,10 +584,13 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
     if (q.img != cur_img) {  // first item on a new x image: convert the staged rows
       mbar_wait(bars + kBarX, (uint32_t)(xbatch & 1));
       ++xbatch;
-      const int nt = MP * ((q.C + 3) >> 2);
-      for (int task = warp; task < nt; task += kW) prep_x<MP>(q, P.M, smem, task, lane);
+      // each warp converts exactly the chunks it reads (c = warp + 16 i, lane
+      // group i % 4 per pass): the image needs no CTA barrier
+      const int nmine = (q.C - warp + kW - 1) / kW;  // chunks of this warp
+      for (int m = 0; m < MP; ++m)
+        for (int i0 = 0; i0 < nmine; i0 += 4)
+          prep_x<MP>(q, P.M, smem, m, warp + kW * (i0 + (lane >> 3)), lane);
       cur_img = q.img;
-      cw_sync();
       GV_TRACE(2 + (q.img & 7));
     }
     const uint32_t tb = kTblAddr | ((uint32_t)(g & 1) << 7) | laneoff;
