@@ -36,8 +36,9 @@
 //    barrier).
 //  * x enters once per image: raw bf16 rows by cp.async.bulk, converted in
 //    place to the permuted fp16 image the code bytes index, plus per-chunk
-//    (2^-e, sum x). Consecutive problems that read the same x share the image;
-//    images alternate between two banks.
+//    (2^-e, sum x); each compute warp converts exactly the chunks it reads, so
+//    no CTA barrier follows. Consecutive problems that read the same x share
+//    the image; images alternate between two banks.
 //  * The writer warp reduces the 16 warp partials of an item in a fixed order,
 //    stores y, and after its items of a problem releases that problem
 //    grid-wide (done[p], in problem order). It also stages x: for a dependent
