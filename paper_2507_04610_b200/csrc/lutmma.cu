@@ -33,7 +33,12 @@ namespace anyq_b200 {
 
 namespace {
 
-constexpr int kMmaWarps = 4;
+// warps (row blocks) per CTA: 4, or 8 for the widest x tiles (M > 16), where
+// the register-heavy accumulators leave few CTAs per SM
+template <int NT>
+constexpr int mma_warps() {
+  return NT >= 4 ? 8 : 4;
+}
 constexpr int kTileStride = 136;  // bf16 per shared row (128 + 8 pad: conflict-free ldmatrix)
 
 struct MmaArgs {
@@ -70,11 +75,13 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1
 
 template <int NT>
 constexpr uint32_t mma_smem_bytes() {  // xs + weight tiles + tables
+  constexpr int kMmaWarps = mma_warps<NT>();
   return (uint32_t)(NT * 8 * kTileStride * 2 + kMmaWarps * 32 * kTileStride * 2 + kMmaWarps * 16 * 32 * 4);
 }
 
 template <int NT>  // n8 tiles of x rows: M <= 8 * NT
-__global__ void __launch_bounds__(kMmaWarps * 32) k_lutmma(const MmaArgs A) {
+__global__ void __launch_bounds__(mma_warps<NT>() * 32) k_lutmma(const MmaArgs A) {
+  constexpr int kMmaWarps = mma_warps<NT>();
   extern __shared__ __align__(16) uint8_t smem[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem);
   __nv_bfloat16* wt_base_ptr = xs + NT * 8 * kTileStride;
@@ -265,7 +272,7 @@ void launch_mma(const MmaArgs& A, int blocks, cudaStream_t s) {
     ANYQ_CUDA(cudaFuncSetAttribute(k_lutmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  k_lutmma<NT><<<blocks, kMmaWarps * 32, smem, s>>>(A);
+  k_lutmma<NT><<<blocks, mma_warps<NT>() * 32, smem, s>>>(A);
   ANYQ_LAUNCHED();
 }
 
@@ -292,8 +299,10 @@ void lutmma_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y3
   A.C = t->C;
   A.GR = t->GR;
   A.gshift = t->gv_gshift;
+  const int nt = m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 8;
+  const int warps_per_cta = nt >= 4 ? 8 : 4;  // mma_warps<NT>()
   // split K until the grid covers ~2 CTAs per SM (at least 2 chunks per split)
-  const int groups = (t->RB + kMmaWarps - 1) / kMmaWarps;
+  const int groups = (t->RB + warps_per_cta - 1) / warps_per_cta;
   int S = std::max(1, std::min((2 * t->sms + groups - 1) / groups, std::max(1, t->C / 2)));
   A.cps = (t->C + S - 1) / S;
   S = (t->C + A.cps - 1) / A.cps;
@@ -306,9 +315,9 @@ void lutmma_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y3
     A.part = nullptr;
   }
   const int blocks = groups * S;
-  if (m <= 8) launch_mma<1>(A, blocks, s);
-  else if (m <= 16) launch_mma<2>(A, blocks, s);
-  else if (m <= 32) launch_mma<4>(A, blocks, s);
+  if (nt == 1) launch_mma<1>(A, blocks, s);
+  else if (nt == 2) launch_mma<2>(A, blocks, s);
+  else if (nt == 4) launch_mma<4>(A, blocks, s);
   else launch_mma<8>(A, blocks, s);
   if (S > 1) {
     const int64_t MN = m * t->rows;
