@@ -664,7 +664,7 @@ struct WarpKm {
   Rng rng;
   int ncen;
   double redd[kMaxG];  // cross-warp reduction slots
-  long long redl[kMaxG];
+  long long redl[kMaxG], redl2[kMaxG];
   int redi[kMaxG];
   double bcd;  // broadcasts from thread 0
   int bci;
@@ -722,7 +722,10 @@ __device__ __forceinline__ double g_sum(double v, WarpKm& S, const Grp& g) {
   __syncthreads();
   return s;
 }
-__device__ __forceinline__ double g_scan_excl(double v, WarpKm& S, const Grp& g, double* total) {
+// g_scan_excl, and the next RNG draw (thread 0, broadcast) when the total is
+// positive or `always`: the draw rides on the scan's barriers
+__device__ __forceinline__ double g_scan_excl_draw(double v, WarpKm& S, const Grp& g, double* total,
+                                                   double* u, bool always) {
   double incl = v;
   for (int off = 1; off < 32; off <<= 1) {
     const double o = __shfl_up_sync(kFull, incl, off);
@@ -732,6 +735,9 @@ __device__ __forceinline__ double g_scan_excl(double v, WarpKm& S, const Grp& g,
   double ex = __shfl_up_sync(kFull, incl, 1);
   if (g.lane == 0) ex = 0.0;
   if (g.G == 1) {
+    double d = 0.0;
+    if (g.lane == 0 && (always || wtot > 0.0)) d = S.rng.next_double();
+    *u = __shfl_sync(kFull, d, 0);
     *total = wtot;
     return ex;
   }
@@ -743,28 +749,37 @@ __device__ __forceinline__ double g_scan_excl(double v, WarpKm& S, const Grp& g,
     base = S.redd[0];
     for (int w = 1; w < g.warp; ++w) base = __dadd_rn(base, S.redd[w]);
   }
+  if (g.t == 0 && (always || tot > 0.0)) S.bcd = S.rng.next_double();
   __syncthreads();
   *total = tot;
+  *u = S.bcd;
   return g.warp > 0 ? __dadd_rn(base, ex) : ex;
 }
-__device__ __forceinline__ long long g_min_ll(long long v, WarpKm& S, const Grp& g) {
-  for (int off = 16; off; off >>= 1) v = min(v, __shfl_xor_sync(kFull, v, off));
-  if (g.G == 1) return v;
-  if (g.lane == 0) S.redl[g.warp] = v;
+// min of a and max of b over the group in one barrier round
+__device__ __forceinline__ void g_minmax_ll(long long a, long long b, WarpKm& S, const Grp& g,
+                                            long long* mn, long long* mx) {
+  for (int off = 16; off; off >>= 1) {
+    a = min(a, __shfl_xor_sync(kFull, a, off));
+    b = max(b, __shfl_xor_sync(kFull, b, off));
+  }
+  if (g.G == 1) {
+    *mn = a;
+    *mx = b;
+    return;
+  }
+  if (g.lane == 0) {
+    S.redl[g.warp] = a;
+    S.redl2[g.warp] = b;
+  }
   __syncthreads();
-  long long m = S.redl[0];
-  for (int w = 1; w < g.G; ++w) m = min(m, S.redl[w]);
+  long long m = S.redl[0], x = S.redl2[0];
+  for (int w = 1; w < g.G; ++w) {
+    m = min(m, S.redl[w]);
+    x = max(x, S.redl2[w]);
+  }
   __syncthreads();
-  return m;
-}
-__device__ __forceinline__ long long g_max_ll(long long v, WarpKm& S, const Grp& g) {
-  return -g_min_ll(-v, S, g);
-}
-__device__ __forceinline__ double g_rng(WarpKm& S, const Grp& g) {
-  __syncthreads();
-  if (g.t == 0) S.bcd = S.rng.next_double();
-  __syncthreads();
-  return S.bcd;
+  *mn = m;
+  *mx = x;
 }
 
 __device__ __forceinline__ void w_sort(WarpKm& S, int k, const Grp& g) {
@@ -877,8 +892,8 @@ __device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, W
         break;
       }
   }
-  const long long c = g_min_ll(cand, S, g);
-  const long long lp = g_max_ll(lastpos, S, g);
+  long long c, lp;
+  g_minmax_ll(cand, lastpos, S, g, &c, &lp);
   return c != LLONG_MAX ? c : (lp >= 0 ? lp : 0);
 }
 
@@ -892,8 +907,8 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
     const double m = (double)R.wv[R.idx(g.t, j)];
     if (m > 0.0) part = __dadd_rn(part, m);
   }
-  double excl = g_scan_excl(part, S, g, &total);
-  double u = g_rng(S, g);
+  double u;
+  double excl = g_scan_excl_draw(part, S, g, &total, &u, true);
   long long pick = w_sample<0>(R, d2, S, g, excl, __dmul_rn(u, total));
   for (int j = 0; j < cnt; ++j) d2[j * R.T + g.t] = INFINITY;
   if (g.t == 0) {
@@ -919,9 +934,8 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
         if (m > 0.0) part = __dadd_rn(part, m);
       }
     }
-    excl = g_scan_excl(part, S, g, &total);
+    excl = g_scan_excl_draw(part, S, g, &total, &u, false);  // draws iff total > 0
     if (total > 0.0) {
-      u = g_rng(S, g);
       pick = w_sample<1>(R, d2, S, g, excl, __dmul_rn(u, total));
       if (g.t == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
       __syncthreads();
@@ -932,9 +946,8 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
       const double m = d2[j * R.T + g.t];
       if (m > 0.0) part = __dadd_rn(part, m);
     }
-    excl = g_scan_excl(part, S, g, &total);
+    excl = g_scan_excl_draw(part, S, g, &total, &u, false);  // draws iff total > 0
     if (total > 0.0) {
-      u = g_rng(S, g);
       pick = w_sample<2>(R, d2, S, g, excl, __dmul_rn(u, total));
       if (g.t == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
       __syncthreads();
