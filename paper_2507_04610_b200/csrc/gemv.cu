@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
     }
     // the next item's table goes into the other buffer
     if (nx.p < P.np) table(g + 1);
-    if (g < 8) GV_TRACE(32 + g);
+    if (g < 31) GV_TRACE(32 + g);
     s = nx;
     item_next(P, b, nx);
     ++g;

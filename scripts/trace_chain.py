@@ -56,7 +56,7 @@ def main():
             rel = (col - t0) / 1e3
             print(f"  {nm:16s} med {np.median(rel):7.2f}  min {rel.min():7.2f}  max {rel.max():7.2f}")
     for b in (0, 1, 100):
-        row = t[b, 32:40]
+        row = t[b, 32:63]
         print(f"  CTA {b} item ends: " + " ".join(f"{(v - t0) / 1e3:.1f}" for v in row if v > 0))
     return
     print("CTA 0 per warp (rows: seg g stage k; cols: warps 0..15):")

@@ -16,9 +16,10 @@ from gemv_probe import SHAPES, synthetic  # noqa: E402
 
 from paper_2507_04610_b200 import anyq  # noqa: E402
 
-NAMES = {0: "start", 1: "loads_issued", 2: "table0_built", 3: "dep_wait_done", 4: "xprep_done",
-         5: "bar0", 6: "seg0_done", 7: "seg0_bar", 8: "seg1_done", 9: "seg1_bar", 10: "seg2_done",
-         11: "seg2_bar", 12: "seg3_done", 13: "seg3_bar", 15: "end"}
+# trace slots of gemv.cu (GV_TRACE)
+NAMES = {0: "start", 1: "table0_built", **{2 + i: f"xprep_img{i}" for i in range(8)},
+         **{16 + p: f"dep_wait_p{p}" for p in range(8)}, **{24 + p: f"dep_done_p{p}" for p in range(8)},
+         **{32 + g: f"item{g}_done" for g in range(8)}, 63: "end"}
 
 
 def main():
@@ -35,6 +36,13 @@ def main():
         for _ in range(50):
             dt.gemm(x, y, path=1)
         torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(200):
+        dt.gemm(x, y, path=1)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{name} M={m}: {e0.elapsed_time(e1) * 1e3 / 200:.2f} us per call, same tensor back to back")
     for rep in range(3):
         tr.zero_()
         L.anyq_debug_set_gemv_trace(C.c_void_p(tr.data_ptr()))
@@ -44,8 +52,6 @@ def main():
         t = tr.cpu().numpy().reshape(148, 64)
         t0 = t[:, 0][t[:, 0] > 0].min()
         print(f"{name} M={m} rep {rep}: us after first CTA start: median / min / max")
-        ghz = (t[:, 13] - t[:, 12]) / np.maximum(t[:, 15] - t[:, 0], 1)
-        print(f"  SM clock during kernel: median {np.median(ghz):.3f} GHz")
         for s, nm in NAMES.items():
             col = t[:, s]
             col = col[col > 0]
