@@ -345,6 +345,49 @@ def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):
         d.close()
 
 
+def test_gemm_chain_edge_cases(aq, orc, cuda):
+    """The chain at its limits: 8 problems (the maximum), the same DeviceTensor
+    in two problems, a 1-row and a 31-row tensor (a partial row block), a ragged
+    K, a dependency reaching back 7 problems and two reading the same earlier
+    output; equals the single launches bit for bit. 9 problems are refused."""
+    import torch
+
+    shapes = [(1, 256), (31, 256), (256, 256), (96, 256), (256, 200), (256, 256), (40, 256), (256, 256)]
+    deps = [-1, -1, -1, 2, -1, 2, -1, 0]
+    base = []
+    for i, (n, k) in enumerate(shapes):
+        qt = aq.quantize_any(orc.gaussian(n, k, 130 + i), cfg(codebook=3, max_iters=3, seed=i))
+        base.append(aq.DeviceTensor(qt))
+    dts = list(base)
+    dts[5] = dts[2]  # same weights twice
+    # problem 7 reads y0, which has 1 column: it needs a K = 1 tensor
+    qt7 = aq.quantize_any(orc.gaussian(256, 1, 140), cfg(codebook=3, max_iters=3, seed=7))
+    dts[7] = aq.DeviceTensor(qt7)
+    for m in (1, 2, 4):
+        xin = {256: torch.from_numpy(bf16(orc.gaussian(m, 256, 150 + m))).cuda().to(torch.bfloat16),
+               200: torch.from_numpy(bf16(orc.gaussian(m, 200, 160 + m))).cuda().to(torch.bfloat16)}
+        ns = [d.rows for d in dts]
+        ys = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for n in ns]
+        y32 = [torch.empty(m, n, device="cuda", dtype=torch.float32) for n in ns]
+        xs = []
+        for i, d in enumerate(deps):
+            xs.append(ys[d] if d >= 0 else xin[dts[i].cols])
+        for _ in range(2):
+            aq.gemm_chain(dts, xs, ys, y32s=y32, deps=deps)
+        torch.cuda.synchronize()
+        for i, d in enumerate(dts):
+            xi = xs[i].clone()
+            r = torch.empty(m, d.rows, device="cuda", dtype=torch.float32)
+            d.gemm(xi, None, r, path=1)
+            torch.cuda.synchronize()
+            assert torch.equal(r, y32[i]), (m, i)
+    with pytest.raises(aq.ShapeError):
+        x = torch.zeros(1, 256, device="cuda", dtype=torch.bfloat16)
+        aq.gemm_chain([base[2]] * 9, [x] * 9, deps=[-1] * 9)
+    for d in base + [dts[7]]:
+        d.close()
+
+
 @pytest.mark.parametrize("m", [1, 17, 64, 300])
 @pytest.mark.parametrize("n,k,g", [(200, 384, 128), (4096, 1024, 256), (96, 1280, 1280), (70, 200, 128)])
 def test_dequant_gemm_large_m(aq, orc, cuda, m, n, k, g):
