@@ -481,8 +481,12 @@ __device__ __forceinline__ void producer_loop(const GvParams& P, uint32_t bars, 
       const int n = min(kStageChunks, q.C - c0);
       const int g0 = c0 >> q.gshift, g1 = (c0 + n - 1) >> q.gshift;
       if (round > 0) mbar_wait(sempty + 8 * slot, (round - 1) & 1);
+#ifdef GV_NOLOAD  // compute-only experiment build: the ring keeps stale codes
+      mbar_expect_tx(sfull + 8 * slot, (uint32_t)(g1 - g0 + 1) * 128);
+#else
       mbar_expect_tx(sfull + 8 * slot, (uint32_t)n * 2048 + (uint32_t)(g1 - g0 + 1) * 128);
       bulk_g2s(sbase + P.ring[slot], cg + (size_t)c0 * 2048, (uint32_t)n * 2048, sfull + 8 * slot);
+#endif
       bulk_g2s(abring + slot * kStageAb, ag + (size_t)g0 * 128, (uint32_t)(g1 - g0 + 1) * 128,
                sfull + 8 * slot);
       if (++slot == P.nring) {
