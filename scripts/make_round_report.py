@@ -53,6 +53,14 @@ def main():
         L.append(f"| {k} | {v['value']} {v['unit']} |")
     L += ["", "Stalls per issued instruction: " +
           ", ".join(f"{k} {v}" for k, v in sorted(n["stalls_per_issue"].items(), key=lambda kv: -kv[1])[:8])]
+    kmp = os.path.join(ROOT, "profiles", "ncu_kmeans.json")
+    if os.path.exists(kmp):  # scripts/make_kmeans_profile.py
+        kn = json.load(open(kmp))
+        L += ["", "## ncu — k_kmeans_warp (4096x4096, G = 4 warps per row)", "", "| metric | value |", "|---|---|"]
+        for k, v in kn["metrics"].items():
+            L.append(f"| {k} | {v['value']} {v['unit']} |")
+        L += ["", "Stalls per issued instruction: " +
+              ", ".join(f"{k} {v}" for k, v in sorted(kn["stalls_per_issue"].items(), key=lambda kv: -kv[1])[:8])]
     with open(os.path.join(ROOT, "profiles", "round1.md"), "w") as f:
         f.write("\n".join(L) + "\n")
 
