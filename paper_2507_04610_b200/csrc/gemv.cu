@@ -448,10 +448,14 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
     }
     __syncwarp();
     if (lane == 0) {
-      __threadfence();
-      const int old = atomicAdd(&P.done[p], 1);
-      if (p == P.np - 1 && old == P.ncta - 1)  // last CTA of the last problem: reset
-        for (int r = 0; r < P.np; ++r) P.done[r] = 0;
+      if (p < P.np - 1) {  // fire-and-forget release (this warp's y stores ordered by __syncwarp)
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&P.done[p]) : "memory");
+      } else {  // the last problem's release also finds the last CTA, which resets the counters
+        __threadfence();
+        const int old = atomicAdd(&P.done[p], 1);
+        if (old == P.ncta - 1)
+          for (int r = 0; r < P.np; ++r) P.done[r] = 0;
+      }
     }
     __syncwarp();
   }
