@@ -160,6 +160,12 @@ anyq_status anyq_dequantize_values(const float* v, int64_t rows, int64_t cols,
                                    const anyq_config* cfg, const float* alphas,
                                    const float* betas, float* out);
 
+/* calibration.cpp:62-67, the per-layer statistic of collect_stats
+ * (calibration.hpp:43): exj[j] = float(sum_{m in order} |double(x[m][j])| / M)
+ * over the M x K row-major activations x, bit-identical to the reference.
+ * ShapeError when M < 1, NonFiniteError on NaN/Inf inputs (require_finite). */
+anyq_status anyq_column_mean_abs(const float* x, int64_t m, int64_t k, float* exj);
+
 /* ---------------------------------------------------------------------------
  * GEMM (host buffers)
  * ------------------------------------------------------------------------- */
@@ -241,6 +247,10 @@ anyq_status anyq_dev_quantize_any(const float* w_dev, int64_t rows, int64_t cols
                                   int64_t row_offset, uint8_t* codes_dev,
                                   float* luts_dev, float* alphas_dev,
                                   float* betas_dev, void* stream);
+
+/* anyq_column_mean_abs on device buffers (validation syncs the stream once). */
+anyq_status anyq_dev_column_mean_abs(const float* x_dev, int64_t m, int64_t k, float* exj_dev,
+                                     void* stream);
 
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches accounting). */

@@ -1084,6 +1084,21 @@ int orc_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int64_t
   API_END
 }
 
+/* collect_stats, calibration.cpp:50-67: the per-layer statistic of the first
+ * layer's inputs — E|x_j| = float(sum over samples in order of |double(x)| / M);
+ * require_finite(inputs) (:52), at least one sample (:54). */
+int orc_column_mean_abs(const float* x, int64_t m, int64_t k, float* out) {
+  API_BEGIN
+  require_finite(x, m * k, "collect_stats inputs");
+  if (m < 1) fail(ANYQ_ERR_SHAPE, "need at least one input sample");
+  for (int64_t j = 0; j < k; ++j) {
+    double acc = 0;
+    for (int64_t r = 0; r < m; ++r) acc += fabs((double)x[r * k + j]);
+    out[j] = (float)(acc / (double)m);
+  }
+  API_END
+}
+
 int orc_gemm_reference(const float* x, int64_t m, const anyq_qtensor* qt, float* y) {
   API_BEGIN
   float* w = dequant(qt);

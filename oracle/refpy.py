@@ -65,6 +65,7 @@ class _Lib:
             "gemm_reference": (i32, [fptr, i64, qt, fptr]),
             "gemm_fused": (i32, [fptr, i64, i64, qt, i32, i32, fptr]),
             "gemm_dense": (i32, [fptr, i64, fptr, i64, i64, fptr]),
+            "column_mean_abs": (i32, [fptr, i64, i64, fptr]),
             "pack_codes": (i32, [u8, i64, i64, i32, u8]),
             "unpack_codes": (i32, [u8, i64, i64, i32, u8]),
             "to_ktiled": (i32, [qt, i32, u8]),
@@ -225,6 +226,13 @@ class _Lib:
                                   _abi.fp(y))
         )
         return y
+
+    def column_mean_abs(self, x) -> np.ndarray:
+        """E|x_j| of collect_stats (calibration.cpp:62-67) over M x K activations."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty(x.shape[1], np.float32)
+        self._check(self.fn["column_mean_abs"](_abi.fp(x), x.shape[0], x.shape[1], _abi.fp(out)))
+        return out
 
     def pack_codes(self, codes, bits) -> np.ndarray:
         codes = np.ascontiguousarray(codes, np.uint8)

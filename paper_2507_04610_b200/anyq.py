@@ -136,6 +136,8 @@ def lib() -> C.CDLL:
         "anyq_dev_gemm_chain_deps": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                           C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
+        "anyq_column_mean_abs": (st, [fptr, i64, i64, fptr]),
+        "anyq_dev_column_mean_abs": (st, [vp, i64, i64, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -156,6 +158,7 @@ EXPORTED_SYMBOLS = (
     "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_auto_path", "anyq_dev_quantize_any",
     "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
+    "anyq_column_mean_abs", "anyq_dev_column_mean_abs",
 )
 
 
@@ -441,6 +444,30 @@ def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None, dep
                     s.cuda_stream, wait_prev,
                     [y.data_ptr() for y in y32s] if y32s is not None else None, deps)
     return ys
+
+
+def column_mean_abs(x) -> np.ndarray:
+    """E|x_j| over M x K activations: the per-layer statistic of collect_stats
+    (calibration.cpp:62-67), computed on the GPU, bit-identical to the reference."""
+    x = _f32(x)
+    if x.ndim != 2:
+        raise ShapeError("activations must be a 2-D (samples x channels) array")
+    out = np.empty(x.shape[1], np.float32)
+    _check(lib().anyq_column_mean_abs(_abi.fp(x), x.shape[0], x.shape[1], _abi.fp(out)))
+    return out
+
+
+def dev_column_mean_abs(x, out=None, stream=None):
+    """column_mean_abs on a contiguous fp32 CUDA tensor; returns the (K,) fp32 tensor."""
+    import torch
+
+    assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.dim() == 2
+    if out is None:
+        out = torch.empty(x.shape[1], dtype=torch.float32, device=x.device)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(lib().anyq_dev_column_mean_abs(C.c_void_p(x.data_ptr()), x.shape[0], x.shape[1],
+                                          C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
+    return out
 
 
 def dev_quantize_any(w, cfg: Config, exj=None, row_offset: int = 0, stream=None):

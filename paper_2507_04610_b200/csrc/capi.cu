@@ -461,6 +461,31 @@ anyq_status anyq_dequantize_values(const float* v, int64_t rows, int64_t cols,
   return affine_host(v, rows, cols, cfg, alphas, betas, 0, out);
 }
 
+static void column_mean_abs_device(const float* x, int64_t m, int64_t k, float* exj, cudaStream_t s) {
+  if (m < 1) fail(ANYQ_ERR_SHAPE, "need at least one input sample");
+  if (k < 0) fail(ANYQ_ERR_SHAPE, "negative channel count");
+  DevBuf<int> err(1, s);
+  ANYQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+  launch_col_mean_abs(x, m, k, exj, err.p, s);
+  ANYQ_CUDA(cudaStreamSynchronize(s));
+  check_device_error(err.p, "collect_stats inputs");  // NonFiniteError as require_finite
+}
+
+anyq_status anyq_column_mean_abs(const float* x, int64_t m, int64_t k, float* exj) {
+  return guard([&] {
+    if (m < 1) fail(ANYQ_ERR_SHAPE, "need at least one input sample");
+    DevBuf<float> dx(m * k), de(k);
+    dx.upload(x, m * k);
+    column_mean_abs_device(dx.p, m, k, de.p, 0);
+    de.download(exj, k);
+  });
+}
+
+anyq_status anyq_dev_column_mean_abs(const float* x_dev, int64_t m, int64_t k, float* exj_dev,
+                                     void* stream) {
+  return guard([&] { column_mean_abs_device(x_dev, m, k, exj_dev, (cudaStream_t)stream); });
+}
+
 anyq_status anyq_dequantize(const anyq_qtensor* qt, float* w_out) {
   return guard([&] {
     check_qt(qt);

@@ -10,6 +10,9 @@
 namespace anyq_b200 {
 
 void launch_check_finite(const float* p, int64_t n, int* err, int status, cudaStream_t s);
+// E|x_j| of collect_stats (calibration.cpp:62-67), bit-identical (quant_kernels.cu)
+// (non-finite inputs set *err = ANYQ_ERR_NONFINITE; the output is then undefined)
+void launch_col_mean_abs(const float* x, int64_t m, int64_t k, float* out, int* err, cudaStream_t s);
 void launch_check_stats(const float* p, int64_t n, int* err, cudaStream_t s);
 void launch_scales(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg, float qmin,
                    float qmax, float* alphas, float* betas, cudaStream_t s);

@@ -463,4 +463,65 @@ void launch_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int
   ANYQ_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------------
+// Activation statistics E|x_j| (collect_stats, calibration.cpp:62-67): per
+// channel j, sum over the samples m = 0..M-1 IN ORDER of |x(m, j)| in double,
+// divided by M in double, rounded once to float. The sum stays sequential per
+// channel (bit-identical to the reference); what is parallel is the memory:
+// a CTA owns 32 channels, its 8 warps load the next 256-sample x 32-channel
+// tile (one 128-B row segment per load, 32 loads in flight per lane) while
+// warp 0 runs the 32 sequential double sums over the current tile in shared
+// memory. HBM-bound when M is large and the DADD chain (M deep) otherwise.
+// ---------------------------------------------------------------------------
+constexpr int kStatCols = 32, kStatRows = 256, kStatThreads = 256;
+
+__global__ void __launch_bounds__(kStatThreads) k_col_mean_abs(const float* __restrict__ x, int64_t m,
+                                                               int64_t k, float* __restrict__ out,
+                                                               int* __restrict__ err) {
+  __shared__ float tile[kStatRows][kStatCols + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kStatCols + lane;
+  const bool col = j < k;
+  constexpr int kPer = kStatRows / (kStatThreads / 32);  // rows per warp and tile
+  float v[kPer];
+  auto load = [&](int64_t r0) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int64_t r = r0 + warp * kPer + i;
+      v[i] = (col && r < m) ? __ldg(x + r * k + j) : 0.0f;
+    }
+  };
+  double acc = 0.0;
+  bool finite = true;  // require_finite(inputs) (calibration.cpp:52), fused into the one pass
+  load(0);
+  for (int64_t r0 = 0; r0 < m; r0 += kStatRows) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      finite &= isfinite(v[i]);
+      tile[warp * kPer + i][lane] = v[i];
+    }
+    __syncthreads();
+    if (r0 + kStatRows < m) load(r0 + kStatRows);  // next tile in flight during the sums
+    if (warp == 0) {
+      const int n = (int)(m - r0 < kStatRows ? m - r0 : kStatRows);
+      if (n == kStatRows) {  // shared-memory reads run ahead of the dependent adds
+#pragma unroll 32
+        for (int i = 0; i < kStatRows; ++i) acc += fabs((double)tile[i][lane]);
+      } else {
+        for (int i = 0; i < n; ++i) acc += fabs((double)tile[i][lane]);
+      }
+    }
+    __syncthreads();
+  }
+  if (!finite) atomicExch(err, (int)ANYQ_ERR_NONFINITE);
+  if (warp == 0 && col) out[j] = (float)(acc / (double)m);
+}
+
+void launch_col_mean_abs(const float* x, int64_t m, int64_t k, float* out, int* err, cudaStream_t s) {
+  if (k <= 0 || m <= 0) return;
+  k_col_mean_abs<<<(unsigned)((k + kStatCols - 1) / kStatCols), kStatThreads, 0, s>>>(x, m, k, out,
+                                                                                       err);
+  ANYQ_LAUNCHED();
+}
+
 }  // namespace anyq_b200

@@ -201,3 +201,34 @@ def test_oracle_equals_reference(orc, ref, fmt, trial):
         assert bits_equal(a.luts, b.luts)
     x = orc.gaussian(1 + int(r[5] * 9), k, 800 + trial)
     assert bits_equal(orc.gemm_fused(x, a), ref.gemm_fused(x, b))
+
+
+def _seq_mean_abs(x):
+    """collect_stats' statistic in numpy: the double sum runs over samples in order."""
+    acc = np.zeros(x.shape[1], np.float64)
+    for r in range(x.shape[0]):
+        acc += np.abs(x[r].astype(np.float64))
+    return (acc / x.shape[0]).astype(np.float32)
+
+
+def test_column_mean_abs_oracle(orc):
+    """E|x_j| of collect_stats (calibration.cpp:62-67): the reference's own hand
+    case (test_calibration.cpp:30-40), zeros, order/duplication invariance
+    (test_calibration.cpp:64-84, 1e-6) and the sequential double sum."""
+    from oracle.refpy import OracleError
+
+    assert orc.column_mean_abs(np.array([[1, -1], [3, -3]], np.float32)).tolist() == [2.0, 2.0]
+    assert not orc.column_mean_abs(np.zeros((5, 4), np.float32)).any()
+    x = orc.gaussian(32, 16, 77)
+    base = orc.column_mean_abs(x)
+    assert np.allclose(orc.column_mean_abs(x[::-1]), base, rtol=1e-6, atol=0)
+    assert np.allclose(orc.column_mean_abs(np.vstack([x, x])), base, rtol=1e-6, atol=0)
+    for shape, seed in [((1, 7), 1), ((300, 33), 2), ((1000, 5), 3)]:
+        x = orc.heavy_tailed(*shape, seed, 0.05, 40.0)
+        assert np.array_equal(orc.column_mean_abs(x), _seq_mean_abs(x))
+    bad = np.ones((3, 3), np.float32)
+    bad[1, 2] = np.inf
+    with pytest.raises(OracleError):
+        orc.column_mean_abs(bad)
+    with pytest.raises(OracleError):
+        orc.column_mean_abs(np.zeros((0, 3), np.float32))
