@@ -166,6 +166,18 @@ anyq_status anyq_dequantize_values(const float* v, int64_t rows, int64_t cols,
  * ShapeError when M < 1, NonFiniteError on NaN/Inf inputs (require_finite). */
 anyq_status anyq_column_mean_abs(const float* x, int64_t m, int64_t k, float* exj);
 
+/* eval.cpp:11-29 weight_error(w, qt) -> (mse, relative Frobenius error) and
+ * eval.cpp:31-46 output_error(w, qt, x) -> mean squared output error of
+ * gemm_reference(x, qt) against gemm_dense(x, w). Both GEMMs and the
+ * dequantisation are the bit-identical device paths; the double sums are a
+ * deterministic tree (equal to the reference's sequential sums up to
+ * reassociation). ShapeError on mismatched shapes, CodeRangeError from
+ * dequantize. */
+anyq_status anyq_weight_error(const float* w, int64_t rows, int64_t cols, const anyq_qtensor* qt,
+                              double* mse, double* rel);
+anyq_status anyq_output_error(const float* w, int64_t rows, int64_t cols, const anyq_qtensor* qt,
+                              const float* x, int64_t m, int64_t x_cols, double* mse);
+
 /* ---------------------------------------------------------------------------
  * GEMM (host buffers)
  * ------------------------------------------------------------------------- */

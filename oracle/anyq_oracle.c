@@ -1084,6 +1084,40 @@ int orc_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int64_t
   API_END
 }
 
+/* weight_error, eval.cpp:11-29 (sequential double sums over i, j). */
+int orc_weight_error(const float* w, const anyq_qtensor* qt, double* mse, double* rel) {
+  API_BEGIN
+  float* d = dequant(qt);
+  double sq = 0, ref = 0;
+  for (int64_t e = 0; e < qt->rows * qt->cols; ++e) {
+    double x = (double)w[e] - (double)d[e];
+    sq += x * x;
+    ref += (double)w[e] * (double)w[e];
+  }
+  double count = (double)qt->rows * (double)qt->cols;
+  *mse = sq / count;
+  *rel = ref > 0 ? sqrt(sq) / sqrt(ref) : sqrt(sq);
+  API_END
+}
+
+/* output_error, eval.cpp:31-46: gemm_dense(x, w) vs gemm_reference(x, qt). */
+int orc_output_error(const float* w, const anyq_qtensor* qt, const float* x, int64_t m, double* mse) {
+  API_BEGIN
+  const int64_t n = qt->rows, k = qt->cols;
+  float* y = (float*)oalloc(sizeof(float) * (size_t)(m * n + 1));
+  float* yq = (float*)oalloc(sizeof(float) * (size_t)(m * n + 1));
+  float* d = dequant(qt);
+  dense(x, m, w, n, k, y);
+  dense(x, m, d, n, k, yq);
+  double sq = 0;
+  for (int64_t e = 0; e < m * n; ++e) {
+    double v = (double)yq[e] - (double)y[e];
+    sq += v * v;
+  }
+  *mse = sq / ((double)m * (double)n);
+  API_END
+}
+
 /* collect_stats, calibration.cpp:50-67: the per-layer statistic of the first
  * layer's inputs — E|x_j| = float(sum over samples in order of |double(x)| / M);
  * require_finite(inputs) (:52), at least one sample (:54). */

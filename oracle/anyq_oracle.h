@@ -35,6 +35,8 @@ int orc_time_gemm_fused(const float* x, int64_t m, const anyq_qtensor* qt, int r
                         double* secs);
 int orc_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int64_t k, float* y);
 int orc_column_mean_abs(const float* x, int64_t m, int64_t k, float* out);
+int orc_weight_error(const float* w, const anyq_qtensor* qt, double* mse, double* rel);
+int orc_output_error(const float* w, const anyq_qtensor* qt, const float* x, int64_t m, double* mse);
 int orc_pack_codes(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out);
 int orc_unpack_codes(const uint8_t* packed, int64_t rows, int64_t cols, int bits, uint8_t* out);
 int orc_to_ktiled(const anyq_qtensor* qt, int tile_k, uint8_t* codes_out);

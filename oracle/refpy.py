@@ -66,6 +66,8 @@ class _Lib:
             "gemm_fused": (i32, [fptr, i64, i64, qt, i32, i32, fptr]),
             "gemm_dense": (i32, [fptr, i64, fptr, i64, i64, fptr]),
             "column_mean_abs": (i32, [fptr, i64, i64, fptr]),
+            "weight_error": (i32, [fptr, qt, dptr, dptr]),
+            "output_error": (i32, [fptr, qt, fptr, i64, dptr]),
             "pack_codes": (i32, [u8, i64, i64, i32, u8]),
             "unpack_codes": (i32, [u8, i64, i64, i32, u8]),
             "to_ktiled": (i32, [qt, i32, u8]),
@@ -233,6 +235,23 @@ class _Lib:
         out = np.empty(x.shape[1], np.float32)
         self._check(self.fn["column_mean_abs"](_abi.fp(x), x.shape[0], x.shape[1], _abi.fp(out)))
         return out
+
+    def weight_error(self, w, qt: QuantizedTensor):
+        """eval.cpp:11-29 -> (mse, rel)."""
+        w = np.ascontiguousarray(w, np.float32)
+        mse, rel = C.c_double(), C.c_double()
+        c = qt.as_c()
+        self._check(self.fn["weight_error"](_abi.fp(w), C.byref(c), C.byref(mse), C.byref(rel)))
+        return mse.value, rel.value
+
+    def output_error(self, w, qt: QuantizedTensor, x) -> float:
+        """eval.cpp:31-46."""
+        w = np.ascontiguousarray(w, np.float32)
+        x = np.ascontiguousarray(x, np.float32)
+        mse = C.c_double()
+        c = qt.as_c()
+        self._check(self.fn["output_error"](_abi.fp(w), C.byref(c), _abi.fp(x), x.shape[0], C.byref(mse)))
+        return mse.value
 
     def pack_codes(self, codes, bits) -> np.ndarray:
         codes = np.ascontiguousarray(codes, np.uint8)

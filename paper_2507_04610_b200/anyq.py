@@ -137,6 +137,8 @@ def lib() -> C.CDLL:
                                           C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
         "anyq_column_mean_abs": (st, [fptr, i64, i64, fptr]),
+        "anyq_weight_error": (st, [fptr, i64, i64, qt, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "anyq_output_error": (st, [fptr, i64, i64, qt, fptr, i64, i64, C.POINTER(C.c_double)]),
         "anyq_dev_column_mean_abs": (st, [vp, i64, i64, vp, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -158,7 +160,7 @@ EXPORTED_SYMBOLS = (
     "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_auto_path", "anyq_dev_quantize_any",
     "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
-    "anyq_column_mean_abs", "anyq_dev_column_mean_abs",
+    "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
 )
 
 
@@ -301,6 +303,26 @@ def dequantize(qt: QuantizedTensor) -> np.ndarray:
     c = qt.as_c()
     _check(lib().anyq_dequantize(C.byref(c), _abi.fp(out)))
     return out
+
+
+def weight_error(w, qt: QuantizedTensor):
+    """eval.cpp:11-29: (mse, relative Frobenius error) of dequantize(qt) against w."""
+    w = _f32(w)
+    mse, rel = C.c_double(), C.c_double()
+    c = qt.as_c()
+    _check(lib().anyq_weight_error(_abi.fp(w), w.shape[0], w.shape[1], C.byref(c), C.byref(mse),
+                                   C.byref(rel)))
+    return mse.value, rel.value
+
+
+def output_error(w, qt: QuantizedTensor, x) -> float:
+    """eval.cpp:31-46: mean squared error of gemm_reference(x, qt) against gemm_dense(x, w)."""
+    w, x = _f32(w), _f32(x)
+    mse = C.c_double()
+    c = qt.as_c()
+    _check(lib().anyq_output_error(_abi.fp(w), w.shape[0], w.shape[1], C.byref(c), _abi.fp(x),
+                                   x.shape[0], x.shape[1], C.byref(mse)))
+    return mse.value
 
 
 # ---------------------------------------------------------------------------

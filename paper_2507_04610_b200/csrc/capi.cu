@@ -2,6 +2,7 @@
 // argument validation with the reference's error classes, H2D/D2H staging for
 // the host-buffer calls, and kernel launches. All compute is on the device.
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -486,20 +487,70 @@ anyq_status anyq_dev_column_mean_abs(const float* x_dev, int64_t m, int64_t k, f
   return guard([&] { column_mean_abs_device(x_dev, m, k, exj_dev, (cudaStream_t)stream); });
 }
 
+// dequantize(qt) into a device buffer (shared by dequantize and the eval metrics)
+static void dequant_to_device(const anyq_qtensor* qt, DevTensorArrays& t, float* w_dev) {
+  t.upload(qt);
+  Table fixed{};
+  if (qt->cfg.codebook != ANYQ_CB_ANY)
+    fixed = effective_table(fixed_table(qt->cfg), qt->cfg.symmetric != 0);
+  DevBuf<int> err(1);
+  err.zero();
+  launch_dequant(t.codes.p, qt->rows, qt->cols, qt->cfg.bits, qt->layout == ANYQ_LAYOUT_KTILED,
+                 qt->tile_k, t.luts.p, fixed, qt->cfg, t.alphas.p, t.betas.p, w_dev, err.p, 0);
+  check_device_error(err.p, "dequantize");
+}
+
+static void sqdiff_sums(const float* a, const float* b, int64_t n, double out[2]) {
+  DevBuf<double> part(2 * 592), sums(2);
+  launch_sqdiff_sums(a, b, n, part.p, sums.p, 0);
+  sums.download(out, 2);
+}
+
+anyq_status anyq_weight_error(const float* w, int64_t rows, int64_t cols, const anyq_qtensor* qt,
+                              double* mse, double* rel) {
+  return guard([&] {
+    check_qt(qt);
+    if (rows != qt->rows || cols != qt->cols) fail(ANYQ_ERR_SHAPE, "weight_error: shapes differ");
+    const int64_t n = rows * cols;
+    DevBuf<float> dw(n), dq(n);
+    dw.upload(w, n);
+    DevTensorArrays t;
+    dequant_to_device(qt, t, dq.p);
+    double s[2] = {0.0, 0.0};
+    if (n > 0) sqdiff_sums(dw.p, dq.p, n, s);
+    *mse = s[0] / ((double)rows * (double)cols);
+    *rel = s[1] > 0 ? std::sqrt(s[0]) / std::sqrt(s[1]) : std::sqrt(s[0]);
+  });
+}
+
+anyq_status anyq_output_error(const float* w, int64_t rows, int64_t cols, const anyq_qtensor* qt,
+                              const float* x, int64_t m, int64_t x_cols, double* mse) {
+  return guard([&] {
+    check_qt(qt);
+    if (rows != qt->rows || cols != qt->cols)
+      fail(ANYQ_ERR_SHAPE, "output_error: weight shapes differ");
+    if (x_cols != cols) fail(ANYQ_ERR_SHAPE, "output_error: activation width mismatch");
+    DevBuf<float> dw(rows * cols), dq(rows * cols), dx(m * cols), y(m * rows), yq(m * rows);
+    dw.upload(w, rows * cols);
+    dx.upload(x, m * cols);
+    DevTensorArrays t;
+    dequant_to_device(qt, t, dq.p);
+    double s[2] = {0.0, 0.0};
+    if (m > 0 && rows > 0) {
+      launch_gemm_dense(dx.p, m, dw.p, rows, cols, y.p, 0);   // gemm_dense(x, w)
+      launch_gemm_dense(dx.p, m, dq.p, rows, cols, yq.p, 0);  // gemm_reference(x, qt)
+      sqdiff_sums(yq.p, y.p, m * rows, s);
+    }
+    *mse = s[0] / ((double)m * (double)rows);
+  });
+}
+
 anyq_status anyq_dequantize(const anyq_qtensor* qt, float* w_out) {
   return guard([&] {
     check_qt(qt);
     DevTensorArrays t;
-    t.upload(qt);
-    Table fixed{};
-    if (qt->cfg.codebook != ANYQ_CB_ANY)
-      fixed = effective_table(fixed_table(qt->cfg), qt->cfg.symmetric != 0);
     DevBuf<float> w(qt->rows * qt->cols);
-    DevBuf<int> err(1);
-    err.zero();
-    launch_dequant(t.codes.p, qt->rows, qt->cols, qt->cfg.bits, qt->layout == ANYQ_LAYOUT_KTILED,
-                   qt->tile_k, t.luts.p, fixed, qt->cfg, t.alphas.p, t.betas.p, w.p, err.p, 0);
-    check_device_error(err.p, "dequantize");
+    dequant_to_device(qt, t, w.p);
     w.download(w_out, qt->rows * qt->cols);
   });
 }

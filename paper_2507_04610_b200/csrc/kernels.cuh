@@ -10,6 +10,9 @@
 namespace anyq_b200 {
 
 void launch_check_finite(const float* p, int64_t n, int* err, int status, cudaStream_t s);
+// out2 = {sum (a-b)^2, sum a^2} in double, deterministic tree; part: 2 * 592 doubles
+void launch_sqdiff_sums(const float* a, const float* b, int64_t n, double* part, double* out2,
+                        cudaStream_t s);
 // E|x_j| of collect_stats (calibration.cpp:62-67), bit-identical (quant_kernels.cu)
 // (non-finite inputs set *err = ANYQ_ERR_NONFINITE; the output is then undefined)
 void launch_col_mean_abs(const float* x, int64_t m, int64_t k, float* out, int* err, cudaStream_t s);

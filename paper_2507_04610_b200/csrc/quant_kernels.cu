@@ -524,4 +524,72 @@ void launch_col_mean_abs(const float* x, int64_t m, int64_t k, float* out, int* 
   ANYQ_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------------
+// eval.cpp:11-46 (weight_error / output_error): sum (a - b)^2 and sum a^2 in
+// double, products and sums rounded separately like the reference's
+// `sq += e * e` (no FMA contraction). The reference sums sequentially; here a
+// fixed-shape two-level tree (kRedBlocks x kRedThreads strided partials, then
+// one block) -- deterministic on any device, equal to the reference up to
+// reassociation of the double sums.
+// ---------------------------------------------------------------------------
+constexpr int kRedBlocks = 592, kRedThreads = 256;
+
+__device__ __forceinline__ void tree2(double* r1, double* r2, double& s1, double& s2) {
+  const int t = threadIdx.x;
+  r1[t] = s1;
+  r2[t] = s2;
+  __syncthreads();
+  for (int w = kRedThreads / 2; w > 0; w >>= 1) {
+    if (t < w) {
+      r1[t] = __dadd_rn(r1[t], r1[t + w]);
+      r2[t] = __dadd_rn(r2[t], r2[t + w]);
+    }
+    __syncthreads();
+  }
+  s1 = r1[0];
+  s2 = r2[0];
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sqdiff_partial(const float* __restrict__ a,
+                                                                const float* __restrict__ b, int64_t n,
+                                                                double* __restrict__ part) {
+  __shared__ double r1[kRedThreads], r2[kRedThreads];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; e < n;
+       e += (int64_t)kRedBlocks * kRedThreads) {
+    const double av = (double)a[e];
+    const double d = __dsub_rn(av, (double)b[e]);
+    s1 = __dadd_rn(s1, __dmul_rn(d, d));
+    s2 = __dadd_rn(s2, __dmul_rn(av, av));
+  }
+  tree2(r1, r2, s1, s2);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s1;
+    part[kRedBlocks + blockIdx.x] = s2;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sum_partials(const double* __restrict__ part,
+                                                              double* __restrict__ out) {
+  __shared__ double r1[kRedThreads], r2[kRedThreads];
+  double s1 = 0.0, s2 = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += kRedThreads) {
+    s1 = __dadd_rn(s1, part[i]);
+    s2 = __dadd_rn(s2, part[kRedBlocks + i]);
+  }
+  tree2(r1, r2, s1, s2);
+  if (threadIdx.x == 0) {
+    out[0] = s1;
+    out[1] = s2;
+  }
+}
+
+void launch_sqdiff_sums(const float* a, const float* b, int64_t n, double* part, double* out2,
+                        cudaStream_t s) {
+  k_sqdiff_partial<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, part);
+  ANYQ_LAUNCHED();
+  k_sum_partials<<<1, kRedThreads, 0, s>>>(part, out2);
+  ANYQ_LAUNCHED();
+}
+
 }  // namespace anyq_b200

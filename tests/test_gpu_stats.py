@@ -1,5 +1,6 @@
-"""E|x_j| activation statistics on the GPU (collect_stats, calibration.cpp:62-67;
-SURVEY.md §8(f) row 4) against the oracle restatement: bit-exact."""
+"""The statistics around the path on the GPU: E|x_j| of
+collect_stats (calibration.cpp:62-67, bit-exact) and weight_error / output_error
+(eval.cpp:11-46), against the oracle restatement."""
 import numpy as np
 import pytest
 
@@ -37,3 +38,34 @@ def test_column_mean_abs_errors(aq, cuda):
         aq.column_mean_abs(bad)
     with pytest.raises(aq.ShapeError):
         aq.column_mean_abs(np.zeros((0, 3), np.float32))
+
+
+@pytest.mark.parametrize("fmt", ["any4", "int4", "fp4", "nf4", "any3"])
+def test_eval_metrics_match_oracle(aq, orc, cuda, fmt):
+    """weight_error / output_error (eval.cpp:11-46): dequantisation and both GEMMs are the
+    bit-identical device paths; the double sums differ from the reference's sequential
+    order only by reassociation (rtol 1e-12)."""
+    from anyq_testutil import cfg
+
+    codebook, bits = {"any4": (3, 4), "int4": (0, 4), "fp4": (1, 4), "nf4": (2, 4), "any3": (3, 3)}[fmt]
+    w = orc.heavy_tailed(300, 520, 11, 0.02, 20.0)
+    qt = orc.quantize(w, cfg(codebook=codebook, bits=bits, granularity=3, group_size=128,
+                             max_iters=6, seed=2))
+    mse, rel = aq.weight_error(w, qt)
+    omse, orel = orc.weight_error(w, qt)
+    assert np.isclose(mse, omse, rtol=1e-12, atol=0) and np.isclose(rel, orel, rtol=1e-12, atol=0)
+    for m in (1, 7, 64):
+        x = orc.gaussian(m, 520, 20 + m)
+        assert np.isclose(aq.output_error(w, qt, x), orc.output_error(w, qt, x), rtol=1e-12, atol=0)
+
+
+def test_eval_metrics_edges(aq, orc, cuda):
+    from anyq_testutil import cfg
+
+    w = np.zeros((8, 64), np.float32)  # zero reference energy: rel = sqrt(sq) (eval.cpp:27)
+    qt = orc.quantize(orc.gaussian(8, 64, 1), cfg(codebook=3, granularity=3, group_size=64, max_iters=3))
+    assert np.isclose(aq.weight_error(w, qt)[1], orc.weight_error(w, qt)[1], rtol=1e-12)
+    with pytest.raises(aq.ShapeError):
+        aq.weight_error(np.zeros((8, 63), np.float32), qt)
+    with pytest.raises(aq.ShapeError):
+        aq.output_error(np.zeros((8, 64), np.float32), qt, np.zeros((2, 63), np.float32))

@@ -232,3 +232,18 @@ def test_column_mean_abs_oracle(orc):
         orc.column_mean_abs(bad)
     with pytest.raises(OracleError):
         orc.column_mean_abs(np.zeros((0, 3), np.float32))
+
+
+def test_eval_metrics_oracle(orc):
+    """weight_error / output_error restated from eval.cpp:11-46, against numpy."""
+    w = orc.gaussian(40, 200, 5)
+    qt = orc.quantize(w, cfg(codebook=3, granularity=3, group_size=64, max_iters=5, seed=1))
+    d = orc.dequantize(qt).astype(np.float64)
+    mse, rel = orc.weight_error(w, qt)
+    e = w.astype(np.float64) - d
+    assert np.isclose(mse, (e * e).sum() / w.size, rtol=1e-12)
+    assert np.isclose(rel, np.sqrt((e * e).sum()) / np.sqrt((w.astype(np.float64) ** 2).sum()), rtol=1e-12)
+    x = orc.gaussian(6, 200, 6)
+    y = orc.gemm_dense(x, w).astype(np.float64)
+    yq = orc.gemm_reference(x, qt).astype(np.float64)
+    assert np.isclose(orc.output_error(w, qt, x), ((yq - y) ** 2).mean(), rtol=1e-12)
