@@ -178,6 +178,18 @@ anyq_status anyq_weight_error(const float* w, int64_t rows, int64_t cols, const 
 anyq_status anyq_output_error(const float* w, int64_t rows, int64_t cols, const anyq_qtensor* qt,
                               const float* x, int64_t m, int64_t x_cols, double* mse);
 
+/* ANYQ v1 files (pack.hpp write_file / read_file, pack.cpp:293-471).
+ * anyq_write_file is byte-identical to write_file (lut_store / scale_store of
+ * qt choose the stored precision). anyq_read_file_header parses and validates
+ * the header and section table and fills the scalar fields of hdr (rows, cols,
+ * cfg, layout, tile_k, stores, num_groups; LUT entries = anyq_lut_entries);
+ * the caller then allocates the arrays and calls anyq_read_file, which runs
+ * every check of read_file in its order (MagicError, VersionError,
+ * TruncatedError, InvariantError, CodeRangeError). Host only: no device. */
+anyq_status anyq_write_file(const anyq_qtensor* qt, const char* path);
+anyq_status anyq_read_file_header(const char* path, anyq_qtensor* hdr);
+anyq_status anyq_read_file(const char* path, anyq_qtensor* qt);
+
 /* ---------------------------------------------------------------------------
  * GEMM (host buffers)
  * ------------------------------------------------------------------------- */
@@ -251,6 +263,9 @@ anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
                                      const void* const* x_bf16, void* const* y_bf16,
                                      float* const* y_f32, const int32_t* deps, int64_t m,
                                      void* stream);
+
+/* read_file straight into the prepacked device layout. */
+anyq_status anyq_dev_tensor_load(const char* path, anyq_dev_tensor** out);
 
 /* Device quantize: rows [row_offset, row_offset+rows) of a matrix, fp32 in,
  * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device. */

@@ -66,6 +66,8 @@ class _Lib:
             "gemm_fused": (i32, [fptr, i64, i64, qt, i32, i32, fptr]),
             "gemm_dense": (i32, [fptr, i64, fptr, i64, i64, fptr]),
             "column_mean_abs": (i32, [fptr, i64, i64, fptr]),
+            "write_file": (i32, [qt, C.c_char_p]),
+            "read_file": (i32, [C.c_char_p, qt]),
             "weight_error": (i32, [fptr, qt, dptr, dptr]),
             "output_error": (i32, [fptr, qt, fptr, i64, dptr]),
             "pack_codes": (i32, [u8, i64, i64, i32, u8]),
@@ -234,6 +236,19 @@ class _Lib:
         x = np.ascontiguousarray(x, np.float32)
         out = np.empty(x.shape[1], np.float32)
         self._check(self.fn["column_mean_abs"](_abi.fp(x), x.shape[0], x.shape[1], _abi.fp(out)))
+        return out
+
+    def write_file(self, qt: QuantizedTensor, path) -> None:
+        """pack.cpp:293-345 (reference build only)."""
+        c = qt.as_c()
+        self._check(self.fn["write_file"](C.byref(c), os.fsencode(path)))
+
+    def read_file(self, path, like: QuantizedTensor) -> QuantizedTensor:
+        """pack.cpp:347-471 (reference build only); `like` supplies the array sizes."""
+        out = like.clone()
+        c = out.as_c()
+        self._check(self.fn["read_file"](os.fsencode(path), C.byref(c)))
+        out.layout, out.tile_k, out.lut_store, out.scale_store = c.layout, c.tile_k, c.lut_store, c.scale_store
         return out
 
     def weight_error(self, w, qt: QuantizedTensor):

@@ -137,6 +137,10 @@ def lib() -> C.CDLL:
                                           C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
         "anyq_column_mean_abs": (st, [fptr, i64, i64, fptr]),
+        "anyq_write_file": (st, [qt, C.c_char_p]),
+        "anyq_read_file_header": (st, [C.c_char_p, qt]),
+        "anyq_read_file": (st, [C.c_char_p, qt]),
+        "anyq_dev_tensor_load": (st, [C.c_char_p, C.POINTER(vp)]),
         "anyq_weight_error": (st, [fptr, i64, i64, qt, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "anyq_output_error": (st, [fptr, i64, i64, qt, fptr, i64, i64, C.POINTER(C.c_double)]),
         "anyq_dev_column_mean_abs": (st, [vp, i64, i64, vp, vp]),
@@ -161,6 +165,7 @@ EXPORTED_SYMBOLS = (
     "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
     "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
+    "anyq_write_file", "anyq_read_file_header", "anyq_read_file", "anyq_dev_tensor_load",
 )
 
 
@@ -305,6 +310,25 @@ def dequantize(qt: QuantizedTensor) -> np.ndarray:
     return out
 
 
+def write_file(qt: QuantizedTensor, path) -> None:
+    """pack.cpp:293-345 write_file: byte-identical ANYQ v1 file (lut_store / scale_store of qt)."""
+    c = qt.as_c()
+    _check(lib().anyq_write_file(C.byref(c), os.fsencode(path)))
+
+
+def read_file(path) -> QuantizedTensor:
+    """pack.cpp:347-471 read_file, with every check of the reference in its order."""
+    p = os.fsencode(path)
+    h = _abi.QTensor()
+    _check(lib().anyq_read_file_header(p, C.byref(h)))
+    qt = QuantizedTensor.empty(int(h.rows), int(h.cols), h.cfg)
+    qt.layout, qt.tile_k, qt.lut_store, qt.scale_store = h.layout, h.tile_k, h.lut_store, h.scale_store
+    c = qt.as_c()
+    _check(lib().anyq_read_file(p, C.byref(c)))
+    qt.cfg = _abi.Config.from_buffer_copy(bytes(c.cfg))
+    return qt
+
+
 def weight_error(w, qt: QuantizedTensor):
     """eval.cpp:11-29: (mse, relative Frobenius error) of dequantize(qt) against w."""
     w = _f32(w)
@@ -394,6 +418,17 @@ class DeviceTensor:
         _check(lib().anyq_dev_tensor_create(C.byref(c), C.byref(self._h)))
         self.rows, self.cols = qt.rows, qt.cols
         self.weight_bytes = int(lib().anyq_dev_tensor_weight_bytes(self._h))
+
+    @classmethod
+    def load(cls, path) -> "DeviceTensor":
+        """An ANYQ v1 file straight into the prepacked device layout (read_file's checks)."""
+        self = cls.__new__(cls)
+        self._h = C.c_void_p()
+        _check(lib().anyq_dev_tensor_load(os.fsencode(path), C.byref(self._h)))
+        self.rows = int(lib().anyq_dev_tensor_rows(self._h))
+        self.cols = int(lib().anyq_dev_tensor_cols(self._h))
+        self.weight_bytes = int(lib().anyq_dev_tensor_weight_bytes(self._h))
+        return self
 
     def close(self):
         if self._h:

@@ -596,6 +596,10 @@ anyq_status anyq_gemm_dense(const float* x, int64_t m, const float* w, int64_t n
 // ---------------------------------------------------------------------------
 // device-resident tensors + tensor-core GEMM (lutgemm.cu)
 // ---------------------------------------------------------------------------
+anyq_status anyq_dev_tensor_load(const char* path, anyq_dev_tensor** out) {
+  return guard([&] { *out = reinterpret_cast<anyq_dev_tensor*>(load_device_tensor(path)); });
+}
+
 anyq_status anyq_dev_tensor_create(const anyq_qtensor* qt, anyq_dev_tensor** out) {
   return guard([&] {
     check_qt(qt);

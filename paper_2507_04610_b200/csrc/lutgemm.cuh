@@ -33,6 +33,7 @@ struct LutTensor {
 };
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt);
+LutTensor* load_device_tensor(const char* path);  // ANYQ v1 file -> prepacked (anyq_file.cu)
 void lutgemm_destroy(LutTensor* t);
 void lutgemm_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null
 // K1a CUDA-core GEMV (m <= 4) over the same prepacked tensor (gemv.cu).
