@@ -12,6 +12,7 @@
 //                                                      qgemm.hpp:28-37
 //   compute_scales  scaling.hpp:52     scale_weights   scaling.hpp:56
 //   dequantize(values, s)  scaling.hpp:60
+//   write_file / read_file  pack.hpp (pack.cpp:293-471, ANYQ v1 files)
 //
 // Linking this object before the reference objects (tests/reftests/Makefile
 // weakens the latter) swaps the hot path of an unmodified reference build —
@@ -252,6 +253,54 @@ QuantizedTensor narrowed(const QuantizedTensor& qt) {
   CView v(out);
   check(anyq_narrow_inplace(&v.t));
   return out;
+}
+
+void write_file(const QuantizedTensor& qt, const std::string& path) {
+  validate(qt.cfg, qt.rows, qt.cols);
+  if (static_cast<Index>(qt.codes.size()) != qt.rows * packed_bytes_per_row(qt.cols, qt.cfg.bits))
+    throw ShapeError("write_file: packed code size does not match shape");
+  CView v(qt);
+  check(anyq_write_file(&v.t, path.c_str()));
+}
+
+QuantizedTensor read_file(const std::string& path) {
+  anyq_qtensor h;
+  std::memset(&h, 0, sizeof h);
+  check(anyq_read_file_header(path.c_str(), &h));
+  QuantizedTensor qt;  // fields the file does not store keep their defaults (pack.cpp:356)
+  qt.rows = h.rows;
+  qt.cols = h.cols;
+  qt.cfg.bits = h.cfg.bits;
+  qt.cfg.codebook = static_cast<CodebookKind>(h.cfg.codebook);
+  qt.cfg.granularity = static_cast<Granularity>(h.cfg.granularity);
+  qt.cfg.symmetric = h.cfg.symmetric != 0;
+  qt.cfg.int_range_shifted = h.cfg.int_range_shifted != 0;
+  qt.cfg.group_size = h.cfg.group_size;
+  qt.cfg.block_size = h.cfg.block_size;
+  qt.cfg.seed = h.cfg.seed;
+  qt.cfg.learner.init = static_cast<LutInit>(h.cfg.init);
+  qt.cfg.learner.weighting = static_cast<Weighting>(h.cfg.weighting);
+  qt.cfg.learner.max_iters = h.cfg.max_iters;
+  qt.cfg.learner.rel_tol = h.cfg.rel_tol;
+  qt.cfg.learner.restarts = h.cfg.restarts;
+  qt.layout = static_cast<Layout>(h.layout);
+  qt.tile_k = h.tile_k;
+  qt.lut_store = static_cast<Store16>(h.lut_store);
+  qt.scale_store = static_cast<Store16>(h.scale_store);
+  qt.codes.resize(static_cast<size_t>(qt.rows * packed_bytes_per_row(qt.cols, qt.cfg.bits)));
+  if (qt.cfg.codebook == CodebookKind::AnyN)
+    qt.luts.resize(static_cast<size_t>(qt.rows) << qt.cfg.bits);
+  qt.scales.granularity = qt.cfg.granularity;
+  qt.scales.rows = qt.rows;
+  qt.scales.cols = qt.cols;
+  qt.scales.group_size = qt.cfg.group_size;
+  qt.scales.block_size = qt.cfg.block_size;
+  qt.scales.symmetric = qt.cfg.symmetric;
+  qt.scales.alphas.resize(static_cast<Index>(h.num_groups));
+  qt.scales.betas.resize(static_cast<Index>(h.num_groups));
+  CView v(qt);  // the C-ABI fills qt's own arrays
+  check(anyq_read_file(path.c_str(), &v.t));
+  return qt;
 }
 
 Matf dequantize(const QuantizedTensor& qt) {
