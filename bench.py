@@ -648,6 +648,63 @@ def gpu_arm(args):
                            "stats": "synthetic E|x_j| ~ U(0.05, 1.05)",
                            "shapes": "q,k,v,o,gate,up (K=4096), down (K=14336)"}
 
+    # the rows around the path: E|x_j| of collect_stats, ANYQ v1
+    # file -> prepacked device tensor, weight_error / output_error; config-1
+    # shapes, rank 0 at P = 1 only (host-API calls, synchronous, wall clock)
+    around = None
+    if not args.quick and P == 1:
+        import tempfile
+
+        xa = torch.randn(4096, 4096, device=dev)
+        ex = torch.empty(4096, device=dev)
+        anyq.dev_column_mean_abs(xa, ex)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(5):
+            anyq.dev_column_mean_abs(xa, ex)
+        s1.record()
+        torch.cuda.synchronize()
+        st = s0.elapsed_time(s1) / 5 * 1e-3
+        qt1 = synthetic_qtensor(4096, 4096, seed=91)
+        with tempfile.TemporaryDirectory() as d:
+            fpath = os.path.join(d, "w.anyq")
+            t0 = time.perf_counter()
+            anyq.write_file(qt1, fpath)
+            tw = time.perf_counter() - t0
+            fbytes = os.path.getsize(fpath)
+            anyq.DeviceTensor.load(fpath).close()  # warm
+            t0 = time.perf_counter()
+            dtl = anyq.DeviceTensor.load(fpath)
+            torch.cuda.synchronize()
+            tl = time.perf_counter() - t0
+            dtl.close()
+        t0 = time.perf_counter()
+        anyq.DeviceTensor(qt1).close()  # same prepack from host arrays: what the load adds
+        torch.cuda.synchronize()
+        tc = time.perf_counter() - t0
+        wref = anyq.dequantize(qt1) + np.float32(1e-3)
+        xh16 = np.random.default_rng(3).standard_normal((16, 4096), dtype=np.float32)
+        anyq.weight_error(wref, qt1)
+        t0 = time.perf_counter()
+        anyq.weight_error(wref, qt1)
+        twe = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        anyq.output_error(wref, qt1, xh16)
+        toe = time.perf_counter() - t0
+        around = {
+            "stats_mean_abs_x": {"shape": "4096x4096 fp32, device-resident", "ms": round(st * 1e3, 3),
+                                 "GBps": round(4096 * 4096 * 4 / st / 1e9, 1),
+                                 "bound": "sequential FP64 add chain per channel (reference order)"},
+            "anyq_file_4096x4096_any4": {"bytes": fbytes, "write_ms": round(tw * 1e3, 2),
+                                         "load_to_device_ms": round(tl * 1e3, 2),
+                                         "load_GBps": round(fbytes / tl / 1e9, 2),
+                                         "prepack_from_host_arrays_ms": round(tc * 1e3, 2)},
+            "weight_error_ms": round(twe * 1e3, 2),
+            "output_error_m16_ms": round(toe * 1e3, 2),
+            "note": "host-API wall clock incl. H2D of the host arrays",
+        }
+
     # roofline of the dominant kernel: the step IS one k_lutgemv chain launch per
     # layer at M=1 (P=1), so its launch duration is the step time
     roof_achieved = value
@@ -712,6 +769,7 @@ def gpu_arm(args):
             "m_sweep": sweep,
             "kmeans": kmeans,
             "variants_q_shape": variants,
+            "around_the_path": around,
             "pct_hbm_peak_step": round(100 * value / peak, 2),
         }
         print(json.dumps(line), flush=True)
