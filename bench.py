@@ -91,7 +91,7 @@ class ClockSampler:
         0x0000000000000080: "hw_power_brake_slowdown",
     }
 
-    def __init__(self, dev_index=0, period=0.05):
+    def __init__(self, dev_index=0, period=0.002):
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self.period = period
