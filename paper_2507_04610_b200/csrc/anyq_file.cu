@@ -12,7 +12,6 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
-#include <iterator>
 #include <string>
 #include <vector>
 
@@ -117,9 +116,13 @@ int checked_enum(uint8_t raw, uint8_t max, const char* what) {
 }
 
 std::string slurp(const char* path) {
-  std::ifstream in(path, std::ios::binary);
+  std::ifstream in(path, std::ios::binary | std::ios::ate);
   if (!in) fail(ANYQ_ERR_IO, std::string("cannot open ANYQ file '") + path + "'");
-  return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  const std::streamoff n = in.tellg();
+  std::string buf(n > 0 ? (size_t)n : 0, '\0');
+  in.seekg(0);
+  if (n > 0 && !in.read(&buf[0], n)) fail(ANYQ_ERR_IO, std::string("cannot read ANYQ file '") + path + "'");
+  return buf;
 }
 
 // temp file + rename (io_util.hpp:62-79): no partial output survives an error
