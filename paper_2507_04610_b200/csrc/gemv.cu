@@ -61,7 +61,7 @@ constexpr int kW = 16;                // compute warps per CTA (one table slice 
 constexpr int kWriterWarp = kW;
 constexpr int kProducerWarp = kW + 1;
 constexpr int kT = (kW + 2) * 32;
-constexpr int kMaxMP = 4;
+constexpr int kMaxMP = 4;  // MP in {1, 2, 3, 4}: one template instance per x-row count
 constexpr int kStageChunks = kW;      // chunks per ring stage: one per compute warp
 constexpr uint32_t kStageBytes = kStageChunks * 2048u;
 constexpr uint32_t kStageAb = kStageChunks * 128u;
@@ -198,9 +198,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
-}
-__device__ __forceinline__ void cw_sync() {  // barrier of the kW compute warps
-  asm volatile("bar.sync 1, %0;" ::"n"(kW * 32) : "memory");
 }
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
@@ -811,6 +808,7 @@ void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs,
   if (n < 1 || !ts) fail(ANYQ_ERR_SHAPE, "empty GEMM chain");
   if (m == 1) launch_gv<1>(n, ts, xs, ys, y32s, deps, m, s);
   else if (m == 2) launch_gv<2>(n, ts, xs, ys, y32s, deps, m, s);
+  else if (m == 3) launch_gv<3>(n, ts, xs, ys, y32s, deps, m, s);
   else launch_gv<4>(n, ts, xs, ys, y32s, deps, m, s);
 }
 
@@ -823,6 +821,7 @@ bool lutgemv_fits(const LutTensor* t, int64_t m) {
   try {
     if (m == 1) plan_chain<1>(1, ts, xs, ys, nullptr, nullptr, m, P);
     else if (m == 2) plan_chain<2>(1, ts, xs, ys, nullptr, nullptr, m, P);
+    else if (m == 3) plan_chain<3>(1, ts, xs, ys, nullptr, nullptr, m, P);
     else plan_chain<4>(1, ts, xs, ys, nullptr, nullptr, m, P);
   } catch (const Failure&) {
     return false;
