@@ -263,6 +263,10 @@ anyq_status anyq_write_file(const anyq_qtensor* qt, const char* path) {
   return host_guard([&] {
     if (!qt || !path) fail(ANYQ_ERR_SHAPE, "null tensor or path");
     validate_config(qt->cfg, qt->rows, qt->cols);
+    if (!qt->codes || !qt->alphas || !qt->betas || (qt->cfg.codebook == ANYQ_CB_ANY && !qt->luts))
+      fail(ANYQ_ERR_SHAPE, "write_file: tensor arrays missing");
+    if (qt->num_groups != group_count(qt->cfg, qt->rows, qt->cols))
+      fail(ANYQ_ERR_SHAPE, "write_file: group count does not match the granularity");
     const int64_t ng = qt->num_groups;
     const uint64_t codes = (uint64_t)qt->rows * (uint64_t)packed_bpr(qt->cols, qt->cfg.bits);
     const uint64_t lut_entries = qt->cfg.codebook == ANYQ_CB_ANY ? (1ull << qt->cfg.bits) : 0ull;
