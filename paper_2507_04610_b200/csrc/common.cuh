@@ -32,6 +32,11 @@ void note_launch(int n = 1);
       ::anyq_b200::fail(ANYQ_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
   } while (0)
 
+// Raises a kernel's dynamic shared-memory limit to `bytes` once per (kernel,
+// device) — the attribute is per device, so a process driving several GPUs
+// configures each (capi.cu).
+void ensure_dyn_smem(const void* kernel, int bytes);
+
 #define ANYQ_LAUNCHED()                 \
   do {                                  \
     ::anyq_b200::note_launch();         \

@@ -763,12 +763,7 @@ void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* c
                float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
   GvParams P;
   const uint32_t smem_bytes = plan_chain<MP>(n, ts, xs, ys, y32s, deps, m, P);
-  static uint32_t configured = 0;
-  if (smem_bytes > configured) {
-    ANYQ_CUDA(cudaFuncSetAttribute(k_lutgemv<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_bytes));
-    configured = smem_bytes;
-  }
+  ensure_dyn_smem((const void*)k_lutgemv<MP>, (int)smem_bytes);
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;

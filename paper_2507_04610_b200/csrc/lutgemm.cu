@@ -757,12 +757,7 @@ void launch_mp(const LutTensor* t, const void* x, int64_t m, void* y, float* y32
   P.ncta = (int)std::min<int64_t>(t->sms, P.U);
   P.trace = g_trace;
   const int smem_bytes = CF::kSmem + 2 * t->C * MP * (int)sizeof(float);
-  static int configured = 0;
-  if (smem_bytes > configured) {
-    ANYQ_CUDA(cudaFuncSetAttribute(k_lutgemm<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_bytes));
-    configured = smem_bytes;
-  }
+  ensure_dyn_smem((const void*)k_lutgemm<MP>, smem_bytes);
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)P.ncta);
   lc.blockDim = dim3(kThreads);

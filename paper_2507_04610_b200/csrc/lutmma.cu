@@ -267,11 +267,7 @@ __global__ void k_lutmma_combine(const float* __restrict__ part, int S, int64_t 
 template <int NT>
 void launch_mma(const MmaArgs& A, int blocks, cudaStream_t s) {
   constexpr uint32_t smem = mma_smem_bytes<NT>();
-  static bool configured = false;
-  if (!configured) {
-    ANYQ_CUDA(cudaFuncSetAttribute(k_lutmma<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  ensure_dyn_smem((const void*)k_lutmma<NT>, (int)smem);
   k_lutmma<NT><<<blocks, mma_warps<NT>() * 32, smem, s>>>(A);
   ANYQ_LAUNCHED();
 }
