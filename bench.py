@@ -528,11 +528,12 @@ def gpu_arm(args):
             for d in ts70:
                 d.close()
 
-    # ---- M sweep (per-GEMM launches, AUTO path: GEMV for m = 1, tcgen05 above)
+    # ---- M sweep (per-GEMM launches, AUTO path: GEMV for m <= 4 while its x image fits,
+    # else tcgen05; fused mma for 5..32; dequant + cuBLAS above)
     sweep = {}
     tpeak = hbm_peak_tflops()
     if not args.quick and P == 1:
-        for mm in (1, 2, 4, 8, 16, 64, 256, 1024, 4096):
+        for mm in (1, 2, 3, 4, 8, 16, 32, 64, 256, 1024, 4096):
             xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in (D, FF)}
             for j, (name, n, k) in enumerate(LAYER):
                 if name not in ("q", "gate", "down"):
