@@ -32,16 +32,20 @@ __device__ __forceinline__ float fhfma_hi(uint32_t a, uint32_t b, float c) {
   return d;
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1) k_gemv8(float* out, uint32_t seed) {
+template <int M>
+__global__ void __launch_bounds__(kWarps * 32, 1) k_gemv(float* out, uint32_t seed) {
   __shared__ uint32_t tbl[256 * 32];
   const int lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) tbl[i] = 0x3c003c00u ^ (i * 2654435761u & 0x03ff03ffu);
   __syncthreads();
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(tbl) + lane * 4;
-  uint32_t x[8];
+  uint32_t x[M];
+  float acc[M];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) x[m] = 0x3c003c00u + m;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int m = 0; m < M; ++m) {
+    x[m] = 0x3c003c00u + m;
+    acc[m] = 0.0f;
+  }
   uint32_t s = seed ^ threadIdx.x;
   for (int it = 0; it < kIters; ++it) {
     s = s * 1664525u + 1013904223u;
@@ -51,14 +55,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_gemv8(float* out, uint32_t s
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
+      for (int m = 0; m < M; ++m) {
         acc[m] = fhfma_lo(t[b], x[m], acc[m]);
         acc[m] = fhfma_hi(t[b], x[m], acc[m]);
       }
   }
   float r = 0;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) r += acc[m];
+  for (int m = 0; m < M; ++m) r += acc[m];
   out[blockIdx.x * blockDim.x + threadIdx.x] = r;
 }
 
@@ -111,9 +115,13 @@ int main() {
   cudaMalloc(&out, 148 * kWarps * 32 * sizeof(float));
   const double per_sm = 1.0 / 148;
   // A: per lane per iteration 4 code bytes = 8 weights, x 8 tokens
-  float ms = time_it([&] { k_gemv8<<<148, kWarps * 32>>>(out, 1); });
+  float ms = time_it([&] { k_gemv<8><<<148, kWarps * 32>>>(out, 1); });
   double wt = 148.0 * kWarps * 32 * kIters * 8 * 8;
   printf("A gemv-style M=8 : %.3f ms  %.1f G weight*token/s per SM\n", ms, wt / (ms * 1e-3) * per_sm / 1e9);
+  ms = time_it([&] { k_gemv<1><<<148, kWarps * 32>>>(out, 1); });
+  wt = 148.0 * kWarps * 32 * kIters * 8;
+  printf("A gemv-style M=1 : %.3f ms  %.1f G weight*token/s per SM (x in registers: no broadcast loads)\n",
+         ms, wt / (ms * 1e-3) * per_sm / 1e9);
   // B/C: per warp per iteration one MMA = 16 rows x 16 k weights x 8 tokens
   wt = 148.0 * kWarps * kIters * 256 * 8;
   ms = time_it([&] { k_mma8<1><<<148, kWarps * 32>>>(out, 1); });
