@@ -105,7 +105,7 @@ float get_stored(const std::string& b, size_t off, int s) {
 }
 
 void need(const std::string& buf, uint64_t off, uint64_t len, const char* what) {
-  if (off + len > buf.size())
+  if (off > buf.size() || len > buf.size() - off)
     fail(ANYQ_ERR_TRUNCATED, std::string("ANYQ file truncated reading ") + what + " at offset " +
                                  std::to_string(off));
 }
@@ -205,8 +205,11 @@ Parsed parse_header(const std::string& buf) {
 }
 
 // Section contents into the caller's arrays, with read_file's value checks
-// (pack.cpp:403-470) in its order.
-void read_body(const std::string& buf, const Parsed& P, anyq_qtensor* q) {
+// (pack.cpp:403-470) in its order. The scales are checked from the file
+// bytes first: the header's group count is only trusted (and compared with
+// the caller's capacity `cap_groups`) once it matched the granularity, so a
+// corrupt count can never write past the caller's alpha/beta arrays.
+void read_body(const std::string& buf, const Parsed& P, anyq_qtensor* q, int64_t cap_groups) {
   const anyq_qtensor& h = P.h;
   std::memcpy(q->codes, buf.data() + P.codes_off, P.codes_len);
   const size_t w = store_width(h.scale_store);
@@ -214,14 +217,17 @@ void read_body(const std::string& buf, const Parsed& P, anyq_qtensor* q) {
   for (int64_t g = 0; g < ng; ++g) {
     const float a = get_stored(buf, P.scales_off + w * g, h.scale_store);
     const float b = get_stored(buf, P.scales_off + w * (ng + g), h.scale_store);
-    q->alphas[g] = a;
-    q->betas[g] = b;
     if (!(a > 0) || !std::isfinite(a)) fail(ANYQ_ERR_INVARIANT, "ANYQ file scale alpha must be positive and finite");
     if (!std::isfinite(b)) fail(ANYQ_ERR_INVARIANT, "ANYQ file scale beta must be finite");
     if (h.cfg.symmetric && b != 0) fail(ANYQ_ERR_INVARIANT, "ANYQ file symmetric tensor has nonzero beta");
   }
   if (ng != group_count(h.cfg, h.rows, h.cols))
     fail(ANYQ_ERR_INVARIANT, "ANYQ file group count does not match granularity");
+  if (ng > cap_groups) fail(ANYQ_ERR_SHAPE, "read_file: caller scale arrays are too small");
+  for (int64_t g = 0; g < ng; ++g) {
+    q->alphas[g] = get_stored(buf, P.scales_off + w * g, h.scale_store);
+    q->betas[g] = get_stored(buf, P.scales_off + w * (ng + g), h.scale_store);
+  }
   const size_t lw = store_width(h.lut_store);
   const int64_t nl = h.rows * (int64_t)P.lut_entries;
   for (int64_t i = 0; i < nl; ++i) {
@@ -333,7 +339,12 @@ anyq_status anyq_read_file(const char* path, anyq_qtensor* qt) {
     const Parsed P = parse_header(buf);
     if (!qt->codes || !qt->alphas || !qt->betas || (P.lut_entries && !qt->luts))
       fail(ANYQ_ERR_SHAPE, "read_file: caller arrays not allocated");
-    read_body(buf, P, qt);
+    // codes / LUT sizes follow from rows, cols and cfg, which the caller took
+    // from the header; the scale capacity is the caller's num_groups
+    if (qt->rows != P.h.rows || qt->cols != P.h.cols || qt->cfg.bits != P.h.cfg.bits ||
+        qt->cfg.codebook != P.h.cfg.codebook)
+      fail(ANYQ_ERR_SHAPE, "read_file: caller arrays were sized for a different header");
+    read_body(buf, P, qt, qt->num_groups);
     uint8_t* codes = qt->codes;
     float *luts = qt->luts, *alphas = qt->alphas, *betas = qt->betas;
     *qt = P.h;
@@ -358,7 +369,7 @@ LutTensor* load_device_tensor(const char* path) {
   q.luts = P.lut_entries ? luts.data() : nullptr;
   q.alphas = alphas.data();
   q.betas = betas.data();
-  read_body(buf, P, &q);
+  read_body(buf, P, &q, (int64_t)alphas.size());
   return lutgemm_create(&q);
 }
 }  // namespace anyq_b200

@@ -99,6 +99,10 @@ def test_reader_errors_match_reference(aq, orc, ref, tmp_path):
         "negative_alpha": patched(data, alpha0, (0xBC00).to_bytes(2, "little")),
         "unsorted_lut": patched(data, lut0, (0x7BFF).to_bytes(2, "little")),
         "fp4_code_15": patched(fp4_data, 120, b"\xff"),
+        # header group_size 64 -> 128: the declared group count (consistent with the
+        # section lengths) is twice what the granularity gives, so a reader that
+        # sizes its arrays from the granularity must not write the scales first
+        "fp4_group_count": patched(fp4_data, 24, (128).to_bytes(4, "little")),
     }
     for name, blob in cases.items():
         p = tmp_path / f"{name}.anyq"
