@@ -268,14 +268,25 @@ anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
 anyq_status anyq_dev_tensor_load(const char* path, anyq_dev_tensor** out);
 
 /* Device quantize: rows [row_offset, row_offset+rows) of a matrix, fp32 in,
- * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device. */
+ * reference-layout outputs (packed codes, fp32 LUT/alpha/beta) on device.
+ * Fully stream ordered (no host synchronisation; capturable into a CUDA
+ * graph). Argument/config errors return at once; the data checks of the
+ * reference (require_finite: NonFiniteError, the stats and KmProblem weight
+ * checks: StatsError) run on the device and are reported by
+ * anyq_dev_stream_status(stream). */
 anyq_status anyq_dev_quantize_any(const float* w_dev, int64_t rows, int64_t cols,
                                   const anyq_config* cfg, const float* exj_dev,
                                   int64_t row_offset, uint8_t* codes_dev,
                                   float* luts_dev, float* alphas_dev,
                                   float* betas_dev, void* stream);
 
-/* anyq_column_mean_abs on device buffers (validation syncs the stream once). */
+/* Synchronises `stream` and returns the first data error recorded on the
+ * device by the stream-ordered entries issued on it since the last call (in
+ * the reference's check order), clearing it; ANYQ_OK if none. */
+anyq_status anyq_dev_stream_status(void* stream);
+
+/* anyq_column_mean_abs on device buffers, stream ordered; a non-finite input
+ * is reported by anyq_dev_stream_status. */
 anyq_status anyq_dev_column_mean_abs(const float* x_dev, int64_t m, int64_t k, float* exj_dev,
                                      void* stream);
 

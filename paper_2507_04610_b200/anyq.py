@@ -144,6 +144,7 @@ def lib() -> C.CDLL:
         "anyq_weight_error": (st, [fptr, i64, i64, qt, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "anyq_output_error": (st, [fptr, i64, i64, qt, fptr, i64, i64, C.POINTER(C.c_double)]),
         "anyq_dev_column_mean_abs": (st, [vp, i64, i64, vp, vp]),
+        "anyq_dev_stream_status": (st, [vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -166,6 +167,7 @@ EXPORTED_SYMBOLS = (
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
     "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
     "anyq_write_file", "anyq_read_file_header", "anyq_read_file", "anyq_dev_tensor_load",
+    "anyq_dev_stream_status",
 )
 
 
@@ -514,8 +516,18 @@ def column_mean_abs(x) -> np.ndarray:
     return out
 
 
-def dev_column_mean_abs(x, out=None, stream=None):
-    """column_mean_abs on a contiguous fp32 CUDA tensor; returns the (K,) fp32 tensor."""
+def dev_stream_status(stream=None):
+    """Synchronise the stream and raise the first data error the stream-ordered
+    entries recorded on the device (anyq_dev_stream_status)."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().anyq_dev_stream_status(C.c_void_p(s.cuda_stream)))
+
+
+def dev_column_mean_abs(x, out=None, stream=None, check=True):
+    """column_mean_abs on a contiguous fp32 CUDA tensor; returns the (K,) fp32 tensor.
+    Stream ordered; check=True synchronises and raises a recorded data error."""
     import torch
 
     assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.dim() == 2
@@ -524,14 +536,17 @@ def dev_column_mean_abs(x, out=None, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
     _check(lib().anyq_dev_column_mean_abs(C.c_void_p(x.data_ptr()), x.shape[0], x.shape[1],
                                           C.c_void_p(out.data_ptr()), C.c_void_p(s.cuda_stream)))
+    if check:
+        dev_stream_status(s)
     return out
 
 
-def dev_quantize_any(w, cfg: Config, exj=None, row_offset: int = 0, stream=None):
+def dev_quantize_any(w, cfg: Config, exj=None, row_offset: int = 0, stream=None, check=True):
     """Device-resident quantize_any on torch CUDA tensors.
 
     Returns (codes uint8 [rows, bpr], luts f32 [rows, 2^bits], alphas, betas)
-    as torch tensors in the reference layout.
+    as torch tensors in the reference layout. Stream ordered (capturable);
+    check=True synchronises and raises a data error recorded on the device.
     """
     import torch
 
@@ -550,4 +565,6 @@ def dev_quantize_any(w, cfg: Config, exj=None, row_offset: int = 0, stream=None)
         C.c_void_p(exj.data_ptr()) if exj is not None else None, row_offset,
         C.c_void_p(codes.data_ptr()), C.c_void_p(luts.data_ptr()), C.c_void_p(alphas.data_ptr()),
         C.c_void_p(betas.data_ptr()), C.c_void_p(s.cuda_stream)))
+    if check:
+        dev_stream_status(s)
     return codes, luts, alphas, betas

@@ -122,6 +122,53 @@ int64_t group_count(const anyq_config& c, int64_t rows, int64_t cols) {
   fail(ANYQ_ERR_CONFIG, "unknown granularity");
 }
 
+// Per-(device, stream) workspace, allocated and zeroed once and never freed:
+// the GEMV chain's release counters (self-resetting, so launches on one stream
+// reuse them and launches on different streams never share them) and the
+// sticky stage error words of the stream-ordered entries (anyq_dev_*), read
+// and cleared by anyq_dev_stream_status.
+StreamWs stream_ws(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, StreamWs> table;
+  int dev = 0;
+  ANYQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = table.find({dev, s});
+  if (it != table.end()) return it->second;
+  StreamWs w{};
+  int* block = nullptr;
+  ANYQ_CUDA(cudaMalloc(&block, sizeof(int) * (kWsDone + kWsErr)));
+  // zeroed on a private stream: legal while another stream is being captured
+  cudaStream_t z;
+  ANYQ_CUDA(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking));
+  ANYQ_CUDA(cudaMemsetAsync(block, 0, sizeof(int) * (kWsDone + kWsErr), z));
+  ANYQ_CUDA(cudaStreamSynchronize(z));
+  ANYQ_CUDA(cudaStreamDestroy(z));
+  w.done = block;
+  w.err = block + kWsDone;
+  table.emplace(std::make_pair(dev, s), w);
+  return w;
+}
+
+// First recorded stage error of the stream (stage order = the reference's
+// check order), cleared; synchronises the stream.
+void check_stream_errors(cudaStream_t s, const char* what) {
+  const StreamWs w = stream_ws(s);
+  int h[kWsErr];
+  ANYQ_CUDA(cudaMemcpyAsync(h, w.err, sizeof h, cudaMemcpyDeviceToHost, s));
+  ANYQ_CUDA(cudaStreamSynchronize(s));
+  int first = ANYQ_OK;
+  for (int i = 0; i < kWsErr && first == ANYQ_OK; ++i) first = h[i];
+  if (first == ANYQ_OK) return;
+  ANYQ_CUDA(cudaMemsetAsync(w.err, 0, sizeof(int) * kWsErr, s));
+  ANYQ_CUDA(cudaStreamSynchronize(s));
+  const char* kind = first == ANYQ_ERR_NONFINITE  ? "non-finite value"
+                     : first == ANYQ_ERR_STATS    ? "negative, non-finite or all-zero weights/stats"
+                     : first == ANYQ_ERR_CODE_RANGE ? "code exceeds its value table"
+                                                    : "internal invariant violated";
+  fail((anyq_status)first, std::string(what) + ": " + kind);
+}
+
 void keep_default_pool() {
   static int done_dev = -1;
   int dev = 0;
@@ -187,41 +234,34 @@ static void table_range(const anyq_config& c, float* qmin, float* qmax) {
 }
 
 // Device-side quantize of rows (shared by the host and device entry points).
+// Stream ordered, no host synchronisation (graph capturable): the data checks
+// of the reference (require_finite, the stats check of build_sample_weights,
+// KmProblem::validate) record their status in the stream's stage error words,
+// one word per stage so the first failing stage wins as in the reference;
+// later stages run on whatever the failed stage left and their results are
+// discarded by the caller that checks (check_stream_errors).
 static void quantize_device(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg,
                             const float* exj, int64_t row_offset, uint8_t* packed, float* luts,
                             float* alphas, float* betas, cudaStream_t s) {
   validate_config(cfg, rows, cols);
   float qmin, qmax;
   table_range(cfg, &qmin, &qmax);
-  DevBuf<int> err(1, s);
-  ANYQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
-  launch_check_finite(w, rows * cols, err.p, ANYQ_ERR_NONFINITE, s);
-  ANYQ_CUDA(cudaStreamSynchronize(s));
-  check_device_error(err.p, cfg.codebook == ANYQ_CB_ANY ? "quantize_any" : "quantize_fixed");
+  int* err = stream_ws(s).err;
+  launch_check_finite(w, rows * cols, err + kErrFinite, ANYQ_ERR_NONFINITE, s);
   launch_scales(w, rows, cols, cfg, qmin, qmax, alphas, betas, s);
   DevBuf<float> ws(rows * cols, s), sw;
   DevBuf<uint8_t> codes(rows * cols, s);
   if (cfg.codebook == ANYQ_CB_ANY) {
-    if (exj) {
-      launch_check_stats(exj, cols, err.p, s);
-      ANYQ_CUDA(cudaStreamSynchronize(s));
-      check_device_error(err.p, "sample weights");
-    }
+    if (exj) launch_check_stats(exj, cols, err + kErrStats, s);
     sw.alloc(rows * cols, s);
-    launch_scale_rows(w, rows, cols, cfg, alphas, betas, exj, ws.p, sw.p, err.p, s);
-    ANYQ_CUDA(cudaStreamSynchronize(s));
-    check_device_error(err.p, "KmProblem");
-    launch_kmeans(ws.p, sw.p, rows, cols, cfg, row_offset, luts, codes.p, err.p, s);
+    launch_scale_rows(w, rows, cols, cfg, alphas, betas, exj, ws.p, sw.p, err + kErrRows, s);
+    launch_kmeans(ws.p, sw.p, rows, cols, cfg, row_offset, luts, codes.p, err + kErrLearn, s);
   } else {
-    launch_scale_rows(w, rows, cols, cfg, alphas, betas, nullptr, ws.p, nullptr, err.p, s);
-    ANYQ_CUDA(cudaStreamSynchronize(s));
-    check_device_error(err.p, "round_to_codebook");
+    launch_scale_rows(w, rows, cols, cfg, alphas, betas, nullptr, ws.p, nullptr, err + kErrRows, s);
     Table eff = effective_table(fixed_table(cfg), cfg.symmetric != 0);
     launch_round(ws.p, rows * cols, eff, codes.p, s);
   }
-  launch_pack(codes.p, rows, cols, cfg.bits, packed, err.p, s);
-  ANYQ_CUDA(cudaStreamSynchronize(s));
-  check_device_error(err.p, "quantize");
+  launch_pack(codes.p, rows, cols, cfg.bits, packed, err + kErrPack, s);
 }
 
 static void fill_header(anyq_qtensor* out, int64_t rows, int64_t cols, const anyq_config& cfg) {
@@ -321,6 +361,7 @@ anyq_status anyq_quantize_any(const float* w, int64_t rows, int64_t cols, const 
     DevBuf<float> luts(nl), alphas(ng), betas(ng);
     quantize_device(dw.p, rows, cols, *cfg, dexj.p, row_offset, packed.p, luts.p, alphas.p,
                     betas.p, s);
+    check_stream_errors(s, "quantize_any");
     fill_header(out, rows, cols, *cfg);
     packed.download(out->codes, nb);
     luts.download(out->luts, nl);
@@ -342,6 +383,7 @@ anyq_status anyq_quantize_fixed(const float* w, int64_t rows, int64_t cols, cons
     DevBuf<uint8_t> packed(nb);
     DevBuf<float> alphas(ng), betas(ng);
     quantize_device(dw.p, rows, cols, *cfg, nullptr, 0, packed.p, nullptr, alphas.p, betas.p, s);
+    check_stream_errors(s, "quantize_fixed");
     fill_header(out, rows, cols, *cfg);
     packed.download(out->codes, nb);
     alphas.download(out->alphas, ng);
@@ -358,6 +400,10 @@ anyq_status anyq_dev_quantize_any(const float* w_dev, int64_t rows, int64_t cols
     quantize_device(w_dev, rows, cols, *cfg, exj_dev, row_offset, codes_dev, luts_dev, alphas_dev,
                     betas_dev, (cudaStream_t)stream);
   });
+}
+
+anyq_status anyq_dev_stream_status(void* stream) {
+  return guard([&] { check_stream_errors((cudaStream_t)stream, "stream-ordered call"); });
 }
 
 anyq_status anyq_pack_codes(const uint8_t* codes, int64_t rows, int64_t cols, int32_t bits,
@@ -476,14 +522,12 @@ anyq_status anyq_dequantize_values(const float* v, int64_t rows, int64_t cols,
   return affine_host(v, rows, cols, cfg, alphas, betas, 0, out);
 }
 
+// Stream ordered; a non-finite input (require_finite: NonFiniteError) is
+// recorded in the stream's stage error words.
 static void column_mean_abs_device(const float* x, int64_t m, int64_t k, float* exj, cudaStream_t s) {
   if (m < 1) fail(ANYQ_ERR_SHAPE, "need at least one input sample");
   if (k < 0) fail(ANYQ_ERR_SHAPE, "negative channel count");
-  DevBuf<int> err(1, s);
-  ANYQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
-  launch_col_mean_abs(x, m, k, exj, err.p, s);
-  ANYQ_CUDA(cudaStreamSynchronize(s));
-  check_device_error(err.p, "collect_stats inputs");  // NonFiniteError as require_finite
+  launch_col_mean_abs(x, m, k, exj, stream_ws(s).err + kErrFinite, s);
 }
 
 anyq_status anyq_column_mean_abs(const float* x, int64_t m, int64_t k, float* exj) {
@@ -492,6 +536,7 @@ anyq_status anyq_column_mean_abs(const float* x, int64_t m, int64_t k, float* ex
     DevBuf<float> dx(m * k), de(k);
     dx.upload(x, m * k);
     column_mean_abs_device(dx.p, m, k, de.p, 0);
+    check_stream_errors(0, "collect_stats inputs");
     de.download(exj, k);
   });
 }

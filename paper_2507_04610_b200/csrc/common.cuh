@@ -43,6 +43,20 @@ void ensure_dyn_smem(const void* kernel, int bytes);
     ANYQ_CUDA(cudaGetLastError());      \
   } while (0)
 
+// Per-(device, stream) workspace (capi.cu): GEMV release counters and the
+// stage error words of the stream-ordered entries.
+constexpr int kWsDone = 8;  // GEMV chain release counters (one per problem)
+constexpr int kWsErr = 8;   // stage error words, checked in index order
+constexpr int kErrFinite = 0, kErrStats = 1, kErrRows = 2, kErrLearn = 3, kErrPack = 4,
+              kErrGemv = 5;
+struct StreamWs {
+  int* done;
+  int* err;
+};
+StreamWs stream_ws(cudaStream_t s);
+// Synchronises s; raises the first recorded stage error (and clears the words).
+void check_stream_errors(cudaStream_t s, const char* what);
+
 // Device-side error word: kernels atomicMax an anyq_status into it.
 __device__ __forceinline__ void dev_fail(int* err, int status) {
   if (err) atomicMax(err, status);

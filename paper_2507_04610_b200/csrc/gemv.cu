@@ -48,6 +48,8 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "kernels.cuh"
@@ -661,8 +663,8 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
   P.np = n;
   P.M = (int)m;
   P.ncta = ts[0]->gv_ncta;
-  P.err = ts[0]->gv_err;
-  P.done = ts[0]->gv_done;
+  P.err = nullptr;  // set per launch (stream workspace)
+  P.done = nullptr;
   P.trace = g_gv_trace;
   // dependencies, x images and the chain's item sequence
   int tot = 0;
@@ -763,6 +765,11 @@ void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* c
                float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
   GvParams P;
   const uint32_t smem_bytes = plan_chain<MP>(n, ts, xs, ys, y32s, deps, m, P);
+  // release counters of this stream: launches on one stream are ordered and
+  // leave them at zero; launches on other streams use their own
+  const StreamWs ws = stream_ws(s);
+  P.done = ws.done;
+  P.err = ws.err + kErrGemv;
   ensure_dyn_smem((const void*)k_lutgemv<MP>, (int)smem_bytes);
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -780,6 +787,37 @@ void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* c
   ANYQ_LAUNCHED();
 }
 
+// The pair table's address trick needs the dynamic shared-memory window to
+// start at kDynBase; probed once per device with a kernel of the same shape
+// (no static shared memory), so a toolchain or driver that moves it turns the
+// GEMV off (AUTO picks another path) instead of failing inside the kernel.
+__global__ void k_sbase_probe(uint32_t* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(smem);
+}
+
+bool gv_sbase_ok() {
+  static std::mutex mu;
+  static std::map<int, bool> ok;
+  int dev = 0;
+  ANYQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ok.find(dev);
+  if (it != ok.end()) return it->second;
+  uint32_t* d = nullptr;
+  uint32_t h = 0;
+  cudaStream_t z;
+  ANYQ_CUDA(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking));
+  ANYQ_CUDA(cudaMalloc(&d, sizeof(uint32_t)));
+  k_sbase_probe<<<1, 32, 4096, z>>>(d);
+  ANYQ_LAUNCHED();
+  ANYQ_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, z));
+  ANYQ_CUDA(cudaStreamSynchronize(z));
+  ANYQ_CUDA(cudaFree(d));
+  ANYQ_CUDA(cudaStreamDestroy(z));
+  return ok[dev] = (h == kDynBase);
+}
+
 }  // namespace
 
 void lutgemv_set_trace(long long* dev) { g_gv_trace = dev; }
@@ -791,16 +829,14 @@ void lutgemv_setup(LutTensor* t) {
   t->gv_gshift = -1;
   if (t->GR == 1) t->gv_gshift = 30;
   else if ((t->GC & (t->GC - 1)) == 0) t->gv_gshift = __builtin_ctz((unsigned)t->GC);
-  ANYQ_CUDA(cudaMalloc(&t->gv_err, sizeof(int)));
-  ANYQ_CUDA(cudaMemset(t->gv_err, 0, sizeof(int)));
-  ANYQ_CUDA(cudaMalloc(&t->gv_done, sizeof(int) * kMaxProb));
-  ANYQ_CUDA(cudaMemset(t->gv_done, 0, sizeof(int) * kMaxProb));
 }
 
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                        float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
   if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "LUT GEMV supports 1 <= m <= 4");
   if (n < 1 || !ts) fail(ANYQ_ERR_SHAPE, "empty GEMM chain");
+  if (!gv_sbase_ok())
+    fail(ANYQ_ERR_CONFIG, "LUT GEMV: dynamic shared memory does not start at 0x400 on this device");
   if (m == 1) launch_gv<1>(n, ts, xs, ys, y32s, deps, m, s);
   else if (m == 2) launch_gv<2>(n, ts, xs, ys, y32s, deps, m, s);
   else if (m == 3) launch_gv<3>(n, ts, xs, ys, y32s, deps, m, s);
@@ -808,7 +844,7 @@ void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs,
 }
 
 bool lutgemv_fits(const LutTensor* t, int64_t m) {
-  if (!t || m < 1 || m > kMaxMP || t->gv_gshift < 0) return false;
+  if (!t || m < 1 || m > kMaxMP || t->gv_gshift < 0 || !gv_sbase_ok()) return false;
   const LutTensor* ts[1] = {t};
   const void* xs[1] = {nullptr};
   void* ys[1] = {nullptr};

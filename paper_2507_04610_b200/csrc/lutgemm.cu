@@ -721,6 +721,12 @@ long long* g_trace = nullptr;
 template <int MP>
 void launch_mp(const LutTensor* t, const void* x, int64_t m, void* y, float* y32, cudaStream_t s) {
   using CF = Cfg<MP>;
+  // per-call workspace, stream ordered (concurrent calls on one tensor never share it)
+  DevBuf<__half> ximg((size_t)2 * t->C * 64 * 16, s);
+  DevBuf<float> xinv((size_t)t->C * kMaxMP, s), xsum((size_t)t->C * kMaxMP, s);
+  DevBuf<float> part((size_t)t->RB * t->cmax * kMaxMP * 32, s);
+  DevBuf<int> counters((size_t)t->RB, s);
+  ANYQ_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(int) * t->RB, s));
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -732,18 +738,18 @@ void launch_mp(const LutTensor* t, const void* x, int64_t m, void* y, float* y32
     lc.attrs = attr;
     lc.numAttrs = 1;
     ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_xprep<MP>, reinterpret_cast<const __nv_bfloat16*>(x), (int)m,
-                                 (int64_t)t->cols, t->ximg, t->xinv, t->xsum));
+                                 (int64_t)t->cols, ximg.p, xinv.p, xsum.p));
     ANYQ_LAUNCHED();
   }
   Params P;
   P.codes = t->codes;
   P.lut = t->lut;
   P.ab = t->ab;
-  P.ximg = t->ximg;
-  P.xinv = t->xinv;
-  P.xsum = t->xsum;
-  P.part = t->part;
-  P.counters = t->counters;
+  P.ximg = ximg.p;
+  P.xinv = xinv.p;
+  P.xsum = xsum.p;
+  P.part = part.p;
+  P.counters = counters.p;
   P.y = reinterpret_cast<__nv_bfloat16*>(y);
   P.y32 = y32;
   P.N = t->rows;
@@ -798,51 +804,69 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
     ANYQ_CUDA(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, dev));
     t->weight_bytes = rows * ((cols * 4 + 7) / 8) + ng * 4 + rows * 16 * 2;
 
+    // Prepack on a private stream: no legacy-stream or device-wide
+    // synchronisation, so creating a tensor never waits on other streams' work.
+    struct OwnStream {
+      cudaStream_t s = nullptr;
+      OwnStream() { ANYQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+      ~OwnStream() { cudaStreamDestroy(s); }
+    } own;
+    const cudaStream_t z = own.s;
+    auto h2d = [&](void* d, const void* h, size_t bytes) {
+      if (bytes) ANYQ_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, z));
+    };
     // logical row-major codes on device
     const int64_t nb = rows * packed_bpr(cols, c.bits);
-    DevBuf<uint8_t> dp(nb), logical(rows * cols), tmp;
-    dp.upload(qt->codes, nb);
-    launch_unpack(dp.p, rows, cols, c.bits, logical.p, 0);
+    DevBuf<uint8_t> dp(nb, z), logical(rows * cols, z), tmp;
+    h2d(dp.p, qt->codes, nb);
+    launch_unpack(dp.p, rows, cols, c.bits, logical.p, z);
     if (qt->layout == ANYQ_LAYOUT_KTILED) {
-      tmp.alloc(rows * cols);
-      launch_ktile(logical.p, rows, cols, qt->tile_k, 1, tmp.p, 0);
-      ANYQ_CUDA(cudaMemcpy(logical.p, tmp.p, rows * cols, cudaMemcpyDeviceToDevice));
+      tmp.alloc(rows * cols, z);
+      launch_ktile(logical.p, rows, cols, qt->tile_k, 1, tmp.p, z);
+      ANYQ_CUDA(cudaMemcpyAsync(logical.p, tmp.p, rows * cols, cudaMemcpyDeviceToDevice, z));
     }
-    DevBuf<int> err(1);
-    err.zero();
+    DevBuf<int> err(1, z);
+    ANYQ_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), z));
     Table fixed{};
     if (c.codebook != ANYQ_CB_ANY) {
       fixed = effective_table(fixed_table(c), c.symmetric != 0);
       if (fixed.n < 16) {
-        k_check_codes_below<<<148, 256>>>(logical.p, rows * cols, fixed.n, err.p);
+        k_check_codes_below<<<148, 256, 0, z>>>(logical.p, rows * cols, fixed.n, err.p);
         ANYQ_LAUNCHED();
       }
       for (int i = fixed.n; i < 16; ++i) fixed.v[i] = 0.0f;
     }
     ANYQ_CUDA(cudaMalloc(&t->codes, (size_t)t->RB * t->C * kChunkBytes));
-    k_prepack_codes<<<148 * 8, 256>>>(logical.p, rows, cols, t->RB, t->C, t->codes);
+    k_prepack_codes<<<148 * 8, 256, 0, z>>>(logical.p, rows, cols, t->RB, t->C, t->codes);
     ANYQ_LAUNCHED();
 
-    DevBuf<float> luts, table16(16), alphas(ng), betas(ng);
+    DevBuf<float> luts, table16(16, z), alphas(ng, z), betas(ng, z);
+    std::vector<float> l16;
     if (c.codebook == ANYQ_CB_ANY) {
       const int L = 1 << c.bits;
-      std::vector<float> l16((size_t)rows * 16, 0.0f);
+      l16.assign((size_t)rows * 16, 0.0f);
       for (int64_t r = 0; r < rows; ++r)
         for (int i = 0; i < L; ++i) l16[(size_t)r * 16 + i] = qt->luts[(size_t)r * L + i];
-      luts.alloc(rows * 16);
-      luts.upload(l16.data(), rows * 16);
+      luts.alloc(rows * 16, z);
+      h2d(luts.p, l16.data(), sizeof(float) * rows * 16);
     }
-    table16.upload(fixed.v, 16);
+    h2d(table16.p, fixed.v, sizeof(float) * 16);
     // scales in [row][GR] order (rowwise: GR == 1 per row)
-    alphas.upload(qt->alphas, ng);
-    betas.upload(qt->betas, ng);
+    h2d(alphas.p, qt->alphas, sizeof(float) * ng);
+    h2d(betas.p, qt->betas, sizeof(float) * ng);
     ANYQ_CUDA(cudaMalloc(&t->lut, sizeof(__half) * t->RB * 32 * 16));
     ANYQ_CUDA(cudaMalloc(&t->ab, sizeof(__half2) * t->RB * t->GR * 32));
-    k_prepack_scales<<<148, 256>>>(luts.p, table16.p, alphas.p, betas.p, rows, t->RB, t->GR, t->lut,
-                                   t->ab, err.p);
+    k_prepack_scales<<<148, 256, 0, z>>>(luts.p, table16.p, alphas.p, betas.p, rows, t->RB, t->GR,
+                                         t->lut, t->ab, err.p);
     ANYQ_LAUNCHED();
-    ANYQ_CUDA(cudaDeviceSynchronize());
-    check_device_error(err.p, "dev_tensor_create");
+    int herr = 0;
+    ANYQ_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof herr, cudaMemcpyDeviceToHost, z));
+    ANYQ_CUDA(cudaStreamSynchronize(z));
+    if (herr != ANYQ_OK)
+      fail((anyq_status)herr, herr == ANYQ_ERR_CODE_RANGE ? "dev_tensor_create: code exceeds its value table"
+                              : herr == ANYQ_ERR_IO        ? "dev_tensor_create: value overflows fp16"
+                              : herr == ANYQ_ERR_INVARIANT ? "dev_tensor_create: scale underflows fp16"
+                                                           : "dev_tensor_create: device check failed");
 
     // workspace
     const int64_t U = (int64_t)t->RB * t->C;
@@ -853,12 +877,6 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
       cmax = std::max(cmax, cta((int64_t)(rb + 1) * t->C - 1) - cta((int64_t)rb * t->C) + 1);
     }
     t->cmax = cmax;
-    ANYQ_CUDA(cudaMalloc(&t->ximg, sizeof(__half) * (size_t)2 * t->C * 64 * 16));
-    ANYQ_CUDA(cudaMalloc(&t->xinv, sizeof(float) * t->C * kMaxMP));
-    ANYQ_CUDA(cudaMalloc(&t->xsum, sizeof(float) * t->C * kMaxMP));
-    ANYQ_CUDA(cudaMalloc(&t->part, sizeof(float) * (size_t)t->RB * cmax * kMaxMP * 32));
-    ANYQ_CUDA(cudaMalloc(&t->counters, sizeof(int) * t->RB));
-    ANYQ_CUDA(cudaMemset(t->counters, 0, sizeof(int) * t->RB));
     lutgemv_setup(t);
   } catch (...) {
     lutgemm_destroy(t);
@@ -874,13 +892,6 @@ void lutgemm_destroy(LutTensor* t) {
   cudaFree(t->codes);
   cudaFree(t->lut);
   cudaFree(t->ab);
-  cudaFree(t->ximg);
-  cudaFree(t->xinv);
-  cudaFree(t->xsum);
-  cudaFree(t->part);
-  cudaFree(t->counters);
-  cudaFree(t->gv_err);
-  cudaFree(t->gv_done);
   delete t;
 }
 

@@ -18,17 +18,9 @@ struct LutTensor {
   uint8_t* codes = nullptr;  // [RB][C][4 quarters][32 rows][16 B]
   __half* lut = nullptr;     // [RB*32][16]
   __half2* ab = nullptr;     // [RB][GR][32] (alpha, beta)
-  // per-call workspace (one call in flight per tensor)
-  __half* ximg = nullptr;  // [2C steps][64 rows][16 k] canonical UMMA K-major images
-  float* xinv = nullptr;   // [C][16]  2^-e per (chunk, m)
-  float* xsum = nullptr;   // [C][16]  sum_k x per (chunk, m)
-  float* part = nullptr;   // [RB][cmax][16][32]
-  int* counters = nullptr; // [RB]
-  int cmax = 0;
+  int cmax = 0;  // tcgen05 path: most chunk ranges a row block is split into
   int sms = 148;
-  // CUDA-core GEMV (gemv.cu) work split + workspace
-  int* gv_err = nullptr;      // device error word of the GEMV
-  int* gv_done = nullptr;     // [8] chain completion counters (self-resetting)
+  // CUDA-core GEMV (gemv.cu) work split (its counters live per stream)
   int gv_ncta = 0, gv_gshift = -1;
 };
 

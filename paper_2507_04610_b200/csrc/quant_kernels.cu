@@ -87,38 +87,61 @@ __global__ void k_scales_rowgroup(const float* __restrict__ w, int64_t rows, int
   }
 }
 
-// Ordered 64-bit key for atomic (value, index) reductions: -0.0 and +0.0
-// compare equal (as the reference's float comparisons do) and ties break on
-// the smaller flat index.
+// Column / block / tensor granularity: atomic min/max over an order-preserving
+// 32-bit key of the value (-0.0 and +0.0 share a key, as the reference's
+// float comparisons treat them equal). Only the two zeros are distinct floats
+// with one key, so a second pass finds the FIRST zero (64-bit flat index) of
+// groups whose extreme is zero: the reference keeps the first of equal values.
 __device__ __forceinline__ uint32_t ordered(float v) {
   uint32_t u = __float_as_uint(v == 0.0f ? 0.0f : v);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+__device__ __forceinline__ float unordered(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
 
 __global__ void k_scales_atomic(const float* __restrict__ w, int64_t rows, int64_t cols,
-                                GroupMap gm, unsigned long long* __restrict__ kmin,
-                                unsigned long long* __restrict__ kmax) {
-  int64_t n = rows * cols;
+                                GroupMap gm, uint32_t* __restrict__ kmin,
+                                uint32_t* __restrict__ kmax) {
+  const int64_t n = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = e / cols, j = e % cols;
-    int64_t g = gm(i, j);
-    uint32_t o = ordered(w[e]);
-    atomicMin(&kmin[g], ((unsigned long long)o << 32) | (uint32_t)e);
-    atomicMax(&kmax[g], ((unsigned long long)o << 32) | (0xFFFFFFFFu - (uint32_t)e));
+    const int64_t i = e / cols, j = e % cols;
+    const int64_t g = gm(i, j);
+    const uint32_t o = ordered(w[e]);
+    atomicMin(&kmin[g], o);
+    atomicMax(&kmax[g], o);
+  }
+}
+
+__global__ void k_scales_first_zero(const float* __restrict__ w, int64_t rows, int64_t cols,
+                                    GroupMap gm, const uint32_t* __restrict__ kmin,
+                                    const uint32_t* __restrict__ kmax,
+                                    unsigned long long* __restrict__ zmin,
+                                    unsigned long long* __restrict__ zmax) {
+  const int64_t n = rows * cols;
+  const uint32_t kz = ordered(0.0f);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (w[e] != 0.0f) continue;
+    const int64_t g = gm(e / cols, e % cols);
+    if (kmin[g] == kz) atomicMin(&zmin[g], (unsigned long long)e);
+    if (kmax[g] == kz) atomicMin(&zmax[g], (unsigned long long)e);
   }
 }
 
 __global__ void k_scales_finish(const float* __restrict__ w, int64_t ng,
-                                const unsigned long long* __restrict__ kmin,
-                                const unsigned long long* __restrict__ kmax, bool symmetric,
+                                const uint32_t* __restrict__ kmin, const uint32_t* __restrict__ kmax,
+                                const unsigned long long* __restrict__ zmin,
+                                const unsigned long long* __restrict__ zmax, bool symmetric,
                                 float qmin, float qmax, float* alphas, float* betas) {
-  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
-  uint32_t imn = (uint32_t)(kmin[g] & 0xFFFFFFFFull);
-  uint32_t imx = 0xFFFFFFFFu - (uint32_t)(kmax[g] & 0xFFFFFFFFull);
+  const uint32_t kz = ordered(0.0f);
+  const float mn = kmin[g] == kz ? w[zmin[g]] : unordered(kmin[g]);
+  const float mx = kmax[g] == kz ? w[zmax[g]] : unordered(kmax[g]);
   float a, b;
-  alpha_beta(w[imn], w[imx], symmetric, qmin, qmax, &a, &b);
+  alpha_beta(mn, mx, symmetric, qmin, qmax, &a, &b);
   alphas[g] = a;
   betas[g] = b;
 }
@@ -353,18 +376,23 @@ void launch_scales(const float* w, int64_t rows, int64_t cols, const anyq_config
     ANYQ_LAUNCHED();
     return;
   }
-  if (rows * cols >= (int64_t(1) << 32)) fail(ANYQ_ERR_SHAPE, "tensor too large for scale reduction");
   int64_t ng = group_count(cfg, rows, cols);
-  DevBuf<unsigned long long> kmin(ng), kmax(ng);
-  ANYQ_CUDA(cudaMemsetAsync(kmin.p, 0xFF, sizeof(unsigned long long) * ng, s));
-  ANYQ_CUDA(cudaMemsetAsync(kmax.p, 0x00, sizeof(unsigned long long) * ng, s));
+  DevBuf<uint32_t> kmin(ng, s), kmax(ng, s);
+  DevBuf<unsigned long long> zmin(ng, s), zmax(ng, s);
+  ANYQ_CUDA(cudaMemsetAsync(kmin.p, 0xFF, sizeof(uint32_t) * ng, s));
+  ANYQ_CUDA(cudaMemsetAsync(kmax.p, 0x00, sizeof(uint32_t) * ng, s));
+  ANYQ_CUDA(cudaMemsetAsync(zmin.p, 0xFF, sizeof(unsigned long long) * ng, s));
+  ANYQ_CUDA(cudaMemsetAsync(zmax.p, 0xFF, sizeof(unsigned long long) * ng, s));
   k_scales_atomic<<<grid_for(rows * cols), 256, 0, s>>>(w, rows, cols, gm, kmin.p, kmax.p);
   ANYQ_LAUNCHED();
-  k_scales_finish<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(w, ng, kmin.p, kmax.p,
+  k_scales_first_zero<<<grid_for(rows * cols), 256, 0, s>>>(w, rows, cols, gm, kmin.p, kmax.p,
+                                                            zmin.p, zmax.p);
+  ANYQ_LAUNCHED();
+  k_scales_finish<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(w, ng, kmin.p, kmax.p, zmin.p, zmax.p,
                                                               cfg.symmetric != 0, qmin, qmax,
                                                               alphas, betas);
   ANYQ_LAUNCHED();
-  ANYQ_CUDA(cudaStreamSynchronize(s));  // scratch freed on return
+  // scratch is released stream-ordered on return (no host synchronisation)
 }
 
 void launch_scale_rows(const float* w, int64_t rows, int64_t cols, const anyq_config& cfg,
