@@ -290,6 +290,71 @@ anyq_status anyq_dev_stream_status(void* stream);
 anyq_status anyq_dev_column_mean_abs(const float* x_dev, int64_t m, int64_t k, float* exj_dev,
                                      void* stream);
 
+/* ---------------------------------------------------------------------------
+ * The per-row learner API, codebooks, scalar narrowing, accounting (host
+ * buffers). With these the C++ drop-in (host/anyq_host.cpp) serves every
+ * function of the reference's hot-path headers from this library.
+ * ------------------------------------------------------------------------- */
+
+/* learner.hpp:55 kmeans_pp_init (mode 2), learner.hpp:61 weighted_kmeans
+ * (mode 1) and learner.hpp:66 learn_row_lut (mode 0: centroids = the sorted
+ * LUT widened to double, assignments = the rank-remapped codes, loss) on the
+ * GPU, for `rows` independent KmProblems of n samples each
+ * (samples / weights row-major). rng_key[r], rng_counter[r] are problem r's
+ * Rng state (core.hpp:164-192); the counter is advanced in place exactly as
+ * the reference advances its Rng&. Every reduction runs in the reference's
+ * sample-index order, so results are bit-identical by construction.
+ * Outputs: centroids [rows][k] (learner order, double); mode 1 also
+ * assignments [rows][n] (centroid indices), loss [rows], iters [rows].
+ * cfg supplies the LearnerConfig fields (init, max_iters, rel_tol, restarts).
+ * Errors as KmProblem::validate + the k checks (learner.cpp:11-23, 133, 318-319). */
+anyq_status anyq_kmeans_problems(const float* samples, const float* weights, int64_t rows,
+                                 int64_t n, int32_t k, const anyq_config* cfg, int32_t mode,
+                                 const uint64_t* rng_key, uint64_t* rng_counter,
+                                 double* centroids, uint8_t* assignments, double* loss,
+                                 int32_t* iters);
+
+/* learner.hpp:45 build_sample_weights(s, row, stats, mode) for the scale set
+ * (cfg granularity, rows x cols, alphas[num_groups]); stats may be NULL
+ * (E|x_j| = 1). StatsError on a stats length mismatch or a negative /
+ * non-finite entry (learner.cpp:27-34). out: cols floats. */
+anyq_status anyq_build_sample_weights(const anyq_config* cfg, int64_t rows, int64_t cols,
+                                      const float* alphas, int64_t num_groups, int64_t row,
+                                      const float* stats, int64_t stats_len, int32_t weighting,
+                                      float* out);
+
+/* codebooks.hpp:44 round_to_codebook(ws, cb): nearest of the n sorted table
+ * values, ties to the smaller index (NonFiniteError on non-finite ws). */
+anyq_status anyq_round_to_table(const float* ws, int64_t rows, int64_t cols, const float* table,
+                                int32_t n, uint8_t* codes);
+
+/* pack.hpp:95 scaled_values(qt): the table value of every code (rows x cols). */
+anyq_status anyq_scaled_values(const anyq_qtensor* qt, float* out);
+
+/* codebooks.hpp:27-38 int_grid(bits, shifted) / fp4_table() / nf4_table():
+ * the nominal table of a fixed codebook kind (values[<= 256], *n entries). */
+anyq_status anyq_fixed_table(int32_t codebook, int32_t bits, int32_t shifted, float* values,
+                             int32_t* n);
+
+/* pack.hpp:57-60 RNE narrowing: NonFiniteError on non-finite input, IoError on
+ * overflow to infinity; widening is exact. */
+anyq_status anyq_f32_to_f16(float f, uint16_t* out);
+float anyq_f16_to_f32(uint16_t h);
+anyq_status anyq_f32_to_bf16(float f, uint16_t* out);
+float anyq_bf16_to_f32(uint16_t h);
+
+/* codebooks.hpp:50 storage_bits_per_entry(cfg, rows, cols). */
+anyq_status anyq_storage_bits_per_entry(const anyq_config* cfg, int64_t rows, int64_t cols,
+                                        double* bits);
+
+/* qgemm.hpp:55 bench's timing loop on the device: `repeats` runs (after one
+ * warm-up) of one GEMM with operands resident in HBM, each timed with CUDA
+ * events; ns[r] = run r in nanoseconds. kind 0: fp32 gemm_dense(x, w) (w is
+ * n x k, qt unused); 1: the bit-exact gemm_fused kernel on qt; 2: the A16W4
+ * LUT GEMM on the prepacked tensor (bf16 x, the AUTO kernel for m). */
+anyq_status anyq_bench_gemm(int32_t kind, const anyq_qtensor* qt, const float* w, int64_t n,
+                            int64_t k, const float* x, int64_t m, int32_t repeats, double* ns);
+
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches accounting). */
 uint64_t anyq_launch_count(void);

@@ -145,6 +145,19 @@ def lib() -> C.CDLL:
         "anyq_output_error": (st, [fptr, i64, i64, qt, fptr, i64, i64, C.POINTER(C.c_double)]),
         "anyq_dev_column_mean_abs": (st, [vp, i64, i64, vp, vp]),
         "anyq_dev_stream_status": (st, [vp]),
+        "anyq_kmeans_problems": (st, [fptr, fptr, i64, i64, i32, cfg, i32, vp, vp,
+                                      C.POINTER(C.c_double), u8, C.POINTER(C.c_double),
+                                      C.POINTER(i32)]),
+        "anyq_build_sample_weights": (st, [cfg, i64, i64, fptr, i64, i64, fptr, i64, i32, fptr]),
+        "anyq_round_to_table": (st, [fptr, i64, i64, fptr, i32, u8]),
+        "anyq_scaled_values": (st, [qt, fptr]),
+        "anyq_fixed_table": (st, [i32, i32, i32, fptr, C.POINTER(i32)]),
+        "anyq_f32_to_f16": (st, [C.c_float, C.POINTER(C.c_uint16)]),
+        "anyq_f16_to_f32": (C.c_float, [C.c_uint16]),
+        "anyq_f32_to_bf16": (st, [C.c_float, C.POINTER(C.c_uint16)]),
+        "anyq_bf16_to_f32": (C.c_float, [C.c_uint16]),
+        "anyq_storage_bits_per_entry": (st, [cfg, i64, i64, C.POINTER(C.c_double)]),
+        "anyq_bench_gemm": (st, [i32, qt, fptr, i64, i64, fptr, i64, i32, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -167,7 +180,10 @@ EXPORTED_SYMBOLS = (
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
     "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
     "anyq_write_file", "anyq_read_file_header", "anyq_read_file", "anyq_dev_tensor_load",
-    "anyq_dev_stream_status",
+    "anyq_dev_stream_status", "anyq_kmeans_problems", "anyq_build_sample_weights",
+    "anyq_round_to_table", "anyq_scaled_values", "anyq_fixed_table", "anyq_f32_to_f16",
+    "anyq_f16_to_f32", "anyq_f32_to_bf16", "anyq_bf16_to_f32", "anyq_storage_bits_per_entry",
+    "anyq_bench_gemm",
 )
 
 
@@ -206,10 +222,116 @@ def format_name(cfg: Config) -> str:
 
 
 def storage_bits_per_entry(cfg: Config, rows: int, cols: int) -> float:
-    """codebooks.cpp:99-121 (pure arithmetic on the config)."""
-    groups = _abi.num_groups(cfg, rows, cols)
-    lut_bits = rows * (1 << cfg.bits) * 16.0 if cfg.codebook == CB_ANY else 0.0
-    return cfg.bits + (groups * 2.0 * 16.0 + lut_bits) / (float(rows) * float(cols))
+    """codebooks.cpp:99-121 storage_bits_per_entry (anyq_storage_bits_per_entry)."""
+    out = C.c_double()
+    _check(lib().anyq_storage_bits_per_entry(C.byref(cfg), rows, cols, C.byref(out)))
+    return out.value
+
+
+def fixed_table(codebook: int, bits: int = 4, shifted: bool = False) -> np.ndarray:
+    """codebooks.cpp:8-55 int_grid / fp4_table / nf4_table (nominal values)."""
+    v = np.empty(256, np.float32)
+    n = C.c_int32()
+    _check(lib().anyq_fixed_table(codebook, bits, int(shifted), _abi.fp(v), C.byref(n)))
+    return v[: n.value].copy()
+
+
+def round_to_codebook(ws, table) -> np.ndarray:
+    """codebooks.cpp:75-97 round_to_codebook on the GPU (ties to the lower index)."""
+    ws = _f32(ws)
+    t = _f32(table).ravel()
+    codes = np.empty(ws.shape, np.uint8)
+    _check(lib().anyq_round_to_table(_abi.fp(ws), ws.shape[0], ws.shape[1], _abi.fp(t), t.size,
+                                     _abi.u8p(codes)))
+    return codes
+
+
+def f32_to_f16(f: float) -> int:
+    """pack.cpp:61-101 RNE narrowing (NonFiniteError / IoError on overflow)."""
+    h = C.c_uint16()
+    _check(lib().anyq_f32_to_f16(C.c_float(f), C.byref(h)))
+    return h.value
+
+
+def f32_to_bf16(f: float) -> int:
+    h = C.c_uint16()
+    _check(lib().anyq_f32_to_bf16(C.c_float(f), C.byref(h)))
+    return h.value
+
+
+def f16_to_f32(h: int) -> float:
+    return lib().anyq_f16_to_f32(h)
+
+
+def bf16_to_f32(h: int) -> float:
+    return lib().anyq_bf16_to_f32(h)
+
+
+# ---------------------------------------------------------------------------
+# the per-row learner (learner.hpp:30-68) on the GPU
+# ---------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def rng_for_row(seed: int, row: int) -> list:
+    """core.hpp:196-200: the Rng state [key, counter] of stream (seed, row)."""
+    return [_splitmix64(seed) ^ _splitmix64((0x9E3779B97F4A7C15 * (row + 1)) & _M64), 0]
+
+
+def _km(x, w, k, cfg: Config | None, mode: int, rng):
+    x = np.ascontiguousarray(x, np.float32).ravel()
+    w = np.ascontiguousarray(w, np.float32).ravel()
+    if x.size != w.size:
+        raise ShapeError("KmProblem: samples and weights differ in length")
+    c = cfg if cfg is not None else _abi.default_config(codebook=CB_ANY)
+    key = np.array([rng[0]], np.uint64)
+    ctr = np.array([rng[1]], np.uint64)
+    cen = np.empty(max(k, 1), np.float64)
+    asg = np.empty(max(x.size, 1), np.uint8)
+    loss = C.c_double()
+    iters = C.c_int32()
+    _check(lib().anyq_kmeans_problems(
+        _abi.fp(x), _abi.fp(w), 1, x.size, k, C.byref(c), mode,
+        key.ctypes.data_as(C.c_void_p), ctr.ctypes.data_as(C.c_void_p), _abi.f64p(cen),
+        _abi.u8p(asg), C.byref(loss), C.byref(iters)))
+    rng[1] = int(ctr[0])
+    return cen[:k], asg[:x.size], loss.value, iters.value
+
+
+def kmeans_pp_init(x, w, k: int, rng) -> np.ndarray:
+    """learner.hpp:55 kmeans_pp_init; `rng` = [key, counter] (advanced in place)."""
+    return _km(x, w, k, None, 2, rng)[0]
+
+
+def weighted_kmeans(x, w, k: int, cfg: Config, rng):
+    """learner.hpp:61 weighted_kmeans -> (centroids f64, assignments, loss, iters)."""
+    return _km(x, w, k, cfg, 1, rng)
+
+
+def learn_row_lut(x, w, bits: int, cfg: Config, rng):
+    """learner.hpp:66 learn_row_lut -> (sorted LUT f32, codes, loss)."""
+    cen, codes, loss, _ = _km(x, w, 1 << bits, cfg, 0, rng)
+    return cen.astype(np.float32), codes, loss
+
+
+def build_sample_weights(cfg: Config, rows: int, cols: int, alphas, row: int, stats=None,
+                         weighting: int | None = None) -> np.ndarray:
+    """learner.hpp:45 build_sample_weights for the scale set (cfg's group map)."""
+    a = _f32(alphas).ravel()
+    st = None if stats is None else _f32(stats).ravel()
+    out = np.empty(cols, np.float32)
+    mode = cfg.weighting if weighting is None else weighting
+    _check(lib().anyq_build_sample_weights(
+        C.byref(cfg), rows, cols, _abi.fp(a), a.size, row, None if st is None else _abi.fp(st),
+        0 if st is None else st.size, mode, _abi.fp(out)))
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -303,6 +425,31 @@ def narrowed(qt: QuantizedTensor) -> QuantizedTensor:
     c = out.as_c()
     _check(lib().anyq_narrow_inplace(C.byref(c)))
     return out
+
+
+def scaled_values(qt: QuantizedTensor) -> np.ndarray:
+    """pack.cpp:205-236: the table value of every code (before alpha / beta)."""
+    out = np.empty((qt.rows, qt.cols), np.float32)
+    c = qt.as_c()
+    _check(lib().anyq_scaled_values(C.byref(c), _abi.fp(out)))
+    return out
+
+
+def bench_gemm(kind: int, qt: QuantizedTensor | None, w, x, repeats: int) -> np.ndarray:
+    """qgemm.cpp bench's timing loop on the device (anyq_bench_gemm): per-run ns.
+    kind 0: fp32 gemm_dense(x, w); 1: exact gemm_fused on qt; 2: A16W4 LUT GEMM."""
+    x = _f32(x)
+    ns = np.empty(repeats, np.float64)
+    if kind == 0:
+        w = _f32(w)
+        n, k = w.shape
+        _check(lib().anyq_bench_gemm(0, None, _abi.fp(w), n, k, _abi.fp(x), x.shape[0], repeats,
+                                     _abi.f64p(ns)))
+    else:
+        c = qt.as_c()
+        _check(lib().anyq_bench_gemm(kind, C.byref(c), None, qt.rows, qt.cols, _abi.fp(x),
+                                     x.shape[0], repeats, _abi.f64p(ns)))
+    return ns
 
 
 def dequantize(qt: QuantizedTensor) -> np.ndarray:

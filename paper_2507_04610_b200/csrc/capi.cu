@@ -223,6 +223,22 @@ static anyq_status guard(F&& f) {
   }
 }
 
+// Host-only helpers (tables, scalar narrowing, accounting) need no device.
+template <typename F>
+static anyq_status host_only(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return ANYQ_OK;
+  } catch (const Failure& e) {
+    g_last_error = e.msg;
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ANYQ_ERR_INTERNAL;
+  }
+}
+
 // qmin/qmax of the quantizer (learner.cpp:401, quantize.cpp:12)
 static void table_range(const anyq_config& c, float* qmin, float* qmax) {
   Table t = c.codebook == ANYQ_CB_ANY ? int_grid_table(c.bits, c.int_range_shifted != 0)
@@ -547,7 +563,9 @@ anyq_status anyq_dev_column_mean_abs(const float* x_dev, int64_t m, int64_t k, f
 }
 
 // dequantize(qt) into a device buffer (shared by dequantize and the eval metrics)
-static void dequant_to_device(const anyq_qtensor* qt, DevTensorArrays& t, float* w_dev) {
+// (values_only: the scaled-domain table values, scaled_values pack.cpp:205-236)
+static void dequant_to_device(const anyq_qtensor* qt, DevTensorArrays& t, float* w_dev,
+                              bool values_only = false) {
   t.upload(qt);
   Table fixed{};
   if (qt->cfg.codebook != ANYQ_CB_ANY)
@@ -555,7 +573,8 @@ static void dequant_to_device(const anyq_qtensor* qt, DevTensorArrays& t, float*
   DevBuf<int> err(1);
   err.zero();
   launch_dequant(t.codes.p, qt->rows, qt->cols, qt->cfg.bits, qt->layout == ANYQ_LAYOUT_KTILED,
-                 qt->tile_k, t.luts.p, fixed, qt->cfg, t.alphas.p, t.betas.p, w_dev, err.p, 0);
+                 qt->tile_k, t.luts.p, fixed, qt->cfg, values_only ? nullptr : t.alphas.p,
+                 t.betas.p, w_dev, err.p, 0);
   check_device_error(err.p, "dequantize");
 }
 
@@ -741,6 +760,252 @@ anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
 anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                void* y_bf16, float* y_f32, void* stream) {
   return anyq_dev_gemm_bf16_path(t, x_bf16, m, y_bf16, y_f32, ANYQ_PATH_AUTO, stream);
+}
+
+// ---------------------------------------------------------------------------
+// The per-row learner API, codebooks, scalar narrowing and accounting
+// (learner.hpp:45-68, codebooks.hpp:27-50, pack.hpp:57-96): the entry points
+// the C++ drop-in (host/anyq_host.cpp) serves the rest of the reference API with.
+// ---------------------------------------------------------------------------
+
+anyq_status anyq_kmeans_problems(const float* samples, const float* weights, int64_t rows, int64_t n,
+                                 int32_t k, const anyq_config* cfg, int32_t mode,
+                                 const uint64_t* rng_key, uint64_t* rng_counter, double* centroids,
+                                 uint8_t* assignments, double* loss, int32_t* iters) {
+  return guard([&] {
+    if (mode < 0 || mode > 2) fail(ANYQ_ERR_CONFIG, "k-means mode must be 0, 1 or 2");
+    if (rows < 1) return;
+    // KmProblem::validate (learner.cpp:11-23), then the k checks, in order
+    if (n < 1) fail(ANYQ_ERR_SHAPE, "KmProblem: empty problem");
+    for (int64_t r = 0; r < rows; ++r) {
+      const float* w = weights + r * n;
+      bool any_positive = false;
+      for (int64_t i = 0; i < n; ++i) {
+        if (!(w[i] >= 0) || !std::isfinite(w[i])) fail(ANYQ_ERR_STATS, "KmProblem: weights must be >= 0");
+        any_positive |= w[i] > 0;
+      }
+      if (!any_positive) fail(ANYQ_ERR_STATS, "KmProblem: all sample weights are zero");
+      for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(samples[r * n + i])) fail(ANYQ_ERR_NONFINITE, "KmProblem: non-finite sample");
+    }
+    if (k < 1) fail(ANYQ_ERR_CONFIG, "k must be >= 1");
+    if (mode != 2 && k > 256) fail(ANYQ_ERR_CONFIG, "k must fit an 8-bit code");
+    if (mode == 2 && k > 256) fail(ANYQ_ERR_CONFIG, "k-means++ seeding supports k <= 256");
+    if (mode != 2 && cfg->init == ANYQ_INIT_NF4 && k != 16)
+      fail(ANYQ_ERR_CONFIG, "nf4 seeding needs exactly 16 centroids");
+    if (mode != 2 && (cfg->max_iters < 1 || cfg->restarts < 1))
+      fail(ANYQ_ERR_CONFIG, "learner needs max_iters >= 1 and restarts >= 1");
+    cudaStream_t s = 0;
+    DevBuf<float> dx(rows * n), dw(rows * n), dlut(mode == 0 ? rows * k : 0);
+    DevBuf<uint64_t> dkey(rows), dctr(rows);
+    DevBuf<double> dcen(rows * k), dloss(rows);
+    DevBuf<uint8_t> dasg(mode != 2 ? rows * n : 0);
+    DevBuf<int> diters(rows);
+    dx.upload(samples, rows * n);
+    dw.upload(weights, rows * n);
+    dkey.upload(rng_key, rows);
+    dctr.upload(rng_counter, rows);
+    int* err = stream_ws(s).err;
+    launch_kmeans_problems(dx.p, dw.p, rows, n, k, *cfg, mode, dkey.p, dctr.p, dcen.p, dasg.p,
+                           dloss.p, diters.p, dlut.p, dasg.p, err + kErrLearn, s);
+    check_stream_errors(s, "weighted_kmeans");
+    dctr.download(rng_counter, rows);
+    if (mode == 0) {  // learn_row_lut: sorted LUT (as float) + rank codes + loss
+      std::vector<float> lut(rows * k);
+      dlut.download(lut.data(), rows * k);
+      for (int64_t i = 0; i < rows * k; ++i) centroids[i] = lut[i];
+      dasg.download(assignments, rows * n);
+      dloss.download(loss, rows);
+      return;
+    }
+    dcen.download(centroids, rows * k);
+    if (mode == 1) {
+      dasg.download(assignments, rows * n);
+      dloss.download(loss, rows);
+      std::vector<int> it(rows);
+      diters.download(it.data(), rows);
+      for (int64_t r = 0; r < rows; ++r) iters[r] = it[r];
+    }
+  });
+}
+
+anyq_status anyq_build_sample_weights(const anyq_config* cfg, int64_t rows, int64_t cols,
+                                      const float* alphas, int64_t num_groups, int64_t row,
+                                      const float* stats, int64_t stats_len, int32_t weighting,
+                                      float* out) {
+  return guard([&] {
+    // the stats checks of learner.cpp:27-34, in order
+    if (stats) {
+      if (stats_len != cols)
+        fail(ANYQ_ERR_STATS, "sample weights: stats length " + std::to_string(stats_len) +
+                                 " does not match row length " + std::to_string(cols));
+      for (int64_t j = 0; j < cols; ++j)
+        if (!(stats[j] >= 0) || !std::isfinite(stats[j]))
+          fail(ANYQ_ERR_STATS, "sample weights: negative or non-finite stats entry");
+    }
+    if (weighting < 0 || weighting > 2) fail(ANYQ_ERR_CONFIG, "unknown weighting mode");
+    if (cols < 1) return;
+    if (row < 0 || row >= rows) fail(ANYQ_ERR_SHAPE, "sample weights: row out of range");
+    if (weighting == ANYQ_W_FULL && num_groups != group_count(*cfg, rows, cols))
+      fail(ANYQ_ERR_SHAPE, "sample weights: scale set does not match its granularity");
+    DevBuf<float> da(weighting == ANYQ_W_FULL ? num_groups : 0), ds(stats ? cols : 0), dout(cols);
+    if (weighting == ANYQ_W_FULL) da.upload(alphas, num_groups);
+    if (stats) ds.upload(stats, cols);
+    launch_sample_weights(*cfg, row, cols, da.p, ds.p, weighting, dout.p, 0);
+    dout.download(out, cols);
+  });
+}
+
+anyq_status anyq_round_to_table(const float* ws, int64_t rows, int64_t cols, const float* table,
+                                int32_t n, uint8_t* codes) {
+  return guard([&] {
+    if (n < 1 || n > 256) fail(ANYQ_ERR_CONFIG, "codebook must hold 1..256 values");
+    const int64_t total = rows * cols;
+    if (total <= 0) return;
+    Table t{};
+    t.n = n;
+    std::memcpy(t.v, table, sizeof(float) * n);
+    DevBuf<float> dws(total);
+    DevBuf<uint8_t> dc(total);
+    dws.upload(ws, total);
+    launch_check_finite(dws.p, total, stream_ws(0).err + kErrFinite, ANYQ_ERR_NONFINITE, 0);
+    check_stream_errors(0, "round_to_codebook");  // require_finite (codebooks.cpp:76)
+    launch_round(dws.p, total, t, dc.p, 0);
+    dc.download(codes, total);
+  });
+}
+
+anyq_status anyq_scaled_values(const anyq_qtensor* qt, float* out) {
+  return guard([&] {
+    check_qt(qt);
+    DevTensorArrays t;
+    DevBuf<float> w(qt->rows * qt->cols);
+    dequant_to_device(qt, t, w.p, true);
+    w.download(out, qt->rows * qt->cols);
+  });
+}
+
+anyq_status anyq_fixed_table(int32_t codebook, int32_t bits, int32_t shifted, float* values,
+                             int32_t* n) {
+  return host_only([&] {
+    if (codebook == ANYQ_CB_INT && bits != 2 && bits != 3 && bits != 4 && bits != 8)
+      fail(ANYQ_ERR_CONFIG, "int_grid: bits must be one of {2,3,4,8}");
+    anyq_config c;
+    anyq_config_default(&c);
+    c.codebook = codebook;
+    c.bits = bits;
+    c.int_range_shifted = shifted;
+    const Table t = fixed_table(c);
+    std::memcpy(values, t.v, sizeof(float) * t.n);
+    *n = t.n;
+  });
+}
+
+anyq_status anyq_f32_to_f16(float f, uint16_t* out) {
+  return host_only([&] {
+    int st = ANYQ_OK;
+    const uint16_t h = f32_to_f16_exact(f, &st);
+    if (st == ANYQ_ERR_NONFINITE) fail(ANYQ_ERR_NONFINITE, "fp16 narrowing: non-finite value");
+    if (st != ANYQ_OK) fail((anyq_status)st, "fp16 narrowing: value overflows to infinity");
+    *out = h;
+  });
+}
+float anyq_f16_to_f32(uint16_t h) { return f16_to_f32_exact(h); }
+anyq_status anyq_f32_to_bf16(float f, uint16_t* out) {
+  return host_only([&] {
+    int st = ANYQ_OK;
+    const uint16_t h = f32_to_bf16_exact(f, &st);
+    if (st == ANYQ_ERR_NONFINITE) fail(ANYQ_ERR_NONFINITE, "bf16 narrowing: non-finite value");
+    if (st != ANYQ_OK) fail((anyq_status)st, "bf16 narrowing: value overflows to infinity");
+    *out = h;
+  });
+}
+float anyq_bf16_to_f32(uint16_t h) { return bf16_to_f32_exact(h); }
+
+anyq_status anyq_storage_bits_per_entry(const anyq_config* cfg, int64_t rows, int64_t cols,
+                                        double* bits) {
+  return host_only([&] {
+    validate_config(*cfg, rows, cols);
+    const double entries = (double)rows * (double)cols;
+    const double groups = (double)group_count(*cfg, rows, cols);
+    // n code bits + 2 x 16-bit (scale, offset) per group + 2^n x 16-bit LUT per row for AnyN
+    const double meta = 32.0 * groups +
+                        (cfg->codebook == ANYQ_CB_ANY ? 16.0 * (double)rows * (double)(1 << cfg->bits) : 0.0);
+    *bits = (double)cfg->bits + meta / entries;
+  });
+}
+
+// qgemm.cpp:134-207 bench's timing loop, on the device: operands resident in
+// HBM, one warm-up run, then `repeats` runs each bracketed by CUDA events.
+anyq_status anyq_bench_gemm(int32_t kind, const anyq_qtensor* qt, const float* w, int64_t n,
+                            int64_t k, const float* x, int64_t m, int32_t repeats, double* ns) {
+  return guard([&] {
+    if (repeats < 1) fail(ANYQ_ERR_CONFIG, "bench: repeats must be >= 1");
+    if (m < 1 || n < 1 || k < 1) fail(ANYQ_ERR_SHAPE, "bench: empty GEMM");
+    if (kind != 0) {
+      check_qt(qt);
+      if (qt->rows != n || qt->cols != k) fail(ANYQ_ERR_SHAPE, "bench: tensor shape mismatch");
+    }
+    cudaStream_t s = 0;
+    DevBuf<float> dx(m * k), dy(m * n), dw(kind == 0 ? n * k : 0);
+    dx.upload(x, m * k);
+    DevTensorArrays t;
+    Table fixed{};
+    DevBuf<int> err(1);
+    err.zero();
+    LutTensor* lt = nullptr;
+    DevBuf<uint16_t> xb(kind == 2 ? m * k : 0), yb(kind == 2 ? m * n : 0);
+    if (kind == 0) {
+      dw.upload(w, n * k);
+    } else if (kind == 1) {
+      t.upload(qt);
+      if (qt->cfg.codebook != ANYQ_CB_ANY)
+        fixed = effective_table(fixed_table(qt->cfg), qt->cfg.symmetric != 0);
+    } else if (kind == 2) {
+      lt = lutgemm_create(qt);
+      std::vector<uint16_t> hb(m * k);
+      int st = ANYQ_OK;
+      for (int64_t i = 0; i < m * k; ++i) hb[i] = f32_to_bf16_exact(x[i], &st);
+      xb.upload(hb.data(), m * k);
+    } else {
+      fail(ANYQ_ERR_CONFIG, "bench: kind must be 0 (dense), 1 (exact fused) or 2 (A16W4)");
+    }
+    struct Guard {
+      LutTensor* t;
+      ~Guard() { lutgemm_destroy(t); }
+    } g{lt};
+    auto run = [&] {
+      if (kind == 0) {
+        launch_gemm_dense(dx.p, m, dw.p, n, k, dy.p, s);
+      } else if (kind == 1) {
+        launch_gemm_exact(dx.p, m, qt->cols, t.codes.p, qt->rows, qt->cfg.bits,
+                          qt->layout == ANYQ_LAYOUT_KTILED, qt->tile_k, t.luts.p, fixed, qt->cfg,
+                          t.alphas.p, t.betas.p, dy.p, err.p, s);
+      } else {
+        const int path = anyq_dev_gemm_auto_path(reinterpret_cast<anyq_dev_tensor*>(lt), m);
+        if (path == ANYQ_PATH_GEMV) lutgemv_run(lt, xb.p, m, yb.p, dy.p, s);
+        else if (path == ANYQ_PATH_MMA) lutmma_run(lt, xb.p, m, yb.p, dy.p, s);
+        else if (path == ANYQ_PATH_TC) lutgemm_run(lt, xb.p, m, yb.p, dy.p, s);
+        else dequant_gemm_run(lt, xb.p, m, yb.p, dy.p, s);
+      }
+    };
+    run();
+    check_device_error(err.p, "bench");
+    cudaEvent_t e0, e1;
+    ANYQ_CUDA(cudaEventCreate(&e0));
+    ANYQ_CUDA(cudaEventCreate(&e1));
+    for (int r = 0; r < repeats; ++r) {
+      ANYQ_CUDA(cudaEventRecord(e0, s));
+      run();
+      ANYQ_CUDA(cudaEventRecord(e1, s));
+      ANYQ_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.0f;
+      ANYQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      ns[r] = (double)ms * 1e6;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
 }
 
 // Debug hook (not part of the reference interface): record a per-CTA

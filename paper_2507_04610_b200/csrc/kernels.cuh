@@ -26,6 +26,9 @@ void launch_affine(const float* in, int64_t rows, int64_t cols, const anyq_confi
                    const float* alphas, const float* betas, int inverse, float* out,
                    cudaStream_t s);
 void launch_round(const float* ws, int64_t n, const Table& t, uint8_t* codes, cudaStream_t s);
+// build_sample_weights (learner.cpp:25-51) of one row: out[cols]
+void launch_sample_weights(const anyq_config& cfg, int64_t row, int64_t cols, const float* alphas,
+                           const float* stats, int weighting, float* out, cudaStream_t s);
 void launch_pack(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint8_t* out,
                  int* err, cudaStream_t s);
 void launch_unpack(const uint8_t* packed, int64_t rows, int64_t cols, int bits, uint8_t* codes,
@@ -48,5 +51,16 @@ void launch_gemm_dense(const float* x, int64_t m, const float* w, int64_t n, int
 void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
                    const anyq_config& cfg, int64_t row_offset, float* luts, uint8_t* codes,
                    int* err, cudaStream_t s);
+
+// The per-row learner API (learner.hpp:52-61) on `rows` independent problems
+// of n samples (row-major, original order), every reduction in the
+// reference's order: mode 0 = learn_row_lut (sorted LUT [rows][k] as float,
+// rank codes [rows][n], loss), 1 = weighted_kmeans (centroids [rows][k],
+// assignments [rows][n], loss, iters), 2 = kmeans_pp_init (centroids only).
+// rng_key / rng_ctr: each problem's Rng state, counters advanced in place.
+void launch_kmeans_problems(const float* x, const float* w, int64_t rows, int64_t n, int k,
+                            const anyq_config& cfg, int mode, const uint64_t* rng_key,
+                            uint64_t* rng_ctr, double* centroids, uint8_t* assignments, double* loss,
+                            int* iters, float* luts, uint8_t* codes, int* err, cudaStream_t s);
 
 }  // namespace anyq_b200

@@ -56,6 +56,19 @@ struct KmParams {
   int use_smem;
   const int* row_list;  // if set: process rows row_list[0 .. *row_list_n)
   const int* row_list_n;
+  // Problem mode (the per-row learner API, learner.hpp:52-68): caller RNG
+  // state per row, raw k-means results, every double reduction in the
+  // reference's sample-index order (sequential), so results are bit-identical
+  // by construction. mode: 0 = LUT + codes (quantize), 1 = weighted_kmeans,
+  // 2 = kmeans_pp_init only.
+  int mode;
+  int exact;
+  const uint64_t* rng_key;  // [rows] or null (rng_for_row(seed, row_offset + row))
+  uint64_t* rng_ctr;        // [rows] in/out counters (with rng_key)
+  double* out_cen;          // [rows][k] centroids in the learner's order
+  uint8_t* out_asg;         // [rows][n] assignments, original sample order
+  double* out_loss;         // [rows]
+  int* out_iters;           // [rows]
 };
 
 struct Part {  // partial segment sums
@@ -81,6 +94,7 @@ struct Shared {
   int64_t row;
   Rng rng;
   int ncen;
+  int iters;
 };
 
 __device__ __forceinline__ double dcost(double x, double c) {
@@ -145,6 +159,68 @@ __device__ double block_exclusive_scan(double v, Shared& sh, double* total) {
   double excl_in_warp = __shfl_up_sync(0xffffffffu, incl, 1);
   if (l == 0) excl_in_warp = 0.0;
   return __dadd_rn(base, excl_in_warp);
+}
+
+// Exact mode: sum of the positive masses in sample-index order (thread 0,
+// broadcast), as the reference's sequential `total += mass[i]` (mass >= 0).
+__device__ double seq_sum_pos(const double* mass, int64_t n, Shared& sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+      if (mass[i] > 0.0) t = __dadd_rn(t, mass[i]);
+    sh.dbl_bcast = t;
+  }
+  __syncthreads();
+  const double r = sh.dbl_bcast;
+  __syncthreads();
+  return r;
+}
+
+// Exact mode: sample_index (learner.cpp:64-75) sequentially in thread 0.
+__device__ int64_t seq_sample_index(const double* mass, int64_t n, double r_unit, Shared& sh,
+                                    double* total_out) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) total = __dadd_rn(total, mass[i]);
+    const double r = __dmul_rn(r_unit, total);
+    double acc = 0.0;
+    long long pick = -1, last = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (mass[i] <= 0.0) continue;
+      acc = __dadd_rn(acc, mass[i]);
+      last = i;
+      if (r < acc) {
+        pick = i;
+        break;
+      }
+    }
+    sh.ll_bcast = pick >= 0 ? pick : last;
+    sh.dbl_bcast = total;
+  }
+  __syncthreads();
+  const long long pick = sh.ll_bcast;
+  *total_out = sh.dbl_bcast;
+  __syncthreads();
+  return pick;
+}
+
+// Exact mode: sum_i w_i (x_i - c_{a_i})^2 in sample-index order (total_cost,
+// learner.cpp:198-204); asg_o holds original-order assignments.
+__device__ double seq_loss(const float* xo, const float* wo, const uint8_t* asg_o, int64_t n,
+                           Shared& sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+      l = __dadd_rn(l, __dmul_rn((double)wo[i], dcost((double)xo[i], sh.cen[asg_o[i]])));
+    sh.dbl_bcast = l;
+  }
+  __syncthreads();
+  const double r = sh.dbl_bcast;
+  __syncthreads();
+  return r;
 }
 
 // Sort the current centroids by (value, index): sv/so/rank_of.
@@ -253,7 +329,7 @@ __device__ void init_kmeanspp(const KmParams& P, const float* xo, const float* w
   __syncthreads();
   u = sh.dbl_bcast;
   double total;
-  int64_t pick = sample_index(d2, n, C, u, sh, &total);
+  int64_t pick = P.exact ? seq_sample_index(d2, n, u, sh, &total) : sample_index(d2, n, C, u, sh, &total);
   if (threadIdx.x == 0) {
     sh.cen[0] = (double)xo[pick];
     sh.ncen = 1;
@@ -276,12 +352,12 @@ __device__ void init_kmeanspp(const KmParams& P, const float* xo, const float* w
     double local = 0.0;
     for (int64_t i = b; i < e; ++i)
       if (mass[i] > 0.0) local = __dadd_rn(local, mass[i]);
-    double tot = block_sum(local, sh);
+    double tot = P.exact ? seq_sum_pos(mass, n, sh) : block_sum(local, sh);
     if (tot > 0.0) {
       if (threadIdx.x == 0) sh.dbl_bcast = sh.rng.next_double();
       __syncthreads();
       u = sh.dbl_bcast;
-      pick = sample_index(mass, n, C, u, sh, &total);
+      pick = P.exact ? seq_sample_index(mass, n, u, sh, &total) : sample_index(mass, n, C, u, sh, &total);
       if (threadIdx.x == 0) sh.cen[sh.ncen++] = (double)xo[pick];
       __syncthreads();
       continue;
@@ -291,12 +367,12 @@ __device__ void init_kmeanspp(const KmParams& P, const float* xo, const float* w
     local = 0.0;
     for (int64_t i = b; i < e; ++i)
       if (mass[i] > 0.0) local = __dadd_rn(local, mass[i]);
-    tot = block_sum(local, sh);
+    tot = P.exact ? seq_sum_pos(mass, n, sh) : block_sum(local, sh);
     if (tot > 0.0) {
       if (threadIdx.x == 0) sh.dbl_bcast = sh.rng.next_double();
       __syncthreads();
       u = sh.dbl_bcast;
-      pick = sample_index(mass, n, C, u, sh, &total);
+      pick = P.exact ? seq_sample_index(mass, n, u, sh, &total) : sample_index(mass, n, C, u, sh, &total);
       if (threadIdx.x == 0) sh.cen[sh.ncen++] = (double)xo[pick];
       __syncthreads();
       continue;
@@ -349,14 +425,23 @@ __device__ void init_random(const KmParams& P, const float* xo, const float* xs,
   __syncthreads();
 }
 
-// One Lloyd run (learner.cpp:207-312) on the sorted row. Returns the loss.
+// One Lloyd run (learner.cpp:207-312) on the sorted row. Returns the loss;
+// sh.iters = iterations run. Exact mode (P.exact) forms the M-step sums and
+// the losses in sample-index order from the original-order row (xo, wo).
 __device__ double lloyd(const KmParams& P, const float* xs, const float* wv, uint8_t* asg,
-                        Shared& sh, int k) {
+                        Shared& sh, int k, const float* xo, const float* wo, uint8_t* asg_o) {
   const int64_t n = P.n;
   const int64_t C = (n + kThreads - 1) / kThreads;
   const int64_t b = threadIdx.x * C, e = min(n, b + C);
+  const int* sv = P.svals + sh.row * n;
+  auto original_order = [&]() {
+    __syncthreads();
+    for (int64_t j = b; j < e; ++j) asg_o[sv[j]] = asg[j];
+    __syncthreads();
+  };
   for (int64_t j = b; j < e; ++j) asg[j] = 0;
   double prev = INFINITY;
+  if (threadIdx.x == 0) sh.iters = P.max_iters;
   for (int iter = 0; iter < P.max_iters; ++iter) {
     // ---- E-step
     sort_centroids(sh, k);
@@ -375,6 +460,26 @@ __device__ double lloyd(const KmParams& P, const float* xs, const float* wv, uin
       }
       if (__syncthreads_or(bad) && threadIdx.x == 0) dev_fail(P.err, ANYQ_ERR_INTERNAL);
     }
+    if (P.exact) {
+      // M-step in sample-index order (learner.cpp:245-253), one thread per cluster
+      original_order();
+      for (int q = threadIdx.x; q < k; q += kThreads) {
+        double swx = 0, sw = 0, sx = 0;
+        int c = 0;
+        for (int64_t i = 0; i < n; ++i)
+          if (asg_o[i] == q) {
+            const double w = (double)wo[i], x = (double)xo[i];
+            swx = __dadd_rn(swx, __dmul_rn(w, x));
+            sw = __dadd_rn(sw, w);
+            sx = __dadd_rn(sx, x);
+            ++c;
+          }
+        sh.swx[q] = swx;
+        sh.sw[q] = sw;
+        sh.sx[q] = sx;
+        sh.cnt[q] = c;
+      }
+    }
     // ---- M-step: monotonicity check + segment boundaries
     int mono = 1;
     for (int64_t j = b; j < e; ++j) {
@@ -387,7 +492,9 @@ __device__ double lloyd(const KmParams& P, const float* xs, const float* wv, uin
       for (int t = sh.rank_of[asg[n - 1]] + 1; t <= k; ++t) sh.seg_start[t] = (int)n;
     }
     mono = __syncthreads_and(mono);
-    if (mono) {
+    if (P.exact) {
+      // sums formed above
+    } else if (mono) {
       // per-chunk runs: first / last partials, interior runs are complete
       int nr = 0, fc = -1, lc = -1;
       Part cur = {0, 0, 0};
@@ -532,15 +639,24 @@ __device__ double lloyd(const KmParams& P, const float* xs, const float* wv, uin
       __syncthreads();
     }
     // ---- loss after the update (sample order fixed by chunk, then tree)
-    double local = 0.0;
-    for (int64_t j = b; j < e; ++j)
-      local = __dadd_rn(local, __dmul_rn((double)wv[j], dcost((double)xs[j], sh.cen[asg[j]])));
-    double loss_m = block_sum(local, sh);
+    double loss_m;
+    if (P.exact) {
+      original_order();
+      loss_m = seq_loss(xo, wo, asg_o, n, sh);
+    } else {
+      double local = 0.0;
+      for (int64_t j = b; j < e; ++j)
+        local = __dadd_rn(local, __dmul_rn((double)wv[j], dcost((double)xs[j], sh.cen[asg[j]])));
+      loss_m = block_sum(local, sh);
+    }
     int any_changed = __syncthreads_or(changed) || repairs > 0;
     bool stable = !any_changed && iter > 0;
     bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
     prev = loss_m;
-    if (stable || tol || loss_m == 0.0) break;
+    if (stable || tol || loss_m == 0.0) {
+      if (threadIdx.x == 0) sh.iters = iter + 1;
+      break;
+    }
   }
   // final reassignment and loss
   sort_centroids(sh, k);
@@ -549,6 +665,10 @@ __device__ double lloyd(const KmParams& P, const float* xs, const float* wv, uin
     int q = nearest((double)xs[j], sh, k);
     asg[j] = (uint8_t)q;
     local = __dadd_rn(local, __dmul_rn((double)wv[j], dcost((double)xs[j], sh.cen[q])));
+  }
+  if (P.exact) {
+    original_order();
+    return seq_loss(xo, wo, asg_o, n, sh);
   }
   return block_sum(local, sh);
 }
@@ -591,8 +711,25 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
       if (threadIdx.x == 0) dev_fail(P.err, ANYQ_ERR_STATS);
       continue;
     }
-    if (threadIdx.x == 0) sh.rng = Rng::for_row(P.seed, P.row_offset + row);
+    if (threadIdx.x == 0) {
+      if (P.rng_key) {  // the caller's stream (learner API): key + counter
+        sh.rng.key = P.rng_key[row];
+        sh.rng.counter = P.rng_ctr[row];
+      } else {
+        sh.rng = Rng::for_row(P.seed, P.row_offset + row);
+      }
+    }
+    if (P.mode == 2) {  // kmeans_pp_init only (learner.cpp:132-174)
+      __syncthreads();
+      init_kmeanspp(P, xo, wo, xs, d2, sh, k);
+      for (int q = threadIdx.x; q < k; q += kThreads) P.out_cen[row * k + q] = sh.cen[q];
+      if (threadIdx.x == 0) P.rng_ctr[row] = sh.rng.counter;
+      __syncthreads();
+      continue;
+    }
+    uint8_t* asg_o = asg + n;  // exact mode: original-order assignments
     double best = INFINITY;
+    int best_iters = 0;
     for (int r = 0; r < P.restarts; ++r) {
       __syncthreads();
       switch (P.init) {
@@ -612,12 +749,28 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
         }
       }
       __syncthreads();
-      double loss = lloyd(P, xs, wv, asg, sh, k);
+      double loss = lloyd(P, xs, wv, asg, sh, k, xo, wo, asg_o);
       if (loss < best) {
         best = loss;
+        best_iters = sh.iters;
         for (int q = threadIdx.x; q < k; q += kThreads) sh.best_cen[q] = sh.cen[q];
       }
       __syncthreads();
+    }
+    if (P.mode == 1) {  // weighted_kmeans (learner.cpp:316-341): raw best run
+      for (int q = threadIdx.x; q < k; q += kThreads) sh.cen[q] = sh.best_cen[q];
+      sort_centroids(sh, k);
+      for (int q = threadIdx.x; q < k; q += kThreads) P.out_cen[row * k + q] = sh.best_cen[q];
+      // the best run's returned assignments are nearest(best centroids) (learner.cpp:302-305)
+      for (int64_t j = b; j < e; ++j)
+        P.out_asg[row * n + P.svals[row * n + j]] = (uint8_t)nearest((double)xs[j], sh, k);
+      if (threadIdx.x == 0) {
+        P.out_loss[row] = best;
+        P.out_iters[row] = best_iters;
+        P.rng_ctr[row] = sh.rng.counter;
+      }
+      __syncthreads();
+      continue;
     }
     // best centroids -> sorted LUT + rank-remapped codes (learner.cpp:343-369)
     for (int q = threadIdx.x; q < k; q += kThreads) sh.cen[q] = sh.best_cen[q];
@@ -626,6 +779,10 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
     for (int64_t j = b; j < e; ++j) {
       int q = nearest((double)xs[j], sh, k);
       P.codes[row * n + P.svals[row * n + j]] = (uint8_t)sh.rank_of[q];
+    }
+    if (threadIdx.x == 0 && P.rng_ctr) {  // learn_row_lut (learner.cpp:343-369)
+      P.out_loss[row] = best;
+      P.rng_ctr[row] = sh.rng.counter;
     }
     __syncthreads();
   }
@@ -1551,29 +1708,116 @@ __global__ void k_iota_rows(int* v, int64_t rows, int64_t n) {
 
 }  // namespace
 
+namespace {
+
+// Stable ascending sort of every row (value, original index), stream ordered.
+void sort_rows(const float* ws, int64_t rows, int64_t cols, float* skeys, int* svals,
+               cudaStream_t s) {
+  const int64_t total = rows * cols;
+  DevBuf<int> idx(total, s), offs(rows + 1, s);
+  k_fill_offsets<<<(unsigned)((rows + 256) / 256), 256, 0, s>>>(offs.p, rows, cols);
+  ANYQ_LAUNCHED();
+  k_iota_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(idx.p, rows, cols);
+  ANYQ_LAUNCHED();
+  size_t temp_bytes = 0;
+  ANYQ_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, temp_bytes, ws, skeys, idx.p, svals,
+                                                      (int)total, (int)rows, offs.p, offs.p + 1, s));
+  DevBuf<uint8_t> temp(temp_bytes, s);
+  ANYQ_CUDA(cub::DeviceSegmentedSort::StableSortPairs(temp.p, temp_bytes, ws, skeys, idx.p, svals,
+                                                      (int)total, (int)rows, offs.p, offs.p + 1, s));
+  note_launch(2);
+}
+
+// Dynamic shared memory of k_kmeans_rows for rows of n samples: xs, wv (fp32)
+// + 2n doubles (d2 / mass during k-means++, then the two assignment arrays).
+size_t rows_kernel_smem(int64_t n) {
+  return (((sizeof(float) * 2 * n) + 15) & ~size_t(15)) + sizeof(double) * 2 * n;
+}
+
+// Launches k_kmeans_rows over P.rows rows (shared memory or global scratch).
+void launch_rows_kernel(KmParams& P, int64_t cta_rows, cudaStream_t s) {
+  int dev = 0, sms = 148, max_optin = 0;
+  ANYQ_CUDA(cudaGetDevice(&dev));
+  ANYQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  ANYQ_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t need = rows_kernel_smem(P.n);
+  const size_t static_smem = sizeof(Shared) + 2 * 2 * kMaxK * sizeof(int64_t);
+  DevBuf<uint8_t> gscratch;
+  int blocks;
+  if (need + static_smem <= (size_t)max_optin) {
+    P.use_smem = 1;
+    P.gscratch = nullptr;
+    P.scratch_stride = 0;
+    ensure_dyn_smem((const void*)k_kmeans_rows, (int)need);
+    int per_sm = 0;
+    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, kThreads, need));
+    blocks = (int)std::min<int64_t>(cta_rows, (int64_t)sms * std::max(1, per_sm));
+    k_kmeans_rows<<<blocks, kThreads, need, s>>>(P);
+  } else {
+    int per_sm = 0;
+    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, kThreads, 0));
+    blocks = (int)std::min<int64_t>(cta_rows, (int64_t)sms * std::max(1, per_sm));
+    P.use_smem = 0;
+    P.scratch_stride = (need + 255) & ~size_t(255);
+    gscratch.alloc(P.scratch_stride * blocks, s);
+    P.gscratch = gscratch.p;
+    k_kmeans_rows<<<blocks, kThreads, 0, s>>>(P);
+  }
+  ANYQ_LAUNCHED();
+  // scratch is released stream-ordered on return
+}
+
+}  // namespace
+
+void launch_kmeans_problems(const float* x, const float* w, int64_t rows, int64_t n, int k,
+                            const anyq_config& cfg, int mode, const uint64_t* rng_key,
+                            uint64_t* rng_ctr, double* centroids, uint8_t* assignments, double* loss,
+                            int* iters, float* luts, uint8_t* codes, int* err, cudaStream_t s) {
+  if (rows * n >= (int64_t(1) << 31)) fail(ANYQ_ERR_SHAPE, "k-means batch too large; split rows");
+  if (k < 1 || k > kMaxK) fail(ANYQ_ERR_CONFIG, "k must be in [1, 256]");
+  DevBuf<float> skeys(rows * n, s);
+  DevBuf<int> svals(rows * n, s), counter(1, s);
+  sort_rows(x, rows, n, skeys.p, svals.p, s);
+  ANYQ_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
+  KmParams P{};
+  P.ws = x;
+  P.sw = w;
+  P.skeys = skeys.p;
+  P.svals = svals.p;
+  P.rows = rows;
+  P.n = n;
+  P.k = k;
+  P.init = mode == 2 ? ANYQ_INIT_KMPP : cfg.init;
+  P.max_iters = cfg.max_iters;
+  P.restarts = cfg.restarts;
+  P.check_inv = cfg.check_invariants;
+  P.rel_tol = cfg.rel_tol;
+  P.err = err;
+  P.row_counter = counter.p;
+  P.mode = mode;
+  P.exact = 1;
+  P.rng_key = rng_key;
+  P.rng_ctr = rng_ctr;
+  P.out_cen = centroids;
+  P.out_asg = assignments;
+  P.out_loss = loss;
+  P.out_iters = iters;
+  P.luts = luts;
+  P.codes = codes;
+  launch_rows_kernel(P, rows, s);
+}
+
 void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
                    const anyq_config& cfg, int64_t row_offset, float* luts, uint8_t* codes,
                    int* err, cudaStream_t s) {
   if (rows * cols >= (int64_t(1) << 31)) fail(ANYQ_ERR_SHAPE, "quantize batch too large; split rows");
   const int64_t total = rows * cols;
   DevBuf<float> skeys(total, s);
-  DevBuf<int> idx(total, s), svals(total, s), offs(rows + 1, s), counter(1, s);
-  k_fill_offsets<<<(unsigned)((rows + 256) / 256), 256, 0, s>>>(offs.p, rows, cols);
-  ANYQ_LAUNCHED();
-  k_iota_rows<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(idx.p, rows, cols);
-  ANYQ_LAUNCHED();
-  size_t temp_bytes = 0;
-  ANYQ_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, temp_bytes, ws, skeys.p, idx.p,
-                                                      svals.p, (int)total, (int)rows, offs.p,
-                                                      offs.p + 1, s));
-  DevBuf<uint8_t> temp(temp_bytes, s);
-  ANYQ_CUDA(cub::DeviceSegmentedSort::StableSortPairs(temp.p, temp_bytes, ws, skeys.p, idx.p,
-                                                      svals.p, (int)total, (int)rows, offs.p,
-                                                      offs.p + 1, s));
-  note_launch(2);
+  DevBuf<int> svals(total, s), counter(1, s);
+  sort_rows(ws, rows, cols, skeys.p, svals.p, s);
   ANYQ_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), s));
 
-  KmParams P;
+  KmParams P{};
   P.ws = ws;
   P.sw = sw;
   P.skeys = skeys.p;
@@ -1680,34 +1924,7 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
     P.row_list_n = bail_n.p;
   }
 
-  // per-row scratch: xs, wv (fp32) + 2n doubles (d2/mass during init, asg after)
-  size_t need = (((sizeof(float) * 2 * cols) + 15) & ~size_t(15)) + sizeof(double) * 2 * cols;
-  size_t static_smem = sizeof(Shared) + 2 * 2 * kMaxK * sizeof(int64_t);
-  DevBuf<uint8_t> gscratch;
-  int blocks;
-  const int64_t cta_rows = use_warp ? std::min<int64_t>(rows, (int64_t)sms) : rows;
-  if (need + static_smem <= (size_t)max_optin) {
-    P.use_smem = 1;
-    P.gscratch = nullptr;
-    P.scratch_stride = 0;
-    ANYQ_CUDA(cudaFuncSetAttribute(k_kmeans_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)need));
-    int per_sm = 0;
-    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, kThreads, need));
-    blocks = (int)std::min<int64_t>(cta_rows, (int64_t)sms * std::max(1, per_sm));
-    k_kmeans_rows<<<blocks, kThreads, need, s>>>(P);
-  } else {
-    int per_sm = 0;
-    ANYQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kmeans_rows, kThreads, 0));
-    blocks = (int)std::min<int64_t>(cta_rows, (int64_t)sms * std::max(1, per_sm));
-    P.use_smem = 0;
-    P.scratch_stride = (need + 255) & ~size_t(255);
-    gscratch.alloc(P.scratch_stride * blocks, s);
-    P.gscratch = gscratch.p;
-    k_kmeans_rows<<<blocks, kThreads, 0, s>>>(P);
-  }
-  ANYQ_LAUNCHED();
-  // scratch buffers are released stream-ordered on return
+  launch_rows_kernel(P, use_warp ? std::min<int64_t>(rows, (int64_t)sms) : rows, s);
 }
 
 }  // namespace anyq_b200

@@ -293,8 +293,25 @@ __global__ void k_dequant(const uint8_t* __restrict__ packed, int64_t rows, int6
         v = fixed.v[c];
       }
     }
-    int64_t g = gm(i, j);
-    w[e] = __fadd_rn(__fmul_rn(alphas[g], v), betas[g]);
+    if (alphas) {
+      int64_t g = gm(i, j);
+      w[e] = __fadd_rn(__fmul_rn(alphas[g], v), betas[g]);
+    } else {
+      w[e] = v;  // scaled_values (pack.cpp:205-236): the table value itself
+    }
+  }
+}
+
+// build_sample_weights (learner.cpp:25-51) for one row of a scale set.
+__global__ void k_sample_weights(int64_t row, int64_t cols, GroupMap gm,
+                                 const float* __restrict__ alphas, const float* __restrict__ stats,
+                                 int weighting, float* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cols;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const float e = stats ? stats[j] : 1.0f;
+    out[j] = weighting == ANYQ_W_WEIGHTS ? 1.0f
+             : weighting == ANYQ_W_ACTS  ? e
+                                         : __fmul_rn(alphas[gm(row, j)], e);
   }
 }
 
@@ -425,6 +442,13 @@ void launch_affine(const float* in, int64_t rows, int64_t cols, const anyq_confi
                    cudaStream_t s) {
   GroupMap gm = make_group_map(cfg, cols);
   k_affine<<<grid_for(rows * cols), 256, 0, s>>>(in, rows, cols, gm, alphas, betas, inverse, out);
+  ANYQ_LAUNCHED();
+}
+
+void launch_sample_weights(const anyq_config& cfg, int64_t row, int64_t cols, const float* alphas,
+                           const float* stats, int weighting, float* out, cudaStream_t s) {
+  k_sample_weights<<<grid_for(cols), 256, 0, s>>>(row, cols, make_group_map(cfg, cols), alphas, stats,
+                                                 weighting, out);
   ANYQ_LAUNCHED();
 }
 

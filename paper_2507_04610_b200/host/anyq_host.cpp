@@ -1,26 +1,42 @@
 // C++ host layer of the drop-in: the reference's hot-path API (declared in
-// proj/include/anyq/{learner,quantize,pack,qgemm}.hpp, compiled against those
-// headers in place) implemented on the B200 library through its C-ABI
-// (include/anyq_b200.h). Same signatures, value semantics and exception
-// classes as the reference; every computation runs on the GPU — a host with no
-// device gets anyq::Error from the first call, never a CPU result.
+// proj/include/anyq/{learner,quantize,pack,qgemm,codebooks,scaling,calibration}.hpp,
+// compiled against those headers in place) implemented on the B200 library
+// through its C-ABI (include/anyq_b200.h). Same signatures, value semantics and
+// exception classes as the reference; every computation runs on the GPU — a
+// host with no device gets anyq::Error from the first compute call, never a
+// CPU result. What stays on the host is argument checking, the fixed-table
+// bookkeeping (effective_codebook's 16 subtractions), scalar fp16/bf16
+// conversions (through the library's bit-exact converters), the ANYQ file
+// size arithmetic and string tables.
 //
-//   quantize_any    learner.hpp:74     quantize_fixed  quantize.hpp:17
-//   pack_codes      pack.hpp:50        unpack_codes    pack.hpp:51
-//   narrowed        pack.hpp:68        to_ktiled / from_ktiled  pack.hpp:86-87
-//   dequantize(qt)  pack.hpp:98        gemm_dense / gemm_reference / gemm_fused
-//                                                      qgemm.hpp:28-37
-//   compute_scales  scaling.hpp:52     scale_weights   scaling.hpp:56
-//   dequantize(values, s)  scaling.hpp:60
-//   write_file / read_file  pack.hpp (pack.cpp:293-471, ANYQ v1 files)
+//   quantize_any / learn_row_lut / weighted_kmeans / kmeans_pp_init /
+//     build_sample_weights / KmProblem::validate        learner.hpp:30-75
+//   quantize / quantize_fixed / apply_format / format and enum names
+//                                                       quantize.hpp:17-45
+//   int_grid / fp4_table / nf4_table / fixed_codebook / effective_codebook /
+//     round_to_codebook / storage_bits_per_entry / codebook_json
+//                                                       codebooks.hpp:27-55
+//   pack_codes / unpack_codes / f32_to_f16 ... / narrow_lut / widen_lut /
+//     narrowed / to_ktiled / from_ktiled / scaled_values / dequantize /
+//     file_sizes / write_file / read_file               pack.hpp:50-121
+//   compute_scales / scale_weights / dequantize(values, s)  scaling.hpp:52-60
+//   make_plan / gemm_dense / gemm_reference / gemm_fused / bench / bench_csv
+//                                                       qgemm.hpp:24-59
+//   ActivationStats::for_module                         calibration.hpp:21
 //
-// Linking this object before the reference objects (tests/reftests/Makefile
-// weakens the latter) swaps the hot path of an unmodified reference build —
-// including its CLI and own unit tests — onto the GPU.
+// This object alone (plus libanyq_b200.so) is the drop-in: no reference
+// object is linked into libanyq_host.so or the B200 test binary.
+#include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <numeric>
+#include <sstream>
 #include <string>
+#include <type_traits>
 #include <vector>
 
+#include "anyq/calibration.hpp"
+#include "anyq/codebooks.hpp"
 #include "anyq/learner.hpp"
 #include "anyq/pack.hpp"
 #include "anyq/qgemm.hpp"
@@ -334,6 +350,451 @@ Matf gemm_fused(const Eigen::Ref<const Matf>& x, const QuantizedTensor& qt, cons
   check(anyq_gemm_fused(xf.data(), x.rows(), &v.t, static_cast<int32_t>(plan.layout), plan.tile_k,
                         y.data()));
   return y;
+}
+
+
+// ---------------------------------------------------------------------------
+// calibration.hpp:21
+// ---------------------------------------------------------------------------
+const Vecf& ActivationStats::for_module(const std::string& name, Index cols) const {
+  const auto it = entries.find(name);
+  if (it == entries.end()) throw StatsError("no activation stats for module '" + name + "'");
+  if (it->second.size() != cols)
+    throw StatsError("activation stats for '" + name + "' have " + std::to_string(it->second.size()) +
+                     " channels, matrix has " + std::to_string(cols));
+  return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// Codebooks (codebooks.hpp:27-55). The fixed tables come from the library.
+// ---------------------------------------------------------------------------
+namespace {
+
+Codebook table_of(CodebookKind kind, int bits, bool shifted) {
+  float v[256];
+  int32_t n = 0;
+  check(anyq_fixed_table(static_cast<int32_t>(kind), bits, shifted ? 1 : 0, v, &n));
+  Codebook cb;
+  cb.kind = kind;
+  cb.bits = bits;
+  cb.values.assign(v, v + n);
+  return cb;
+}
+
+}  // namespace
+
+Codebook int_grid(int bits, bool shifted) { return table_of(CodebookKind::IntGrid, bits, shifted); }
+Codebook fp4_table() { return table_of(CodebookKind::Fp4, 4, false); }
+Codebook nf4_table() { return table_of(CodebookKind::Nf4, 4, false); }
+
+Codebook fixed_codebook(const QuantConfig& cfg) {
+  if (cfg.codebook == CodebookKind::AnyN) throw ConfigError("AnyN has no fixed codebook");
+  if (cfg.codebook == CodebookKind::IntGrid) return int_grid(cfg.bits, cfg.int_range_shifted);
+  if (cfg.codebook == CodebookKind::Fp4) return fp4_table();
+  if (cfg.codebook == CodebookKind::Nf4) return nf4_table();
+  throw ConfigError("unknown codebook kind");
+}
+
+Codebook effective_codebook(const Codebook& cb, bool symmetric) {
+  Codebook out = cb;
+  if (!symmetric) {
+    const Real lo = cb.values.front();
+    std::transform(cb.values.begin(), cb.values.end(), out.values.begin(),
+                   [lo](Real v) { return v - lo; });
+  }
+  return out;
+}
+
+CodeMat round_to_codebook(const Eigen::Ref<const Matf>& ws, const Codebook& cb) {
+  const std::vector<float> f = flat(ws);
+  std::vector<uint8_t> c(f.size());
+  check(anyq_round_to_table(f.data(), ws.rows(), ws.cols(), cb.values.data(),
+                            static_cast<int32_t>(cb.values.size()), c.data()));
+  CodeMat codes(ws.rows(), ws.cols());
+  std::memcpy(codes.data(), c.data(), c.size());
+  return codes;
+}
+
+double storage_bits_per_entry(const QuantConfig& cfg, Index rows, Index cols) {
+  validate(cfg, rows, cols);
+  const anyq_config c = to_c(cfg);
+  double bits = 0;
+  check(anyq_storage_bits_per_entry(&c, rows, cols, &bits));
+  return bits;
+}
+
+std::string codebook_json(const Codebook& cb) {
+  static const char* const kNames[] = {"int", "fp4", "nf4", "any"};
+  std::ostringstream os;
+  os.precision(9);
+  os << "{\"kind\":\"" << kNames[static_cast<int>(cb.kind) & 3] << "\",\"bits\":" << cb.bits
+     << ",\"values\":[";
+  const char* sep = "";
+  for (Real v : cb.values) {
+    os << sep << v;
+    sep = ",";
+  }
+  os << "]}";
+  return os.str();
+}
+
+// ---------------------------------------------------------------------------
+// Scalar narrowing (pack.hpp:57-66) and whole-tensor helpers
+// ---------------------------------------------------------------------------
+uint16_t f32_to_f16(Real f) {
+  uint16_t h = 0;
+  check(anyq_f32_to_f16(f, &h));
+  return h;
+}
+Real f16_to_f32(uint16_t h) { return anyq_f16_to_f32(h); }
+uint16_t f32_to_bf16(Real f) {
+  uint16_t h = 0;
+  check(anyq_f32_to_bf16(f, &h));
+  return h;
+}
+Real bf16_to_f32(uint16_t h) { return anyq_bf16_to_f32(h); }
+
+std::vector<uint16_t> narrow_lut(std::span<const Real> values, Store16 target) {
+  if (target == Store16::Fp32) throw ConfigError("narrow_lut targets fp16 or bf16");
+  std::vector<uint16_t> out;
+  out.reserve(values.size());
+  for (Real v : values) out.push_back(target == Store16::Fp16 ? f32_to_f16(v) : f32_to_bf16(v));
+  return out;
+}
+
+std::vector<Real> widen_lut(std::span<const uint16_t> bits, Store16 source) {
+  if (source == Store16::Fp32) throw ConfigError("widen_lut sources fp16 or bf16");
+  std::vector<Real> out;
+  out.reserve(bits.size());
+  for (uint16_t b : bits) out.push_back(source == Store16::Fp16 ? f16_to_f32(b) : bf16_to_f32(b));
+  return out;
+}
+
+Matf scaled_values(const QuantizedTensor& qt) {
+  Matf v(qt.rows, qt.cols);
+  CView view(qt);
+  check(anyq_scaled_values(&view.t, v.data()));
+  return v;
+}
+
+SizeBreakdown file_sizes(const QuantizedTensor& qt) {
+  // ANYQ v1 layout (pack.cpp:240-291): 120-byte header, packed codes, alphas
+  // then betas, row LUTs; 16-bit stores take 2 bytes per value, fp32 4
+  auto width = [](Store16 s) -> uint64_t { return s == Store16::Fp32 ? 4 : 2; };
+  SizeBreakdown b;
+  b.header = 120;
+  b.codes = qt.codes.size();
+  b.scales = 2ull * static_cast<uint64_t>(qt.scales.num_groups()) * width(qt.scale_store);
+  b.luts = static_cast<uint64_t>(qt.luts.size()) * width(qt.lut_store);
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// The per-row learner (learner.hpp:30-68) on the GPU
+// ---------------------------------------------------------------------------
+namespace {
+
+// Rng (core.hpp:164-192) is {key, counter}; the library takes and returns
+// that state so the caller's stream advances exactly as in the reference.
+static_assert(sizeof(Rng) == 2 * sizeof(uint64_t) && std::is_standard_layout_v<Rng>,
+              "Rng is expected to hold {key, counter}");
+void rng_get(const Rng& r, uint64_t* key, uint64_t* ctr) {
+  uint64_t st[2];
+  std::memcpy(st, &r, sizeof st);
+  *key = st[0];
+  *ctr = st[1];
+}
+void rng_set(Rng& r, uint64_t ctr) {
+  uint64_t st[2];
+  std::memcpy(st, &r, sizeof st);
+  st[1] = ctr;
+  std::memcpy(&r, st, sizeof st);
+}
+
+anyq_config learner_cfg(const LearnerConfig& l) {
+  anyq_config c;
+  anyq_config_default(&c);
+  c.init = static_cast<int32_t>(l.init);
+  c.max_iters = l.max_iters;
+  c.rel_tol = l.rel_tol;
+  c.restarts = l.restarts;
+  c.weighting = static_cast<int32_t>(l.weighting);
+  c.check_invariants = l.check_invariants ? 1 : 0;
+  return c;
+}
+
+// One KmProblem through anyq_kmeans_problems (mode 0: learn_row_lut, 1:
+// weighted_kmeans, 2: kmeans_pp_init).
+void run_problem(const std::vector<Real>& x, const std::vector<Real>& w, int k,
+                 const LearnerConfig& l, Rng& rng, int mode, std::vector<double>& cen,
+                 std::vector<uint8_t>& asg, double& loss, int& iters) {
+  uint64_t key = 0, ctr = 0;
+  rng_get(rng, &key, &ctr);
+  const anyq_config c = learner_cfg(l);
+  const int64_t n = static_cast<int64_t>(x.size());
+  cen.assign(k > 0 ? k : 0, 0.0);
+  asg.assign(mode == 2 ? 0 : x.size(), 0);
+  int32_t it = 0;
+  if (w.size() != x.size()) throw ShapeError("KmProblem: samples and weights differ in length");
+  check(anyq_kmeans_problems(x.data(), w.data(), 1, n, k, &c, mode, &key, &ctr, cen.data(),
+                             asg.empty() ? nullptr : asg.data(), &loss, &it));
+  rng_set(rng, ctr);
+  iters = it;
+}
+
+}  // namespace
+
+void KmProblem::validate() const {
+  if (samples.size() != weights.size())
+    throw ShapeError("KmProblem: samples and weights differ in length");
+  if (samples.empty()) throw ShapeError("KmProblem: empty problem");
+  const bool all_ok = std::all_of(weights.begin(), weights.end(),
+                                   [](Real w) { return w >= 0 && std::isfinite(w); });
+  if (!all_ok) throw StatsError("KmProblem: weights must be >= 0");
+  if (std::none_of(weights.begin(), weights.end(), [](Real w) { return w > 0; }))
+    throw StatsError("KmProblem: all sample weights are zero");
+  if (!std::all_of(samples.begin(), samples.end(), [](Real x) { return std::isfinite(x); }))
+    throw NonFiniteError("KmProblem: non-finite sample");
+}
+
+Vecf build_sample_weights(const ScaleSet& s, Index row, const Vecf* stats, Weighting mode) {
+  const anyq_config c = group_cfg(s);
+  Vecf out(s.cols);
+  check(anyq_build_sample_weights(&c, s.rows, s.cols, s.alphas.data(), s.num_groups(), row,
+                                  stats ? stats->data() : nullptr, stats ? stats->size() : 0,
+                                  static_cast<int32_t>(mode), out.data()));
+  return out;
+}
+
+std::vector<double> kmeans_pp_init(const KmProblem& p, int k, Rng& rng) {
+  p.validate();
+  if (k < 1) throw ConfigError("k must be >= 1");
+  std::vector<double> cen;
+  std::vector<uint8_t> asg;
+  double loss = 0;
+  int iters = 0;
+  run_problem(p.samples, p.weights, k, LearnerConfig{}, rng, 2, cen, asg, loss, iters);
+  return cen;
+}
+
+KmResult weighted_kmeans(const KmProblem& p, int k, const LearnerConfig& cfg, Rng& rng) {
+  p.validate();
+  if (k < 1) throw ConfigError("k must be >= 1");
+  if (k > 256) throw ConfigError("k must fit an 8-bit code");
+  KmResult r;
+  run_problem(p.samples, p.weights, k, cfg, rng, 1, r.centroids, r.assignments, r.loss, r.iters);
+  return r;
+}
+
+RowQuant learn_row_lut(std::span<const Real> ws_row, std::span<const Real> weights,
+                       const LearnerConfig& cfg, int bits, Rng& rng) {
+  if (ws_row.size() != weights.size())
+    throw ShapeError("learn_row_lut: row and weights differ in length");
+  KmProblem p;
+  p.samples.assign(ws_row.begin(), ws_row.end());
+  p.weights.assign(weights.begin(), weights.end());
+  p.validate();
+  const int k = 1 << bits;
+  if (k > 256) throw ConfigError("k must fit an 8-bit code");
+  std::vector<double> lut;
+  RowQuant rq;
+  int iters = 0;
+  // mode 0: the GPU sorts the table and rank-remaps the codes (learner.cpp:355-367)
+  run_problem(p.samples, p.weights, k, cfg, rng, 0, lut, rq.codes, rq.loss, iters);
+  rq.lut.values.assign(lut.begin(), lut.end());
+  return rq;
+}
+
+// ---------------------------------------------------------------------------
+// Front door (quantize.hpp:17-45)
+// ---------------------------------------------------------------------------
+QuantizedTensor quantize(const Eigen::Ref<const Matf>& w, const QuantConfig& cfg,
+                         const ActivationStats* stats, const std::string& module_name,
+                         int threads) {
+  if (cfg.codebook != CodebookKind::AnyN) return quantize_fixed(w, cfg);
+  const Vecf* exj = stats ? &stats->for_module(module_name, w.cols()) : nullptr;
+  return quantize_any(w, cfg, exj, threads);
+}
+
+namespace {
+
+template <typename E>
+struct Named {
+  const char* name;
+  E value;
+};
+
+constexpr Named<Granularity> kGranularities[] = {
+    {"tensorwise", Granularity::Tensorwise}, {"rowwise", Granularity::Rowwise},
+    {"columnwise", Granularity::Columnwise}, {"groupwise", Granularity::Groupwise},
+    {"blockwise", Granularity::Blockwise}};
+constexpr Named<Weighting> kWeightings[] = {
+    {"weights", Weighting::WeightsOnly},
+    {"weights-activations", Weighting::WeightsTimesActivations},
+    {"full", Weighting::WeightsTimesActivationsTimesScales}};
+constexpr Named<LutInit> kInits[] = {{"kmeans++", LutInit::KMeansPlusPlus},
+                                     {"random", LutInit::Random},
+                                     {"int-grid", LutInit::IntGridSeed},
+                                     {"nf4", LutInit::Nf4Seed}};
+constexpr Named<Store16> kStores[] = {
+    {"fp16", Store16::Fp16}, {"bf16", Store16::Bf16}, {"fp32", Store16::Fp32}};
+
+template <typename E, size_t N>
+E parse_named(const Named<E> (&table)[N], const std::string& name, const char* what) {
+  for (const auto& e : table)
+    if (name == e.name) return e.value;
+  throw ConfigError(std::string("unknown ") + what + " '" + name + "'");
+}
+
+template <typename E, size_t N>
+std::string name_of(const Named<E> (&table)[N], E value) {
+  for (const auto& e : table)
+    if (e.value == value) return e.name;
+  return "?";
+}
+
+// format names (quantize.cpp:34-54): a codebook kind and a bit width each
+struct Format {
+  const char* name;
+  CodebookKind kind;
+  int bits;
+};
+constexpr Format kFormats[] = {
+    {"int2", CodebookKind::IntGrid, 2}, {"int3", CodebookKind::IntGrid, 3},
+    {"int4", CodebookKind::IntGrid, 4}, {"int8", CodebookKind::IntGrid, 8},
+    {"fp4", CodebookKind::Fp4, 4},      {"nf4", CodebookKind::Nf4, 4},
+    {"any2", CodebookKind::AnyN, 2},    {"any3", CodebookKind::AnyN, 3},
+    {"any4", CodebookKind::AnyN, 4},    {"any8", CodebookKind::AnyN, 8}};
+
+}  // namespace
+
+void apply_format(QuantConfig& cfg, const std::string& format) {
+  for (const auto& f : kFormats) {
+    if (format == f.name) {
+      cfg.codebook = f.kind;
+      cfg.bits = f.bits;
+      return;
+    }
+  }
+  throw ConfigError("unknown format '" + format + "'");
+}
+
+std::string format_name(const QuantConfig& cfg) {
+  switch (cfg.codebook) {
+    case CodebookKind::IntGrid: return "int" + std::to_string(cfg.bits);
+    case CodebookKind::AnyN: return "any" + std::to_string(cfg.bits);
+    case CodebookKind::Fp4: return "fp4";
+    case CodebookKind::Nf4: return "nf4";
+  }
+  return "?";
+}
+
+Granularity parse_granularity(const std::string& name) {
+  return parse_named(kGranularities, name, "granularity");
+}
+std::string granularity_name(Granularity g) { return name_of(kGranularities, g); }
+Weighting parse_weighting(const std::string& name) {
+  return parse_named(kWeightings, name, "weighting");
+}
+std::string weighting_name(Weighting w) { return name_of(kWeightings, w); }
+LutInit parse_init(const std::string& name) { return parse_named(kInits, name, "init"); }
+std::string init_name(LutInit init) { return name_of(kInits, init); }
+Store16 parse_store(const std::string& name) {
+  return parse_named(kStores, name, "storage precision");
+}
+std::string store_name(Store16 s) { return name_of(kStores, s); }
+
+// ---------------------------------------------------------------------------
+// GEMM plan and the benchmark (qgemm.hpp:24, 55-59)
+// ---------------------------------------------------------------------------
+GemmPlan make_plan(const Eigen::Ref<const Matf>& x, const QuantizedTensor& qt) {
+  GemmPlan plan;
+  plan.m = x.rows();
+  plan.n = qt.rows;
+  plan.k = qt.cols;
+  plan.layout = qt.layout;
+  plan.tile_k = qt.tile_k;
+  return plan;
+}
+
+namespace {
+
+// Linear-interpolated percentile of a sample (qgemm.cpp bench semantics).
+double quantile(std::vector<double> v, double p) {
+  std::sort(v.begin(), v.end());
+  const double pos = p * static_cast<double>(v.size() - 1);
+  const size_t lo = static_cast<size_t>(pos);
+  const size_t hi = std::min(lo + 1, v.size() - 1);
+  const double t = pos - static_cast<double>(lo);
+  return v[lo] + (v[hi] - v[lo]) * t;
+}
+
+}  // namespace
+
+// The reference times its CPU gemm_fused per (shape, format) next to a dense
+// fp32 row. Here every timing is a device run with HBM-resident operands
+// (CUDA events): "dense" = fp32 gemm_dense, "rowmajor" = the bit-exact
+// gemm_fused kernel, "b200" = the A16W4 LUT GEMM on the prepacked tensor (the
+// AUTO kernel for m; formats it does not take — 8-bit codes, groups that are
+// not multiples of 128 — get no such row). Inputs are generated as the
+// reference generates them (rng_for_row(seed, row index) Gaussians).
+std::vector<BenchRow> bench(const std::vector<BenchShape>& shapes,
+                            const std::vector<std::string>& formats, int repeats, uint64_t seed) {
+  if (repeats < 1) throw ConfigError("bench: repeats must be >= 1");
+  std::vector<BenchRow> rows;
+  auto gaussian = [](Index r, Index c, Rng& rng) {
+    Matf m(r, c);
+    for (Index i = 0; i < r; ++i)
+      for (Index j = 0; j < c; ++j) m(i, j) = static_cast<Real>(rng.next_gaussian());
+    return m;
+  };
+  for (const BenchShape& shape : shapes) {
+    Rng rng = rng_for_row(seed, static_cast<Index>(rows.size()));
+    const Matf w = gaussian(shape.n, shape.k, rng);
+    const Matf x = gaussian(shape.m, shape.k, rng);
+    std::vector<double> ns(static_cast<size_t>(repeats));
+    auto push = [&](const std::string& fmt, const std::string& layout, double bpw) {
+      BenchRow r;
+      r.shape = shape;
+      r.format = fmt;
+      r.layout = layout;
+      r.median_ns = quantile(ns, 0.5);
+      r.p10_ns = quantile(ns, 0.1);
+      r.p90_ns = quantile(ns, 0.9);
+      r.bytes_per_weight = bpw;
+      rows.push_back(r);
+    };
+    check(anyq_bench_gemm(0, nullptr, w.data(), shape.n, shape.k, x.data(), shape.m, repeats,
+                          ns.data()));
+    push("fp32", "dense", 4.0);
+    for (const std::string& fmt : formats) {
+      QuantConfig cfg;
+      cfg.granularity = Granularity::Groupwise;
+      cfg.group_size = static_cast<int>(std::min<Index>(128, shape.k));
+      cfg.seed = seed;
+      apply_format(cfg, fmt);
+      const QuantizedTensor qt = quantize(w, cfg);
+      const double bpw = storage_bits_per_entry(cfg, shape.n, shape.k) / 8.0;
+      CView v(qt);
+      check(anyq_bench_gemm(1, &v.t, nullptr, shape.n, shape.k, x.data(), shape.m, repeats,
+                            ns.data()));
+      push(fmt, "rowmajor", bpw);
+      if (anyq_bench_gemm(2, &v.t, nullptr, shape.n, shape.k, x.data(), shape.m, repeats,
+                          ns.data()) == ANYQ_OK)
+        push(fmt, "b200", bpw);
+    }
+  }
+  return rows;
+}
+
+std::string bench_csv(const std::vector<BenchRow>& rows) {
+  std::ostringstream os;
+  os << "shape,format,layout,median_ns,p10_ns,p90_ns,bytes_per_weight\n";
+  for (const BenchRow& r : rows)
+    os << r.shape.m << 'x' << r.shape.n << 'x' << r.shape.k << ',' << r.format << ',' << r.layout
+       << ',' << static_cast<uint64_t>(r.median_ns) << ',' << static_cast<uint64_t>(r.p10_ns)
+       << ',' << static_cast<uint64_t>(r.p90_ns) << ',' << r.bytes_per_weight << '\n';
+  return os.str();
 }
 
 }  // namespace anyq

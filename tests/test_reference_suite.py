@@ -48,3 +48,38 @@ def test_reference_suite_on_b200(cuda):
     r = _run(B200_BIN)
     assert r.returncode == 0, (r.stdout[-500:], r.stderr[-4000:])
     assert "76 passed | 0 failed" in r.stdout
+
+
+def _defined(path, demangle=True):
+    """Defined (text, weak, data) symbol names of an object or shared library."""
+    args = ["nm", "--defined-only"] + (["-C"] if demangle else []) + ([] if path.endswith(".o") else ["-D"])
+    out = subprocess.run(args + [path], capture_output=True, text=True, check=True).stdout
+    syms = set()
+    for line in out.splitlines():
+        parts = line.split(" ", 2)
+        if len(parts) == 3 and parts[1] in "TWVBDR":
+            syms.add(parts[2])
+    return syms
+
+
+def test_drop_in_links_no_reference_code():
+    """libanyq_host.so and the B200 test binary are anyq_host.o + libanyq_b200.so
+    only: the Makefile has no rule that pulls (or weakens) reference objects
+    into them, every anyq:: function the .so defines is defined by anyq_host.o,
+    and it exports none of the oracle shim's ref_* entry points."""
+    mk = open(os.path.join(HERE, "reftests", "Makefile")).read()
+    assert "objcopy" not in mk and "weak/" not in mk
+    b200_rule = mk[mk.index("$(B)/anyq_tests_b200:"):mk.index("$(LIBDIR)/libanyq_host.so:")]
+    host_rule = mk[mk.index("$(LIBDIR)/libanyq_host.so:"):mk.index("clean:")]
+    for rule in (b200_rule, host_rule):
+        assert "oracle/_ref" not in rule and "REF_LINK_OBJS" not in rule
+    so = os.path.join(HERE, "..", "paper_2507_04610_b200", "_lib", "libanyq_host.so")
+    obj = os.path.join(BUILD, "anyq_host.o")
+    if not (os.path.exists(so) and os.path.exists(obj)):
+        pytest.skip("drop-in not built (make -C tests/reftests)")
+    lib_syms = {s for s in _defined(so) if s.startswith("anyq::")}
+    obj_syms = {s for s in _defined(obj) if s.startswith("anyq::")}
+    assert lib_syms and lib_syms <= obj_syms, sorted(lib_syms - obj_syms)[:10]
+    assert not any(s.startswith("ref_") for s in _defined(so, demangle=False))
+    needed = subprocess.run(["readelf", "-d", so], capture_output=True, text=True).stdout
+    assert "anyq_ref" not in needed
