@@ -235,10 +235,13 @@ anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
  *   ANYQ_PATH_TC    tensor-core (tcgen05, A in TMEM) LUT GEMM, m <= 16
  *   ANYQ_PATH_DEQUANT  bf16 dequantization + cuBLAS GEMM, any m (large-M path)
  *   ANYQ_PATH_MMA   fused dequant-to-shared-memory + mma.sync, m <= 64 (lutmma.cu)
+ *   ANYQ_PATH_GEMV_TC  K1t: the persistent GEMV chain with the products on
+ *                   tcgen05 (pair-table lookups -> TMEM A operand), m <= 16 (gemv.cu)
  *   ANYQ_PATH_AUTO  GEMV for m <= 4 when its shared-memory plan fits (else
  *                   tcgen05), fused mma for 5 <= m <= 32, dequant above
  *                   (measured crossovers; what anyq_dev_gemm_bf16 uses) */
-enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2, ANYQ_PATH_DEQUANT = 3, ANYQ_PATH_MMA = 4 };
+enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2, ANYQ_PATH_DEQUANT = 3, ANYQ_PATH_MMA = 4,
+       ANYQ_PATH_GEMV_TC = 5 };
 anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                     void* y_bf16, float* y_f32, int32_t path, void* stream);
 /* The path ANYQ_PATH_AUTO takes for this tensor at m rows of x. */
@@ -263,6 +266,14 @@ anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
                                      const void* const* x_bf16, void* const* y_bf16,
                                      float* const* y_f32, const int32_t* deps, int64_t m,
                                      void* stream);
+
+/* Same, with the chain engine chosen explicitly: ANYQ_PATH_GEMV (CUDA-core,
+ * m <= 4), ANYQ_PATH_GEMV_TC (tcgen05, m <= 16) or ANYQ_PATH_AUTO (what
+ * anyq_dev_gemm_chain_deps uses). */
+anyq_status anyq_dev_gemm_chain_path(int32_t n, const anyq_dev_tensor* const* t,
+                                     const void* const* x_bf16, void* const* y_bf16,
+                                     float* const* y_f32, const int32_t* deps, int64_t m,
+                                     int32_t path, void* stream);
 
 /* read_file straight into the prepacked device layout. */
 anyq_status anyq_dev_tensor_load(const char* path, anyq_dev_tensor** out);

@@ -135,6 +135,8 @@ def lib() -> C.CDLL:
                                      C.POINTER(vp), C.POINTER(i32), i64, vp]),
         "anyq_dev_gemm_chain_deps": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                           C.POINTER(vp), C.POINTER(i32), i64, vp]),
+        "anyq_dev_gemm_chain_path": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                          C.POINTER(vp), C.POINTER(i32), i64, i32, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
         "anyq_column_mean_abs": (st, [fptr, i64, i64, fptr]),
         "anyq_write_file": (st, [qt, C.c_char_p]),
@@ -175,7 +177,8 @@ EXPORTED_SYMBOLS = (
     "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
     "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
     "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
-    "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_auto_path", "anyq_dev_quantize_any",
+    "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_chain_path", "anyq_dev_gemm_auto_path",
+    "anyq_dev_quantize_any",
     "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
     "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
@@ -551,7 +554,7 @@ def gemm_fused(x, qt: QuantizedTensor, plan: GemmPlan | None = None) -> np.ndarr
 
 # ---------------------------------------------------------------------------
 # device-resident fast path (LUT GEMV / tensor-core LUT GEMM)
-PATH_AUTO, PATH_GEMV, PATH_TC, PATH_DEQUANT, PATH_MMA = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_GEMV, PATH_TC, PATH_DEQUANT, PATH_MMA, PATH_GEMV_TC = 0, 1, 2, 3, 4, 5
 # ---------------------------------------------------------------------------
 class DeviceTensor:
     """A prepacked any4/int4/nf4/fp4 weight resident in HBM.
@@ -616,13 +619,14 @@ class DeviceTensor:
 
 
 def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None, y32_ptrs=None,
-                    deps=None):
+                    deps=None, path=None):
     """One launch of y_i = x_i W_i^T for a list of DeviceTensors.
 
     deps[i] = j (< i) makes problem i read x_i only after problem j completed
     (x_i is y_j); -1 = no dependency (anyq_dev_gemm_chain_deps). The older
     wait_prev[i] = 1 waits for every earlier problem (anyq_dev_gemm_chain).
-    Pointers are raw device addresses.
+    Pointers are raw device addresses. path (PATH_GEMV / PATH_GEMV_TC /
+    PATH_AUTO) picks the chain engine (anyq_dev_gemm_chain_path).
     """
     n = len(tensors)
     VP = C.c_void_p * n
@@ -630,6 +634,12 @@ def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None
     xs = VP(*x_ptrs)
     ys = VP(*y_ptrs)
     y32 = VP(*[p or 0 for p in y32_ptrs]) if y32_ptrs is not None else None
+    if path is not None:
+        if deps is None:
+            deps = [i - 1 if (wait_prev and i > 0 and wait_prev[i]) else -1 for i in range(n)]
+        d = (C.c_int32 * n)(*deps)
+        _check(lib().anyq_dev_gemm_chain_path(n, t, xs, ys, y32, d, m, path, C.c_void_p(stream)))
+        return
     if deps is not None:
         d = (C.c_int32 * n)(*deps)
         _check(lib().anyq_dev_gemm_chain_deps(n, t, xs, ys, y32, d, m, C.c_void_p(stream)))
@@ -638,7 +648,8 @@ def gemm_chain_ptrs(tensors, x_ptrs, y_ptrs, m: int, stream: int, wait_prev=None
     _check(lib().anyq_dev_gemm_chain(n, t, xs, ys, y32, w, m, C.c_void_p(stream)))
 
 
-def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None, deps=None):
+def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None, deps=None,
+               path=None):
     """gemm_chain_ptrs on torch CUDA tensors; returns the list of y (bf16)."""
     import torch
 
@@ -648,7 +659,7 @@ def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None, dep
     s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
     gemm_chain_ptrs(tensors, [x.data_ptr() for x in xs], [y.data_ptr() for y in ys], m,
                     s.cuda_stream, wait_prev,
-                    [y.data_ptr() for y in y32s] if y32s is not None else None, deps)
+                    [y.data_ptr() for y in y32s] if y32s is not None else None, deps, path)
     return ys
 
 

@@ -137,13 +137,19 @@ StreamWs stream_ws(cudaStream_t s) {
   if (it != table.end()) return it->second;
   StreamWs w{};
   int* block = nullptr;
-  ANYQ_CUDA(cudaMalloc(&block, sizeof(int) * (kWsDone + kWsErr)));
-  // zeroed on a private stream: legal while another stream is being captured
-  cudaStream_t z;
-  ANYQ_CUDA(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking));
-  ANYQ_CUDA(cudaMemsetAsync(block, 0, sizeof(int) * (kWsDone + kWsErr), z));
-  ANYQ_CUDA(cudaStreamSynchronize(z));
-  ANYQ_CUDA(cudaStreamDestroy(z));
+  // The first call on a stream may come while it is being captured into a
+  // graph: allocate in relaxed capture mode (cudaMalloc is otherwise refused
+  // during a global-mode capture) and zero on a private stream.
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  ANYQ_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+  cudaError_t e = cudaMalloc(&block, sizeof(int) * (kWsDone + kWsErr));
+  cudaStream_t z = nullptr;
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemsetAsync(block, 0, sizeof(int) * (kWsDone + kWsErr), z);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(z);
+  if (z) cudaStreamDestroy(z);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  ANYQ_CUDA(e);
   w.done = block;
   w.err = block + kWsDone;
   table.emplace(std::make_pair(dev, s), w);
@@ -727,6 +733,8 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
       dequant_gemm_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else if (path == ANYQ_PATH_MMA)
       lutmma_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_GEMV_TC)
+      lutgemv_tc_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else
       fail(ANYQ_ERR_CONFIG, "unknown GEMM path");
   });
@@ -754,6 +762,23 @@ anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
     if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
     lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
                       m, (cudaStream_t)stream);
+  });
+}
+
+anyq_status anyq_dev_gemm_chain_path(int32_t n, const anyq_dev_tensor* const* t,
+                                     const void* const* x_bf16, void* const* y_bf16,
+                                     float* const* y_f32, const int32_t* deps, int64_t m,
+                                     int32_t path, void* stream) {
+  return guard([&] {
+    if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
+    const auto* ts = reinterpret_cast<const LutTensor* const*>(t);
+    if (path == ANYQ_PATH_AUTO) path = ANYQ_PATH_GEMV;
+    if (path == ANYQ_PATH_GEMV)
+      lutgemv_chain_run(n, ts, x_bf16, y_bf16, y_f32, deps, m, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_GEMV_TC)
+      lutgemv_tc_chain_run(n, ts, x_bf16, y_bf16, y_f32, deps, m, (cudaStream_t)stream);
+    else
+      fail(ANYQ_ERR_CONFIG, "gemm chain: path must be AUTO, GEMV or GEMV_TC");
   });
 }
 

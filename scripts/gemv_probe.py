@@ -56,6 +56,7 @@ def main():
     ap.add_argument("--shapes", default="q,k,gate,down")
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--chain", action="store_true", help="also time the 8B layer as one chain launch")
+    ap.add_argument("--chain-paths", default="1", help="chain engines: 1 = GEMV (K1a), 5 = K1t")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -124,8 +125,8 @@ def main():
         nl = 4
         tens = [[anyq.DeviceTensor(synthetic(n, k, seed=10 * l + i)) for i, (_, n, k) in enumerate(layer)]
                 for l in range(nl)]
-        for m in (int(v) for v in args.ms.split(",")):
-            if m > 4:
+        for m, cpath in ((int(v), int(c)) for v in args.ms.split(",") for c in args.chain_paths.split(",")):
+            if m > (4 if cpath == 1 else 16):
                 continue
             x = torch.randn(m, 4096, device=dev).to(torch.bfloat16)
             ys = [torch.empty(m, n, device=dev, dtype=torch.bfloat16) for _, n, _ in layer]
@@ -138,7 +139,7 @@ def main():
                 with torch.cuda.graph(g, stream=stream):
                     for l in range(nl):
                         anyq.gemm_chain([tens[l][j] for j in order], [xs[j] for j in order],
-                                        [ys[j] for j in order], deps=deps, stream=stream)
+                                        [ys[j] for j in order], deps=deps, stream=stream, path=cpath)
                 reps = 20
                 with torch.cuda.stream(stream):
                     for _ in range(3):
@@ -153,7 +154,7 @@ def main():
                 us = e0.elapsed_time(e1) * 1e3 / (reps * nl)
                 nb = sum(n * k // 2 + n * (k // 128) * 4 + n * 32 + m * k * 2 + m * n * 2 for _, n, k in layer)
                 gbs = nb / (us * 1e-6) / 1e9
-                key = f"layer_chain_m{m}{tag}"
+                key = f"layer_chain_m{m}_p{cpath}{tag}"
                 out[key] = {"us": round(us, 3), "GBps": round(gbs, 1), "pct": round(100 * gbs / peak, 1)}
                 print(key, out[key], flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
