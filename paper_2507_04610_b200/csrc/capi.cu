@@ -706,12 +706,17 @@ int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t) {
 }
 
 int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
-  // measured crossovers on B200 (profiles/round1.md): the GEMV while its x
-  // image fits shared memory (m <= 4; else the tcgen05 kernel), the fused
-  // dequant-to-shared-memory mma.sync kernel for 5 <= m <= 32, dequant +
-  // cuBLAS above
+  // measured crossovers on B200 (profiles/round2_k1t.md): the CUDA-core GEMV
+  // at m = 1 (and m = 2 for fewer than 2 row blocks per SM); K1t (tcgen05
+  // GEMV) for 3 <= m <= 4, and up to m = 16 with at least 2 row blocks per
+  // SM, while its shared-memory plan fits; the fused dequant-to-shared-memory
+  // mma.sync kernel up to m = 32 (it splits K over every SM, which wins on
+  // small N); dequant + cuBLAS above
   const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
+  const bool many_rows = lt->RB >= 2 * lt->sms;
   try {
+    if (m >= 2 && m <= 16 && (many_rows || (m >= 3 && m <= 4)) && lutgemv_tc_fits(lt, m))
+      return ANYQ_PATH_GEMV_TC;
     if (lutgemv_fits(lt, m)) return ANYQ_PATH_GEMV;
   } catch (...) {
   }
@@ -749,8 +754,8 @@ anyq_status anyq_dev_gemm_chain(int32_t n, const anyq_dev_tensor* const* t,
     // "after every earlier problem" == after problem i-1 (problems are released in order)
     int32_t deps[8];
     for (int i = 0; i < n; ++i) deps[i] = (wait_prev && i > 0 && wait_prev[i]) ? i - 1 : -1;
-    lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
-                      m, (cudaStream_t)stream);
+    lutgemv_chain_run_auto(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
+                           m, (cudaStream_t)stream);
   });
 }
 
@@ -760,8 +765,8 @@ anyq_status anyq_dev_gemm_chain_deps(int32_t n, const anyq_dev_tensor* const* t,
                                      void* stream) {
   return guard([&] {
     if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
-    lutgemv_chain_run(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
-                      m, (cudaStream_t)stream);
+    lutgemv_chain_run_auto(n, reinterpret_cast<const LutTensor* const*>(t), x_bf16, y_bf16, y_f32, deps,
+                           m, (cudaStream_t)stream);
   });
 }
 
@@ -772,8 +777,9 @@ anyq_status anyq_dev_gemm_chain_path(int32_t n, const anyq_dev_tensor* const* t,
   return guard([&] {
     if (n < 1 || n > 8 || !t || !x_bf16 || !y_bf16) fail(ANYQ_ERR_SHAPE, "gemm chain: bad arguments");
     const auto* ts = reinterpret_cast<const LutTensor* const*>(t);
-    if (path == ANYQ_PATH_AUTO) path = ANYQ_PATH_GEMV;
-    if (path == ANYQ_PATH_GEMV)
+    if (path == ANYQ_PATH_AUTO)
+      lutgemv_chain_run_auto(n, ts, x_bf16, y_bf16, y_f32, deps, m, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_GEMV)
       lutgemv_chain_run(n, ts, x_bf16, y_bf16, y_f32, deps, m, (cudaStream_t)stream);
     else if (path == ANYQ_PATH_GEMV_TC)
       lutgemv_tc_chain_run(n, ts, x_bf16, y_bf16, y_f32, deps, m, (cudaStream_t)stream);

@@ -1440,15 +1440,12 @@ void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* c
   lc.stream = s;
   lc.attrs = attr;
   lc.numAttrs = 2;
-  {  // debug knobs (experiments): ANYQ_GV_LAUNCH = 1 no cooperative, 2 no PDL, 3 neither
-    static const int knob = std::getenv("ANYQ_GV_LAUNCH") ? std::atoi(std::getenv("ANYQ_GV_LAUNCH")) : 0;
-    if (knob == 1) lc.numAttrs = 1;
-    if (knob == 2) {
-      attr[0] = attr[1];
-      lc.numAttrs = 1;
-    }
-    if (knob == 3) lc.numAttrs = 0;
-  }
+  // Co-residency is only needed when a problem waits for another grid-wide;
+  // an independent launch skips the cooperative attribute (measured 1-2 us
+  // less launch latency). 1 CTA per SM and grid = SM count either way.
+  bool waits = false;
+  for (int i = 0; i < n; ++i) waits |= P.p[i].dep >= 0;
+  if (!waits) lc.numAttrs = 1;
   if constexpr (TC) {
     ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_lutgemv_tc<MP>, P));
   } else {
@@ -1549,6 +1546,26 @@ void lutgemv_tc_chain_run(int n, const LutTensor* const* ts, const void* const* 
     launch_gv<decltype(mp)::value, true>(n, ts, xs, ys, y32s, deps, m, s);
     return 0;
   });
+}
+
+// AUTO engine of a chain (measured, profiles/round2_k1t.md): the CUDA-core
+// GEMV at m <= 2, K1t from m = 3 while its shared-memory plan fits.
+void lutgemv_chain_run_auto(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
+                            float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
+  if (m >= 3 && m <= kTcMaxMP && gv_sbase_ok()) {
+    bool fits = true;
+    try {
+      GvParams P;
+      tc_dispatch(m, [&](auto mp) { return plan_chain<decltype(mp)::value, true>(n, ts, xs, ys, y32s, deps, m, P); });
+    } catch (const Failure&) {
+      fits = false;
+    }
+    if (fits || m > kMaxMP) {
+      lutgemv_tc_chain_run(n, ts, xs, ys, y32s, deps, m, s);
+      return;
+    }
+  }
+  lutgemv_chain_run(n, ts, xs, ys, y32s, deps, m, s);
 }
 
 bool lutgemv_tc_fits(const LutTensor* t, int64_t m) {

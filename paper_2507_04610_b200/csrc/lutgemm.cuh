@@ -42,6 +42,8 @@ void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16
 void lutgemv_tc_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                           float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
 bool lutgemv_tc_fits(const LutTensor* t, int64_t m);
+void lutgemv_chain_run_auto(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
+                            float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
 void lutgemv_tc_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                     cudaStream_t s);
 // 1 <= M <= 64: fused dequant-to-shared-memory + mma.sync LUT GEMM (lutmma.cu).

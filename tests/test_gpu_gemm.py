@@ -226,7 +226,7 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
         # chain: y0 = x0 W0, y1 = x0 W1 (independent), y2 = x2 W2, y3 = y2 W3 (waits on y2)
         ys = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for n, _ in shapes]
         y32 = [torch.empty(m, n, device="cuda", dtype=torch.float32) for n, _ in shapes]
-        aq.gemm_chain(dts, [x0, x0, x2, ys[2]], ys, wait_prev=[0, 0, 1, 1], y32s=y32)
+        aq.gemm_chain(dts, [x0, x0, x2, ys[2]], ys, wait_prev=[0, 0, 1, 1], y32s=y32, path=aq.PATH_GEMV)
         torch.cuda.synchronize()
         xs = [x0, x0, x2, ys[2].clone()]
         for i, d in enumerate(dts):
@@ -238,7 +238,7 @@ def test_gemm_chain_matches_single_launches(aq, orc, cuda):
             assert np.all(np.abs(r.cpu().numpy() - ref) <= tc_tolerance(orc, xs[i].float().cpu().numpy(), qts[i]))
         # repeated launches reuse the self-resetting counters
         for _ in range(3):
-            aq.gemm_chain(dts, [x0, x0, x2, ys[2]], ys, wait_prev=[0, 0, 1, 1])
+            aq.gemm_chain(dts, [x0, x0, x2, ys[2]], ys, wait_prev=[0, 0, 1, 1], path=aq.PATH_GEMV)
         torch.cuda.synchronize()
     for d in dts:
         d.close()
@@ -282,15 +282,16 @@ def test_fused_mma_path(aq, orc, cuda, m, n, k, g):
 
 
 def test_auto_path_choice_and_agreement(aq, orc, cuda):
-    """AUTO: GEMV while its x image fits shared memory (m <= 4), the fused mma
-    kernel for 5 <= m <= 32, dequant + cuBLAS above; a long-K tensor leaves
-    the GEMV at m = 3 for tcgen05. AUTO's output equals the explicit path's
-    output bit for bit."""
+    """AUTO on a small tensor (3 row blocks): GEMV at m <= 2, K1t (tcgen05
+    GEMV) at 3 <= m <= 4, the fused mma kernel for 5 <= m <= 32 (few row
+    blocks), dequant + cuBLAS above; a long-K tensor leaves the GEMV at m = 3
+    for the tcgen05 LUT GEMM; a tall tensor takes K1t from m = 2 to 16. AUTO's
+    output equals the explicit path's output bit for bit."""
     import torch
 
     qt = aq.quantize_any(orc.gaussian(96, 512, 7), cfg(codebook=3, max_iters=4))
     dt = aq.DeviceTensor(qt)
-    expect = {1: aq.PATH_GEMV, 2: aq.PATH_GEMV, 3: aq.PATH_GEMV, 4: aq.PATH_GEMV,
+    expect = {1: aq.PATH_GEMV, 2: aq.PATH_GEMV, 3: aq.PATH_GEMV_TC, 4: aq.PATH_GEMV_TC,
               5: aq.PATH_MMA, 8: aq.PATH_MMA, 32: aq.PATH_MMA, 33: aq.PATH_DEQUANT,
               64: aq.PATH_DEQUANT}
     for m, path in expect.items():
@@ -309,6 +310,9 @@ def test_auto_path_choice_and_agreement(aq, orc, cuda):
     assert long_k.auto_path(1) == aq.PATH_GEMV
     assert long_k.auto_path(3) == aq.PATH_TC
     long_k.close()
+    tall = aq.DeviceTensor(aq.quantize_any(orc.gaussian(300 * 32, 256, 10), cfg(codebook=3, max_iters=2)))
+    assert [tall.auto_path(m) for m in (1, 2, 8, 16, 17)] == [aq.PATH_GEMV] + [aq.PATH_GEMV_TC] * 3 + [aq.PATH_MMA]
+    tall.close()
 
 
 def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):
@@ -331,7 +335,7 @@ def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):
         y32 = [torch.empty(m, n, device="cuda", dtype=torch.float32) for n, _ in shapes]
         xs = [x0 if d < 0 else ys[d] for d in deps]
         for _ in range(3):  # repeated launches reuse the self-resetting counters
-            aq.gemm_chain(dts, xs, ys, y32s=y32, deps=deps)
+            aq.gemm_chain(dts, xs, ys, y32s=y32, deps=deps, path=aq.PATH_GEMV)
         torch.cuda.synchronize()
         for i, d in enumerate(dts):
             xi = (x0 if deps[i] < 0 else ys[deps[i]]).clone()
@@ -373,7 +377,7 @@ def test_gemm_chain_edge_cases(aq, orc, cuda):
         for i, d in enumerate(deps):
             xs.append(ys[d] if d >= 0 else xin[dts[i].cols])
         for _ in range(2):
-            aq.gemm_chain(dts, xs, ys, y32s=y32, deps=deps)
+            aq.gemm_chain(dts, xs, ys, y32s=y32, deps=deps, path=aq.PATH_GEMV)
         torch.cuda.synchronize()
         for i, d in enumerate(dts):
             xi = xs[i].clone()

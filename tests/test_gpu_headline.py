@@ -77,7 +77,7 @@ def check_rows(orc, qt, x, y32, rows, what):
         assert np.all(err <= tol), (what, r0, float(np.max(err / tol)))
 
 
-def run_chain(aq, torch, qts, m, seed):
+def run_chain(aq, torch, qts, m, seed, path=None):
     dts = [aq.DeviceTensor(q) for q in qts]
     x0 = torch.from_numpy(np.random.default_rng(seed).standard_normal((m, qts[0].cols),
                                                                        dtype=np.float32))
@@ -85,7 +85,7 @@ def run_chain(aq, torch, qts, m, seed):
     ys = [torch.empty(m, q.rows, device="cuda", dtype=torch.bfloat16) for q in qts]
     y32 = [torch.empty(m, q.rows, device="cuda", dtype=torch.float32) for q in qts]
     xs = [x0 if d < 0 else ys[d] for d in DEPS]
-    aq.gemm_chain(dts, xs, ys, y32s=y32, deps=DEPS)
+    aq.gemm_chain(dts, xs, ys, y32s=y32, deps=DEPS, path=path)
     torch.cuda.synchronize()
     out = [(xs[i].float().cpu().numpy(), y32[i].cpu().numpy()) for i in range(len(qts))]
     for d in dts:
@@ -103,6 +103,14 @@ def test_llama3_8b_layer_chain(aq, orc, cuda, m):
     qts = [synthetic_qt(n, k, 100 + i) for i, (n, k) in enumerate(LAYER_8B)]
     for i, (x, y) in enumerate(run_chain(aq, cuda, qts, m, 7 + m)):
         check_rows(orc, qts[i], x, y, range(0, qts[i].rows, 2048), f"8b chain m={m} problem {i}")
+
+
+@pytest.mark.parametrize("m", [1, 2])
+def test_llama3_8b_layer_chain_tcgen05(aq, orc, cuda, m):
+    """The same decoder-layer chain on the K1t engine (tcgen05 products)."""
+    qts = [synthetic_qt(n, k, 100 + i) for i, (n, k) in enumerate(LAYER_8B)]
+    for i, (x, y) in enumerate(run_chain(aq, cuda, qts, m, 7 + m, path=aq.PATH_GEMV_TC)):
+        check_rows(orc, qts[i], x, y, range(0, qts[i].rows, 2048), f"8b K1t chain m={m} problem {i}")
 
 
 def test_llama3_70b_layer_chain(aq, orc, cuda):
