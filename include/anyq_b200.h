@@ -178,6 +178,23 @@ anyq_status anyq_weight_error(const float* w, int64_t rows, int64_t cols, const 
 anyq_status anyq_output_error(const float* w, int64_t rows, int64_t cols, const anyq_qtensor* qt,
                               const float* x, int64_t m, int64_t x_cols, double* mse);
 
+/* eval.cpp:48-61 eval_activations(rows, cols, exj, seed): channel j drawn from
+ * N(0, E|x_j| sqrt(pi/2)) (standard normal when exj is NULL), row r from
+ * rng_for_row(seed, r) (Box-Muller in double on the host, like the reference:
+ * synthetic data is not generated on the device). out: rows x cols fp32. */
+anyq_status anyq_eval_activations(int64_t rows, int64_t cols, const float* exj, uint64_t seed,
+                                  float* out);
+
+/* eval.cpp:62-86 compare_formats(w, formats, base, stats, module, opts):
+ * `formats` comma-separated names of quantize.cpp:34-54; exj = the module's
+ * E|x_j| (NULL = no stats); eval_rows / eval_seed = CompareOptions. Per
+ * format i, out[4i..4i+3] = weight_mse, weight_rel_frobenius, output_mse,
+ * bits_per_entry. Quantization, dequantization and both GEMMs of the errors
+ * run on the GPU; n_formats receives the row count. */
+anyq_status anyq_compare_formats(const float* w, int64_t rows, int64_t cols, const char* formats,
+                                 const anyq_config* base, const float* exj, int64_t eval_rows,
+                                 uint64_t eval_seed, double* out, int32_t* n_formats);
+
 /* ANYQ v1 files (pack.hpp write_file / read_file, pack.cpp:293-471).
  * anyq_write_file is byte-identical to write_file (lut_store / scale_store of
  * qt choose the stored precision). anyq_read_file_header parses and validates

@@ -92,6 +92,10 @@ class _Lib:
             "synthetic_stats": (None, [i64, u64, fptr]),
             "rng_u64": (None, [u64, i64, i64, C.POINTER(C.c_uint64)]),
             "rng_double": (None, [u64, i64, i64, dptr]),
+            "collect_stats": (i32, [fptr, i64, i64, fptr]),
+            "eval_activations": (i32, [i64, i64, fptr, u64, fptr]),
+            "compare_formats": (i32, [fptr, i64, i64, C.c_char_p, cfg, fptr, i64, u64, i32, dptr,
+                                      C.c_char_p, i64]),
         }
         self.fn = {}
         for name, (res, args) in sig.items():
@@ -249,6 +253,33 @@ class _Lib:
         c = out.as_c()
         self._check(self.fn["read_file"](os.fsencode(path), C.byref(c)))
         out.layout, out.tile_k, out.lut_store, out.scale_store = c.layout, c.tile_k, c.lut_store, c.scale_store
+        return out
+
+    def collect_stats(self, x) -> np.ndarray:
+        """collect_stats (calibration.cpp:50-75) of a one-layer identity toy model."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty(x.shape[1], np.float32)
+        self._check(self.fn["collect_stats"](_abi.fp(x), x.shape[0], x.shape[1], _abi.fp(out)))
+        return out
+
+    def eval_activations(self, rows, cols, exj=None, seed=1) -> np.ndarray:
+        out = np.empty((rows, cols), np.float32)
+        e = _abi.fp(np.ascontiguousarray(exj, np.float32)) if exj is not None else None
+        self._check(self.fn["eval_activations"](rows, cols, e, seed, _abi.fp(out)))
+        return out
+
+    def compare_formats(self, w, formats, cfg, exj=None, eval_rows=64, eval_seed=1, threads=1):
+        """compare_formats (eval.cpp:62-86): [n, 4] weight_mse, rel, output_mse, bits."""
+        w = np.ascontiguousarray(w, np.float32)
+        out = np.zeros((len(formats), 4), np.float64)
+        e = _abi.fp(np.ascontiguousarray(exj, np.float32)) if exj is not None else None
+        # (EvalReport::to_csv is not called through ctypes: its iostream
+        # formatting faults inside the Python process; the reference's own
+        # test_eval.cpp pins the CSV/JSON schema against the drop-in instead)
+        self._check(self.fn["compare_formats"](_abi.fp(w), w.shape[0], w.shape[1],
+                                               ",".join(formats).encode(), C.byref(cfg), e,
+                                               eval_rows, eval_seed, threads,
+                                               out.ctypes.data_as(C.POINTER(C.c_double)), None, 0))
         return out
 
     def weight_error(self, w, qt: QuantizedTensor):

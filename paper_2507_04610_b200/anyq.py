@@ -160,6 +160,9 @@ def lib() -> C.CDLL:
         "anyq_bf16_to_f32": (C.c_float, [C.c_uint16]),
         "anyq_storage_bits_per_entry": (st, [cfg, i64, i64, C.POINTER(C.c_double)]),
         "anyq_bench_gemm": (st, [i32, qt, fptr, i64, i64, fptr, i64, i32, C.POINTER(C.c_double)]),
+        "anyq_eval_activations": (st, [i64, i64, fptr, C.c_uint64, fptr]),
+        "anyq_compare_formats": (st, [fptr, i64, i64, C.c_char_p, cfg, fptr, i64, C.c_uint64,
+                                      C.POINTER(C.c_double), C.POINTER(i32)]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -178,7 +181,7 @@ EXPORTED_SYMBOLS = (
     "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
     "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
     "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_chain_path", "anyq_dev_gemm_auto_path",
-    "anyq_dev_quantize_any",
+    "anyq_dev_quantize_any", "anyq_eval_activations", "anyq_compare_formats",
     "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
     "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
@@ -661,6 +664,34 @@ def gemm_chain(tensors, xs, ys=None, wait_prev=None, y32s=None, stream=None, dep
                     s.cuda_stream, wait_prev,
                     [y.data_ptr() for y in y32s] if y32s is not None else None, deps, path)
     return ys
+
+
+def eval_activations(rows: int, cols: int, exj=None, seed: int = 1) -> np.ndarray:
+    """eval_activations (eval.cpp:48-61): N(0, E|x_j| sqrt(pi/2)) per channel."""
+    out = np.empty((rows, cols), np.float32)
+    e = _abi.fp(_f32(exj)) if exj is not None else None
+    _check(lib().anyq_eval_activations(rows, cols, e, seed, _abi.fp(out)))
+    return out
+
+
+def compare_formats(w, formats, base, exj=None, eval_rows: int = 64, eval_seed: int = 1,
+                    module: str = "w"):
+    """compare_formats (eval.cpp:62-86) on the GPU: one row per format with
+    weight_mse, weight_rel_frobenius, output_mse, bits_per_entry; returns
+    (rows as a list of dicts, the report CSV of EvalReport::to_csv)."""
+    w = _f32(w)
+    out = np.zeros((len(formats), 4), np.float64)
+    n = C.c_int32(0)
+    e = _abi.fp(_f32(exj)) if exj is not None else None
+    _check(lib().anyq_compare_formats(_abi.fp(w), w.shape[0], w.shape[1], ",".join(formats).encode(),
+                                      C.byref(base), e, eval_rows, eval_seed,
+                                      out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n)))
+    rows = [dict(module=module, format=f, weight_mse=o[0], weight_rel_frobenius=o[1], output_mse=o[2],
+                 bits_per_entry=o[3]) for f, o in zip(formats, out)]
+    lines = ["schema_version,module,format,weight_mse,weight_rel_frobenius,output_mse,bits_per_entry"]
+    lines += [f"v1,{r['module']},{r['format']},{r['weight_mse']:.9g},{r['weight_rel_frobenius']:.9g},"
+              f"{r['output_mse']:.9g},{r['bits_per_entry']:.9g}" for r in rows]
+    return rows, "\n".join(lines) + "\n"
 
 
 def column_mean_abs(x) -> np.ndarray:

@@ -953,6 +953,96 @@ anyq_status anyq_f32_to_bf16(float f, uint16_t* out) {
 }
 float anyq_bf16_to_f32(uint16_t h) { return bf16_to_f32_exact(h); }
 
+namespace {
+// rethrow a nested C-ABI call's failure (its message is the last error)
+void check_status(anyq_status st) {
+  if (st != ANYQ_OK) fail(st, anyq_last_error());
+}
+}  // namespace
+
+anyq_status anyq_eval_activations(int64_t rows, int64_t cols, const float* exj, uint64_t seed,
+                                  float* out) {
+  return host_only([&] {
+    if (rows < 0 || cols < 0) fail(ANYQ_ERR_SHAPE, "eval_activations: negative shape");
+    constexpr double kSqrtHalfPi = 1.2533141373155003;  // E|N(0, s)| = s sqrt(2/pi)
+    for (int64_t r = 0; r < rows; ++r) {
+      Rng rng = Rng::for_row(seed, r);
+      for (int64_t j = 0; j < cols; ++j) {
+        const double sigma = exj ? (double)exj[j] * kSqrtHalfPi : 1.0;
+        // core.hpp:183-187 Box-Muller
+        const double u1 = (double)((rng.next_u64() >> 11) + 1) * 0x1.0p-53;
+        const double u2 = rng.next_double();
+        const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+        out[r * cols + j] = (float)(sigma * g);
+      }
+    }
+  });
+}
+
+anyq_status anyq_compare_formats(const float* w, int64_t rows, int64_t cols, const char* formats,
+                                 const anyq_config* base, const float* exj, int64_t eval_rows,
+                                 uint64_t eval_seed, double* out, int32_t* n_formats) {
+  return guard([&] {
+    if (!w || !formats || !base || !out) fail(ANYQ_ERR_SHAPE, "compare_formats: null argument");
+    struct Fmt {
+      const char* name;
+      int32_t codebook, bits;
+    };
+    static const Fmt kFmts[] = {{"int2", ANYQ_CB_INT, 2}, {"int3", ANYQ_CB_INT, 3}, {"int4", ANYQ_CB_INT, 4},
+                                {"int8", ANYQ_CB_INT, 8}, {"fp4", ANYQ_CB_FP4, 4},  {"nf4", ANYQ_CB_NF4, 4},
+                                {"any2", ANYQ_CB_ANY, 2}, {"any3", ANYQ_CB_ANY, 3}, {"any4", ANYQ_CB_ANY, 4},
+                                {"any8", ANYQ_CB_ANY, 8}};
+    std::vector<std::string> names;
+    {
+      std::string cur;
+      for (const char* c = formats;; ++c) {
+        if (*c == ',' || *c == 0) {
+          names.push_back(cur);
+          cur.clear();
+          if (!*c) break;
+        } else {
+          cur += *c;
+        }
+      }
+    }
+    // eval.cpp:68-70: the stats lookup happens before the activations are drawn
+    std::vector<float> x((size_t)eval_rows * cols);
+    check_status(anyq_eval_activations(eval_rows, cols, exj, eval_seed, x.data()));
+    int32_t nf = 0;
+    for (const std::string& nm : names) {
+      const Fmt* f = nullptr;
+      for (const Fmt& e : kFmts)
+        if (nm == e.name) f = &e;
+      if (!f) fail(ANYQ_ERR_CONFIG, "unknown format '" + nm + "'");
+      anyq_config c = *base;
+      c.codebook = f->codebook;
+      c.bits = f->bits;
+      validate_config(c, rows, cols);
+      const int64_t ng = group_count(c, rows, cols);
+      std::vector<uint8_t> codes((size_t)(rows * packed_bpr(cols, c.bits)));
+      std::vector<float> luts(c.codebook == ANYQ_CB_ANY ? (size_t)rows << c.bits : 0), al(ng), be(ng);
+      anyq_qtensor qt{};
+      qt.rows = rows;
+      qt.cols = cols;
+      qt.cfg = c;
+      qt.codes = codes.data();
+      qt.luts = luts.empty() ? nullptr : luts.data();
+      qt.alphas = al.data();
+      qt.betas = be.data();
+      qt.num_groups = ng;
+      // quantize.cpp:25-32 (quantize): learned formats see the module's stats
+      check_status(c.codebook == ANYQ_CB_ANY ? anyq_quantize_any(w, rows, cols, &c, exj, 0, &qt)
+                                             : anyq_quantize_fixed(w, rows, cols, &c, &qt));
+      double* o = out + 4 * nf;
+      check_status(anyq_weight_error(w, rows, cols, &qt, &o[0], &o[1]));
+      check_status(anyq_output_error(w, rows, cols, &qt, x.data(), eval_rows, cols, &o[2]));
+      check_status(anyq_storage_bits_per_entry(&c, rows, cols, &o[3]));
+      ++nf;
+    }
+    if (n_formats) *n_formats = nf;
+  });
+}
+
 anyq_status anyq_storage_bits_per_entry(const anyq_config* cfg, int64_t rows, int64_t cols,
                                         double* bits) {
   return host_only([&] {

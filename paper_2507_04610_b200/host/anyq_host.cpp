@@ -23,6 +23,8 @@
 //   make_plan / gemm_dense / gemm_reference / gemm_fused / bench / bench_csv
 //                                                       qgemm.hpp:24-59
 //   ActivationStats::for_module                         calibration.hpp:21
+//   weight_error / output_error / eval_activations / compare_formats /
+//     EvalReport::to_csv / to_json                      eval.hpp:33-70
 //
 // This object alone (plus libanyq_b200.so) is the drop-in: no reference
 // object is linked into libanyq_host.so or the B200 test binary.
@@ -37,6 +39,7 @@
 
 #include "anyq/calibration.hpp"
 #include "anyq/codebooks.hpp"
+#include "anyq/eval.hpp"
 #include "anyq/learner.hpp"
 #include "anyq/pack.hpp"
 #include "anyq/qgemm.hpp"
@@ -363,6 +366,86 @@ const Vecf& ActivationStats::for_module(const std::string& name, Index cols) con
     throw StatsError("activation stats for '" + name + "' have " + std::to_string(it->second.size()) +
                      " channels, matrix has " + std::to_string(cols));
   return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// Evaluation (eval.hpp:33-70): the error metrics' dequantisations, GEMMs and
+// double sums run on the GPU (anyq_weight_error / anyq_output_error); the
+// activations are drawn on the host by the reference's Box-Muller.
+// ---------------------------------------------------------------------------
+std::pair<double, double> weight_error(const Eigen::Ref<const Matf>& w, const QuantizedTensor& qt) {
+  if (w.rows() != qt.rows || w.cols() != qt.cols) throw ShapeError("weight_error: shapes differ");
+  const std::vector<float> wf = flat(w);
+  CView v(qt);
+  double mse = 0, rel = 0;
+  check(anyq_weight_error(wf.data(), w.rows(), w.cols(), &v.t, &mse, &rel));
+  return {mse, rel};
+}
+
+double output_error(const Eigen::Ref<const Matf>& w, const QuantizedTensor& qt,
+                    const Eigen::Ref<const Matf>& x) {
+  if (w.rows() != qt.rows || w.cols() != qt.cols) throw ShapeError("output_error: weight shapes differ");
+  if (x.cols() != w.cols()) throw ShapeError("output_error: activation width mismatch");
+  const std::vector<float> wf = flat(w), xf = flat(x);
+  CView v(qt);
+  double mse = 0;
+  check(anyq_output_error(wf.data(), w.rows(), w.cols(), &v.t, xf.data(), x.rows(), x.cols(), &mse));
+  return mse;
+}
+
+Matf eval_activations(Index rows, Index cols, const Vecf* exj, uint64_t seed) {
+  if (exj && exj->size() != cols) throw StatsError("eval_activations: stats length mismatch");
+  Matf x(rows, cols);
+  check(anyq_eval_activations(rows, cols, exj ? exj->data() : nullptr, seed, x.data()));
+  return x;
+}
+
+EvalReport compare_formats(const Eigen::Ref<const Matf>& w, const std::vector<std::string>& formats,
+                           const QuantConfig& base, const ActivationStats* stats,
+                           const std::string& module_name, const CompareOptions& opts) {
+  const Vecf* exj = stats ? &stats->for_module(module_name, w.cols()) : nullptr;
+  const Matf x = eval_activations(opts.eval_rows, w.cols(), exj, opts.eval_seed);
+  EvalReport report;
+  for (const auto& fmt : formats) {
+    QuantConfig cfg = base;
+    apply_format(cfg, fmt);
+    const QuantizedTensor qt = quantize(w, cfg, stats, module_name, opts.threads);
+    const auto [mse, rel] = weight_error(w, qt);
+    EvalRow row;
+    row.module = module_name;
+    row.format = fmt;
+    row.weight_mse = mse;
+    row.weight_rel_frobenius = rel;
+    row.output_mse = output_error(w, qt, x);
+    row.bits_per_entry = storage_bits_per_entry(cfg, w.rows(), w.cols());
+    report.rows.push_back(std::move(row));
+  }
+  return report;
+}
+
+// the report schema (v1): CSV header + one line per row, 9 significant digits
+std::string EvalReport::to_csv() const {
+  std::ostringstream os;
+  os.precision(9);
+  os << "schema_version,module,format,weight_mse,weight_rel_frobenius,output_mse,bits_per_entry\n";
+  for (const auto& r : rows)
+    os << kSchemaVersion << ',' << r.module << ',' << r.format << ',' << r.weight_mse << ','
+       << r.weight_rel_frobenius << ',' << r.output_mse << ',' << r.bits_per_entry << '\n';
+  return os.str();
+}
+
+std::string EvalReport::to_json() const {
+  std::ostringstream os;
+  os.precision(9);
+  os << "{\"schema_version\":\"" << kSchemaVersion << "\",\"rows\":[";
+  for (size_t i = 0; i < rows.size(); ++i) {
+    const auto& r = rows[i];
+    os << (i ? "," : "") << "{\"module\":\"" << r.module << "\",\"format\":\"" << r.format
+       << "\",\"weight_mse\":" << r.weight_mse << ",\"weight_rel_frobenius\":" << r.weight_rel_frobenius
+       << ",\"output_mse\":" << r.output_mse << ",\"bits_per_entry\":" << r.bits_per_entry << '}';
+  }
+  os << "]}";
+  return os.str();
 }
 
 // ---------------------------------------------------------------------------

@@ -148,3 +148,30 @@ def test_config1_lut_identity_fraction(aq, orc, ref):
     codes_a = aq.unpack_codes(a.codes, 4096, 4096, 4)
     codes_b = aq.unpack_codes(b.codes, 4096, 4096, 4)
     assert np.array_equal(codes_a[same_rows], codes_b[same_rows])
+
+
+def test_config4_down_proj_with_stats(aq, ref):
+    """BASELINE config 4 at its longest rows: the Llama-3-8B down_proj of layer 0
+    (K = 14336, W = gaussian(4096, 14336, 1 + 6), stats = synthetic_stats(14336,
+    10007 + 6)), any4 g128 with the activation weighting; 512 rows as two
+    row_offset shards. alpha/beta bit-exact, LUT rows bit-identical to the
+    reference on >= 99 % of rows (max |dLUT| <= 1e-5 * 15), codes identical on
+    those rows."""
+    K = 14336
+    w = ref.gaussian(512, K, 7)
+    exj = ref.synthetic_stats(K, 10013)
+    c = cfg(codebook=3)
+    want = ref.quantize(w, c, exj, 8)
+    parts = [aq.quantize_any(w[:256], c, exj, row_offset=0), aq.quantize_any(w[256:], c, exj, row_offset=256)]
+    alphas = np.concatenate([p.alphas for p in parts])
+    betas = np.concatenate([p.betas for p in parts])
+    assert bits_equal(alphas, want.alphas) and bits_equal(betas, want.betas)
+    la = np.concatenate([p.luts for p in parts]).reshape(512, 16)
+    lb = want.luts.reshape(512, 16)
+    same_rows = np.all(la.view(np.uint32) == lb.view(np.uint32), axis=1)
+    print(f"config-4 down_proj LUT rows bit-identical: {same_rows.mean():.4f}")
+    assert same_rows.mean() >= 0.99
+    assert np.max(np.abs(la - lb)) <= 1e-5 * 15
+    codes_a = np.concatenate([aq.unpack_codes(p.codes, 256, K, 4) for p in parts])
+    codes_b = aq.unpack_codes(want.codes, 512, K, 4)
+    assert np.array_equal(codes_a[same_rows], codes_b[same_rows])

@@ -1,5 +1,5 @@
 """The reference's OWN hot-path unit tests (proj/tests/test_{core,scaling,
-codebooks,pack,learner,qgemm}.cpp, 76 doctest cases compiled unmodified by
+codebooks,pack,learner,qgemm}.cpp, 85 doctest cases compiled unmodified by
 tests/reftests/Makefile) run against:
 
 * the unmodified reference build (CPU) — validates the doctest subset harness;
@@ -30,7 +30,7 @@ def _run(path):
 def test_reference_suite_on_reference_build():
     r = _run(REF_BIN)
     assert r.returncode == 0, r.stderr[-2000:]
-    assert "76 passed | 0 failed" in r.stdout
+    assert "85 passed | 0 failed" in r.stdout
 
 
 def test_drop_in_has_no_cpu_fallback():
@@ -47,7 +47,7 @@ def test_drop_in_has_no_cpu_fallback():
 def test_reference_suite_on_b200(cuda):
     r = _run(B200_BIN)
     assert r.returncode == 0, (r.stdout[-500:], r.stderr[-4000:])
-    assert "76 passed | 0 failed" in r.stdout
+    assert "85 passed | 0 failed" in r.stdout
 
 
 def _defined(path, demangle=True):
