@@ -260,6 +260,43 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def kmeans_cpu_baseline(layer):
+    """Reference quantize_any on the host cores, stratified one-layer sample."""
+    from oracle.refpy import _abi, have_ref, oracle, ref
+
+    lib = ref() if have_ref() else oracle()
+    kind = "reference" if have_ref() else "port"
+    threads = os.cpu_count() or 1
+    cfg = _abi.default_config(codebook=_abi.CB_ANY)
+    rates = {}
+    for k, rows in ((4096, 2048), (14336, 512)):
+        w = lib.gaussian(rows, k, 1)
+        exj = lib.synthetic_stats(k, 10007)
+        secs = lib.time_quantize(w, cfg, exj, threads)
+        rates[k] = rows / secs
+    lrows = sum(n for (_, n, _) in layer)
+    layer_s = sum(n / rates[k] for (_, n, k) in layer)
+    return {"value": round(lrows / layer_s, 1), "unit": "rows/s", "cores": threads, "kind": kind,
+            "rows_per_s_by_K": {str(k): round(v, 1) for k, v in rates.items()},
+            "sample": "reference quantize_any (learner.cpp:392-448), any4 g128 with synthetic stats, "
+                      f"{threads} threads: 2048 rows x 4096 and 512 rows x 14336, one 8B layer "
+                      "(38912 rows at K=4096, 4096 at K=14336) extrapolated from the two rates"}
+
+
+def kmeans_roofline():
+    """The k-means kernel's bound from its committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_kmeans.json")
+    try:
+        m = json.load(open(path))["metrics"]
+        fp64 = float(m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]["value"]) / 100
+        issue = float(m["sm__issue_active.avg.pct_of_peak_sustained_elapsed"]["value"]) / 100
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"bound": "fp64 pipe", "frac": round(fp64, 4), "issue_active": round(issue, 4),
+            "source": "profiles/ncu_kmeans.json (k_kmeans_warp, config 1): FP64 pipe busy fraction; "
+                      "the kernel is latency/barrier bound (stalls: wait, barrier)"}
+
+
 def cpu_baseline_sample():
     """Reference CPU GEMM on a bounded sample (q-proj shape, M=1, 1 core)."""
     from oracle.refpy import have_ref, oracle, ref
@@ -642,6 +679,15 @@ def gpu_arm(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             lsecs = float(t.item())
         lrows = sum(n for (_, n, _) in LAYER)
+        # the reference's CPU quantizer (learner.cpp:392-448, quantize_any with
+        # threads = every host core) on a stratified sample of the same layer:
+        # 2048 rows at K = 4096 and 512 rows at K = 14336, both with synthetic
+        # stats; the layer time is extrapolated from the two per-K row rates
+        if rank == 0 and not args.no_cpu:
+            kmeans["cpu_baseline"] = kmeans_cpu_baseline(LAYER)
+        # bound: the FP64 pipe (the E-step is a boundary search, the M-step FP64
+        # sums in the reference's order; latency/barrier bound, ncu summary)
+        kmeans["roofline"] = kmeans_roofline()
         kmeans["layer"] = {"rows_per_s": round(lrows / lsecs, 1), "rows": lrows,
                            "weights": sum(n * k for (_, n, k) in LAYER),
                            "seconds": round(lsecs, 4),

@@ -93,6 +93,8 @@ class _Lib:
             "rng_u64": (None, [u64, i64, i64, C.POINTER(C.c_uint64)]),
             "rng_double": (None, [u64, i64, i64, dptr]),
             "collect_stats": (i32, [fptr, i64, i64, fptr]),
+            "bench": (i32, [i32, C.POINTER(C.c_int64), C.c_char_p, i32, u64, dptr, C.POINTER(C.c_int),
+                            C.POINTER(C.c_int)]),
             "eval_activations": (i32, [i64, i64, fptr, u64, fptr]),
             "compare_formats": (i32, [fptr, i64, i64, C.c_char_p, cfg, fptr, i64, u64, i32, dptr,
                                       C.c_char_p, i64]),
@@ -254,6 +256,22 @@ class _Lib:
         self._check(self.fn["read_file"](os.fsencode(path), C.byref(c)))
         out.layout, out.tile_k, out.lut_store, out.scale_store = c.layout, c.tile_k, c.lut_store, c.scale_store
         return out
+
+    def bench(self, shapes, formats, repeats=3, seed=1):
+        """qgemm.cpp bench(): [(shape, format, layout, median, p10, p90, bytes_per_weight)]."""
+        mnk = (C.c_int64 * (3 * len(shapes)))(*[v for s in shapes for v in s])
+        nmax = len(shapes) * (len(formats) + 1)
+        out = np.zeros((nmax, 4), np.float64)
+        lay = (C.c_int * nmax)()
+        n = C.c_int(0)
+        self._check(self.fn["bench"](len(shapes), mnk, ",".join(formats).encode(), repeats, seed,
+                                     out.ctypes.data_as(C.POINTER(C.c_double)), lay, C.byref(n)))
+        rows, i = [], 0
+        for s in shapes:
+            for f in ["fp32"] + list(formats):
+                rows.append((s, f, "dense" if lay[i] == 0 else "rowmajor", *out[i]))
+                i += 1
+        return rows[: n.value]
 
     def collect_stats(self, x) -> np.ndarray:
         """collect_stats (calibration.cpp:50-75) of a one-layer identity toy model."""

@@ -1105,6 +1105,7 @@ anyq_status anyq_bench_gemm(int32_t kind, const anyq_qtensor* qt, const float* w
       } else {
         const int path = anyq_dev_gemm_auto_path(reinterpret_cast<anyq_dev_tensor*>(lt), m);
         if (path == ANYQ_PATH_GEMV) lutgemv_run(lt, xb.p, m, yb.p, dy.p, s);
+        else if (path == ANYQ_PATH_GEMV_TC) lutgemv_tc_run(lt, xb.p, m, yb.p, dy.p, s);
         else if (path == ANYQ_PATH_MMA) lutmma_run(lt, xb.p, m, yb.p, dy.p, s);
         else if (path == ANYQ_PATH_TC) lutgemm_run(lt, xb.p, m, yb.p, dy.p, s);
         else dequant_gemm_run(lt, xb.p, m, yb.p, dy.p, s);

@@ -349,6 +349,206 @@ __global__ void k_gemm_exact(const float* __restrict__ x, int64_t m, int64_t k,
   y[r * n + i] = acc;
 }
 
+// The same bit-exact semantics, fast path (<= 4-bit codes, tensorwise /
+// rowwise / groupwise scales). Each output is ONE k-ascending chain of fadd
+// (no contraction) — the reference's — and only that chain is sequential:
+// the weights alpha*T[c]+beta and the products x*w are independent per k.
+// The codes are first rewritten as one byte per weight in 1-KB tiles
+// [row block][k tile][32 rows][32 k] (k_tile_codes) and x as 1-KB tiles
+// [x chunk][k tile][8 rows][32 k], so each tile is ONE cp.async.bulk into an
+// 8-stage shared-memory ring. A CTA owns 32 W rows and up to 8 x rows: 4
+// producer warps turn tile t + 1 into products ([x row][k][W row], warp w:
+// k = 8w..8w+7, lane = W row) while the adder warp (lane = W row) folds tile
+// t into its accumulators in k order; one CTA barrier per tile.
+constexpr int kExRows = 32, kExKT = 32, kExMC = 8, kExProd = 4, kExStages = 8;
+constexpr int kExThreads = (kExProd + 1) * 32;
+constexpr uint32_t kExTile = 1024;  // bytes of a code tile, and of an x tile (8 x 32 fp32)
+
+__global__ void k_tile_codes(const uint8_t* __restrict__ packed, int64_t rows, int64_t cols, int bits,
+                             int ktiled, int64_t tile_k, uint8_t* __restrict__ out) {
+  // one thread per (row, 32-k tile): 32 logical codes of the row
+  const int64_t nt = (cols + kExKT - 1) / kExKT, rb_n = (rows + kExRows - 1) / kExRows;
+  const int64_t bpr = (cols * bits + 7) / 8;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rb_n * kExRows * nt;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e % nt, rr = e / nt;  // rr = global row (incl. padding)
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (rr < rows) {
+      const uint8_t* row = packed + rr * bpr;
+      for (int kk = 0; kk < kExKT; ++kk) {
+        const int64_t j = t * kExKT + kk;
+        if (j < cols) {
+          const int64_t pos = ktiled ? ktiled_pos(j, cols, tile_k) : j;
+          w[kk >> 2] |= code_at(row, pos, bits) << (8 * (kk & 3));
+        }
+      }
+    }
+    uint4* d = reinterpret_cast<uint4*>(out + (((rr / kExRows) * nt + t) * kExRows + rr % kExRows) * kExKT);
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+}
+
+__global__ void k_tile_x(const float* __restrict__ x, int64_t m, int64_t k, float* __restrict__ out) {
+  const int64_t nt = (k + kExKT - 1) / kExKT, mch = (m + kExMC - 1) / kExMC;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mch * nt * kExMC * kExKT;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int kk = (int)(e % kExKT), q = (int)((e / kExKT) % kExMC);
+    const int64_t t = (e / (kExKT * kExMC)) % nt, c = e / (kExKT * kExMC * nt);
+    const int64_t r = c * kExMC + q, j = t * kExKT + kk;
+    out[e] = (r < m && j < k) ? x[r * k + j] : 0.0f;
+  }
+}
+
+template <int MCT>  // x rows this instance carries (1, 2, 4 or 8; the chunk's rows beyond m are zero)
+__global__ void __launch_bounds__(kExThreads) k_gemm_exact_fast(
+    const float* __restrict__ xt, int64_t m, int64_t k, const uint8_t* __restrict__ ctile, int64_t n,
+    const float* __restrict__ luts, int lut_n, Table fixed, GroupMap gm, const float* __restrict__ alphas,
+    const float* __restrict__ betas, float* __restrict__ y, int* err) {
+  extern __shared__ __align__(128) uint8_t ex_smem[];
+  float* prod = reinterpret_cast<float*>(ex_smem);                            // [2][kExMC][kExKT][32]
+  uint8_t* ring = ex_smem + 2 * kExMC * kExKT * 32 * 4;                        // [stages][codes 1 KB | x 1 KB]
+  float* st = reinterpret_cast<float*>(ring + kExStages * 2 * kExTile);        // [32][17]
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + 32 * 17);                  // [stages]
+  uint64_t* empty = full + kExStages;                                          // [stages]
+  float2* sab = reinterpret_cast<float2*>(empty + kExStages);                  // [32][gloc] (alpha, beta)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i0 = (int64_t)blockIdx.x * kExRows, i = i0 + lane;
+  const int64_t mchunk = blockIdx.y, r0 = mchunk * kExMC;
+  const int mc = (int)(m - r0 < kExMC ? m - r0 : kExMC);
+  const int tsize = luts ? lut_n : fixed.n;
+  const bool live = i < n;
+  const int ntiles = (int)((k + kExKT - 1) / kExKT);
+  const bool tile_groups = gm.granularity != ANYQ_G_GROUP || gm.group_size % kExKT == 0;
+  const uint8_t* cbase = ctile + (int64_t)blockIdx.x * ntiles * kExTile;
+  const uint8_t* xbase = reinterpret_cast<const uint8_t*>(xt) + mchunk * ntiles * kExTile;
+  const uint32_t sring = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t sfull = (uint32_t)__cvta_generic_to_shared(full), sempty = (uint32_t)__cvta_generic_to_shared(empty);
+  for (int e = threadIdx.x; e < kExRows * 16; e += kExThreads) {
+    const int rr = e >> 4, c = e & 15;
+    float v = 0.0f;
+    if (c < tsize) v = luts ? (i0 + rr < n ? luts[(i0 + rr) * lut_n + c] : 0.0f) : fixed.v[c];
+    st[rr * 17 + c] = v;
+  }
+  // the rows' scale groups (tensorwise / rowwise: 1, groupwise: ceil(K / g)) in shared memory
+  const int gloc = gm.granularity == ANYQ_G_GROUP ? (int)gm.gpr : 1;
+  for (int e = threadIdx.x; e < kExRows * gloc; e += kExThreads) {
+    const int rr = e / gloc, gg = e % gloc;
+    float2 v = make_float2(1.0f, 0.0f);
+    if (i0 + rr < n) {
+      const int64_t g = gm.granularity == ANYQ_G_GROUP ? (i0 + rr) * gm.gpr + gg : gm(i0 + rr, 0);
+      v = make_float2(alphas[g], betas[g]);
+    }
+    sab[e] = v;
+  }
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < kExStages; ++j) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sfull + 8 * j), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sempty + 8 * j), "r"(kExProd));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int t) {  // one thread: tile t's codes and x into stage t % stages
+    const int s2 = t % kExStages;
+    const uint32_t bar = sfull + 8 * s2, dst = sring + s2 * 2 * kExTile;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * kExTile) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(cbase + (int64_t)t * kExTile), "r"(kExTile), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst + kExTile),
+                 "l"(xbase + (int64_t)t * kExTile), "r"(kExTile), "r"(bar)
+                 : "memory");
+  };
+  auto wait = [&](uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(ok)
+                   : "r"(bar), "r"(parity), "r"(0x989680)
+                   : "memory");
+  };
+  uint32_t bad = 0;
+  auto produce = [&](int t) {
+    const int s2 = t % kExStages;
+    wait(sfull + 8 * s2, (uint32_t)((t / kExStages) & 1));
+    const uint8_t* sc = ring + s2 * 2 * kExTile;
+    const float* sx = reinterpret_cast<const float*>(sc + kExTile);
+    float* pb = prod + (t & 1) * kExMC * kExKT * 32;
+    const int64_t k0 = (int64_t)t * kExKT;
+    if (live) {
+      const uint32_t w0 = *reinterpret_cast<const uint32_t*>(sc + lane * kExKT + warp * 8);
+      const uint32_t w1 = *reinterpret_cast<const uint32_t*>(sc + lane * kExKT + warp * 8 + 4);
+      float2 ab = make_float2(1.0f, 0.0f);
+      if (tile_groups) ab = sab[lane * gloc + (gloc > 1 ? (int)(k0 / gm.group_size) : 0)];
+      // all loads of the 8 k first (table values, x broadcasts), then the arithmetic
+      float tv[8], wv[8];
+      float2 abk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t j = k0 + warp * 8 + u;
+        uint32_t c = ((u < 4 ? w0 : w1) >> (8 * (u & 3))) & 0xFFu;
+        bad |= (uint32_t)(j < k && (int)c >= tsize);
+        c = (int)c >= tsize ? 0u : c;
+        tv[u] = st[lane * 17 + c];
+        abk[u] = tile_groups ? ab : sab[lane * gloc + (j < k ? (int)(j / gm.group_size) : 0)];
+      }
+      float xv[MCT][8];
+#pragma unroll
+      for (int q = 0; q < MCT; ++q) {
+        const float4 x0 = *reinterpret_cast<const float4*>(sx + q * kExKT + warp * 8);
+        const float4 x1 = *reinterpret_cast<const float4*>(sx + q * kExKT + warp * 8 + 4);
+        xv[q][0] = x0.x; xv[q][1] = x0.y; xv[q][2] = x0.z; xv[q][3] = x0.w;
+        xv[q][4] = x1.x; xv[q][5] = x1.y; xv[q][6] = x1.z; xv[q][7] = x1.w;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = __fadd_rn(__fmul_rn(abk[u].x, tv[u]), abk[u].y);
+#pragma unroll
+      for (int q = 0; q < MCT; ++q)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pb[(q * kExKT + warp * 8 + u) * 32 + lane] = __fmul_rn(xv[q][u], wv[u]);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sempty + 8 * s2) : "memory");
+    // the issuing thread refills this stage with tile t + stages once all 4 producers read it
+    if (threadIdx.x == 0 && t + kExStages < ntiles) {
+      wait(sempty + 8 * s2, (uint32_t)((t / kExStages) & 1));
+      issue(t + kExStages);
+    }
+  };
+  float acc[kExMC];
+#pragma unroll
+  for (int q = 0; q < kExMC; ++q) acc[q] = 0.0f;
+  if (threadIdx.x == 0)
+    for (int t = 0; t < kExStages && t < ntiles; ++t) issue(t);
+  if (warp < kExProd) produce(0);
+  __syncthreads();
+  for (int t = 0; t < ntiles; ++t) {
+    if (warp < kExProd) {
+      if (t + 1 < ntiles) produce(t + 1);
+    } else {
+      const float* pb = prod + (t & 1) * kExMC * kExKT * 32;
+      const int kt = (int)(k - (int64_t)t * kExKT < kExKT ? k - (int64_t)t * kExKT : kExKT);
+      if (kt == kExKT) {
+#pragma unroll
+        for (int kk = 0; kk < kExKT; ++kk)
+#pragma unroll
+          for (int q = 0; q < MCT; ++q) acc[q] = __fadd_rn(acc[q], pb[(q * kExKT + kk) * 32 + lane]);
+      } else {  // the ragged last tile: the chain stops at k (no +0 terms)
+        for (int q = 0; q < mc; ++q)
+          for (int kk = 0; kk < kt; ++kk) acc[q] = __fadd_rn(acc[q], pb[(q * kExKT + kk) * 32 + lane]);
+      }
+    }
+    __syncthreads();
+  }
+  if (warp < kExProd) {
+    if (bad) dev_fail(err, ANYQ_ERR_CODE_RANGE);
+  } else if (live) {
+    for (int q = 0; q < mc; ++q) y[(r0 + q) * n + i] = acc[q];
+  }
+}
+
 // gemm_dense (qgemm.cpp:22-34), same order and rounding.
 __global__ void k_gemm_dense(const float* __restrict__ x, int64_t m, const float* __restrict__ w,
                              int64_t n, int64_t k, float* __restrict__ y) {
@@ -502,6 +702,35 @@ void launch_gemm_exact(const float* x, int64_t m, int64_t k, const uint8_t* pack
                        const anyq_config& cfg, const float* alphas, const float* betas, float* y,
                        int* err, cudaStream_t s) {
   GroupMap gm = make_group_map(cfg, k);
+  const int lut_n = 1 << bits;
+  const bool fast_gran = cfg.granularity == ANYQ_G_TENSOR || cfg.granularity == ANYQ_G_ROW ||
+                         cfg.granularity == ANYQ_G_GROUP;
+  const int64_t gl = cfg.granularity == ANYQ_G_GROUP ? gm.gpr : 1;
+  if (bits <= 4 && fast_gran && n > 0 && m > 0 && k > 0 && gl <= 512) {
+    // codes and x in 1-KB tiles (zero padded; the adder stops at k), then the fast kernel
+    const int64_t nt = (k + kExKT - 1) / kExKT, rbn = (n + kExRows - 1) / kExRows;
+    const int64_t mch = (m + kExMC - 1) / kExMC;
+    DevBuf<uint8_t> ct((size_t)(rbn * nt * kExTile), s);
+    DevBuf<float> xt((size_t)(mch * nt * kExMC * kExKT), s);
+    k_tile_codes<<<grid_for(rbn * kExRows * nt), 256, 0, s>>>(packed, n, k, bits, ktiled, tile_k, ct.p);
+    ANYQ_LAUNCHED();
+    k_tile_x<<<grid_for(mch * nt * kExMC * kExKT), 256, 0, s>>>(x, m, k, xt.p);
+    ANYQ_LAUNCHED();
+    dim3 grid((unsigned)rbn, (unsigned)mch);
+    const int gloc = cfg.granularity == ANYQ_G_GROUP ? (int)gm.gpr : 1;
+    const int smem = (int)(2 * kExMC * kExKT * 32 * 4 + kExStages * 2 * kExTile + 32 * 17 * 4 + 2 * kExStages * 8 +
+                           32 * gloc * 8);
+    auto go = [&](auto kern) {
+      ensure_dyn_smem((const void*)kern, smem);
+      kern<<<grid, kExThreads, smem, s>>>(xt.p, m, k, ct.p, n, luts, lut_n, fixed, gm, alphas, betas, y, err);
+    };
+    if (m == 1) go(k_gemm_exact_fast<1>);
+    else if (m == 2) go(k_gemm_exact_fast<2>);
+    else if (m <= 4) go(k_gemm_exact_fast<4>);
+    else go(k_gemm_exact_fast<8>);
+    ANYQ_LAUNCHED();
+    return;
+  }
   dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);
   k_gemm_exact<<<grid, 128, 0, s>>>(x, m, k, packed, n, bits, ktiled, tile_k, luts, fixed, gm,
                                     alphas, betas, y, err);
