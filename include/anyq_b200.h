@@ -254,11 +254,13 @@ anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16,
  *   ANYQ_PATH_MMA   fused dequant-to-shared-memory + mma.sync, m <= 64 (lutmma.cu)
  *   ANYQ_PATH_GEMV_TC  K1t: the persistent GEMV chain with the products on
  *                   tcgen05 (pair-table lookups -> TMEM A operand), m <= 16 (gemv.cu)
+ *   ANYQ_PATH_K2    large M: dequantise to bf16 in shared memory, tcgen05
+ *                   (A and B from shared memory, x by TMA), lutgemm2.cu
  *   ANYQ_PATH_AUTO  GEMV for m <= 4 when its shared-memory plan fits (else
  *                   tcgen05), fused mma for 5 <= m <= 32, dequant above
  *                   (measured crossovers; what anyq_dev_gemm_bf16 uses) */
 enum { ANYQ_PATH_AUTO = 0, ANYQ_PATH_GEMV = 1, ANYQ_PATH_TC = 2, ANYQ_PATH_DEQUANT = 3, ANYQ_PATH_MMA = 4,
-       ANYQ_PATH_GEMV_TC = 5 };
+       ANYQ_PATH_GEMV_TC = 5, ANYQ_PATH_K2 = 6 };
 anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                     void* y_bf16, float* y_f32, int32_t path, void* stream);
 /* The path ANYQ_PATH_AUTO takes for this tensor at m rows of x. */

@@ -557,7 +557,7 @@ def gemm_fused(x, qt: QuantizedTensor, plan: GemmPlan | None = None) -> np.ndarr
 
 # ---------------------------------------------------------------------------
 # device-resident fast path (LUT GEMV / tensor-core LUT GEMM)
-PATH_AUTO, PATH_GEMV, PATH_TC, PATH_DEQUANT, PATH_MMA, PATH_GEMV_TC = 0, 1, 2, 3, 4, 5
+PATH_AUTO, PATH_GEMV, PATH_TC, PATH_DEQUANT, PATH_MMA, PATH_GEMV_TC, PATH_K2 = 0, 1, 2, 3, 4, 5, 6
 # ---------------------------------------------------------------------------
 class DeviceTensor:
     """A prepacked any4/int4/nf4/fp4 weight resident in HBM.

@@ -740,6 +740,8 @@ anyq_status anyq_dev_gemm_bf16_path(const anyq_dev_tensor* t, const void* x_bf16
       lutmma_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else if (path == ANYQ_PATH_GEMV_TC)
       lutgemv_tc_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
+    else if (path == ANYQ_PATH_K2)
+      lutgemm_k2_run(lt, x_bf16, m, y_bf16, y_f32, (cudaStream_t)stream);
     else
       fail(ANYQ_ERR_CONFIG, "unknown GEMM path");
   });
@@ -1106,6 +1108,7 @@ anyq_status anyq_bench_gemm(int32_t kind, const anyq_qtensor* qt, const float* w
         const int path = anyq_dev_gemm_auto_path(reinterpret_cast<anyq_dev_tensor*>(lt), m);
         if (path == ANYQ_PATH_GEMV) lutgemv_run(lt, xb.p, m, yb.p, dy.p, s);
         else if (path == ANYQ_PATH_GEMV_TC) lutgemv_tc_run(lt, xb.p, m, yb.p, dy.p, s);
+        else if (path == ANYQ_PATH_K2) lutgemm_k2_run(lt, xb.p, m, yb.p, dy.p, s);
         else if (path == ANYQ_PATH_MMA) lutmma_run(lt, xb.p, m, yb.p, dy.p, s);
         else if (path == ANYQ_PATH_TC) lutgemm_run(lt, xb.p, m, yb.p, dy.p, s);
         else dequant_gemm_run(lt, xb.p, m, yb.p, dy.p, s);
