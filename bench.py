@@ -589,7 +589,7 @@ def gpu_arm(args):
                                           "TFLOPs": round(tf, 1),
                                           "pct_bf16_peak": round(100 * tf / tpeak, 2),
                                           "path": {1: "gemv", 2: "tcgen05", 3: "dequant+cublas",
-                                                   4: "fused-mma", 5: "gemv-tcgen05"}[
+                                                   4: "fused-mma", 5: "gemv-tcgen05", 6: "k2-tcgen05"}[
                                               layers[0][j][3].auto_path(mm)]}
 
     # ---- config 5 variants: int4 / nf4 (fixed tables) and any3 (3-bit codes on

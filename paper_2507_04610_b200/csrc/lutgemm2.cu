@@ -10,17 +10,18 @@
 // A CTA computes 128 W rows x NT tokens tiles (persistent, round-robin over the
 // tiles, tokens innermost so concurrently running CTAs share the weight rows in
 // L2). Per 128-k step:
-//  * a producer lane issues the x tile as two TMA tensor loads (box 64 k x NT
-//    tokens, SWIZZLE_128B: the canonical UMMA K-major layout) and the step's
-//    codes (4 row blocks x 2 KB of the prepacked layout) and alpha/beta lines
-//    as bulk copies, all on one mbarrier, into a 2-stage ring;
-//  * 16 dequant warps (row block q = warp & 3, k quarter j = warp >> 2; lane =
-//    row) build a private 16-entry bf16 table bf16(alpha * T[i] + beta) of
-//    their row for the step, then look each code up (one LDS.U16 per weight)
-//    and store the bf16 pairs as the A operand in the canonical K-major
-//    no-swizzle layout (per 16-k slice [8-row group][k half][8 rows][16 B]);
+//  * an x producer lane issues the x tile as two TMA tensor loads (box 64 k x
+//    NT tokens, SWIZZLE_128B: the canonical UMMA K-major layout) into a 4-6
+//    stage ring; a code producer lane streams the step's codes (4 row blocks x
+//    2 KB of the prepacked layout) and alpha/beta lines by bulk copies into an
+//    8-stage ring (the weight stream is the HBM-latency-bound one);
+//  * 16 dequant warps (row block q = warp & 3 = TMEM lane quarter, k quarter
+//    j = warp >> 2; lane = row) build a private 16-entry bf16 table
+//    bf16(alpha * T[i] + beta) of their row for the step, look each code up
+//    (one LDS.U16 per weight) and store the bf16 pairs straight into TMEM as
+//    the A operand (tcgen05.st; 4 A stages of 64 columns);
 //  * one thread issues 8 tcgen05.mma kind::f16 (bf16 x bf16, M = 128, N = NT,
-//    K = 16; A and B from shared memory, D in TMEM) and commits the stage;
+//    K = 16; A from TMEM, B from shared memory, D in TMEM) and commits;
 //  * 4 epilogue warps read the finished tile from TMEM (two accumulator
 //    buffers, so the next tile's MMAs overlap) and store y (bf16, optionally
 //    fp32).
@@ -37,36 +38,40 @@ namespace anyq_b200 {
 
 namespace {
 
-constexpr int kK2Dq = 16;       // dequant warps: 4 row blocks x 4 k quarters
+constexpr int kK2Dq = 16;       // dequant warps: 4 row blocks (TMEM lane quarters) x 4 k quarters
 constexpr int kK2Epi0 = 16;     // epilogue warps 16..19 (TMEM lane quarter = warp & 3)
 constexpr int kK2Mma = 20;
-constexpr int kK2Prod = 21;
-constexpr int kK2T = 22 * 32;
-constexpr int kK2Stages = 2;
-constexpr uint32_t kK2A = 8 * 4096;       // A of one step: 8 slices x (16 groups x 256 B)
+constexpr int kK2ProdX = 21;    // x tiles (TMA tensor loads)
+constexpr int kK2ProdC = 22;    // codes + alpha/beta (bulk copies)
+constexpr int kK2T = 23 * 32;
+constexpr int kK2CStages = 8;             // code ring
+constexpr int kK2AStages = 4;             // A stages in TMEM (64 columns each)
 constexpr uint32_t kK2Codes = 4 * 2048;   // codes of one step: 4 row blocks x one chunk
 constexpr uint32_t kK2Ab = 4 * 128;       // alpha/beta lines of one step
-constexpr uint32_t kK2Tbl = 16 * 64;      // a dequant warp's table: 16 entries x 32 lanes x bf16
+constexpr uint32_t kK2CStage = kK2Codes + kK2Ab;
+constexpr uint32_t kK2Tbl = 16 * 64;      // a row block's table: 16 entries x 32 rows x bf16 (x2 buffers)
 
 template <int NT>
 struct K2Cfg {
+  static constexpr int kXStages = NT >= 128 ? 4 : 6;
   static constexpr uint32_t kBox = NT * 128;           // one 64-k x NT box of x (bf16), 1024-aligned
   static constexpr uint32_t kB = 2 * kBox;             // x of one 128-k step
   static constexpr uint32_t kOffB = 0;
-  static constexpr uint32_t kOffA = kOffB + kK2Stages * kB;
-  static constexpr uint32_t kOffCodes = kOffA + kK2Stages * kK2A;
-  static constexpr uint32_t kOffAb = kOffCodes + kK2Stages * kK2Codes;
-  static constexpr uint32_t kOffTbl = kOffAb + kK2Stages * kK2Ab;
-  static constexpr uint32_t kOffBars = kOffTbl + kK2Dq * kK2Tbl;
-  static constexpr uint32_t kSmem = kOffBars + 256;
-  static constexpr int kTmemCols = 2 * NT <= 256 ? 256 : 512;
+  static constexpr uint32_t kOffC = kOffB + kXStages * kB;
+  static constexpr uint32_t kOffTbl = kOffC + kK2CStages * kK2CStage;
+  static constexpr uint32_t kOffBars = kOffTbl + 4 * 2 * kK2Tbl;
+  static constexpr uint32_t kSmem = kOffBars + 512;
+  static constexpr uint32_t kACol0 = 2 * NT;            // D buffers at columns [0, 2 NT), A after
+  static constexpr int kTmemCols = 512;
   // kind::f16 instruction descriptor: D f32 (bit 4), A and B bf16 (format 1 at
   // bits 7 and 10), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   static constexpr uint32_t kIdesc =
       (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
 };
-// mbarrier offsets (from kOffBars)
-constexpr uint32_t kQFull = 0, kQEmpty = 16, kQAFull = 32, kQDFull = 48, kQDEmpty = 64, kQTmem = 80;
+// mbarrier offsets (from kOffBars): x full/empty [6], codes full/empty [8],
+// A full/empty [4], D full/empty [2], TMEM slot
+constexpr uint32_t kQXFull = 0, kQXEmpty = 48, kQCFull = 96, kQCEmpty = 160, kQAFull = 224, kQAEmpty = 256,
+                   kQDFull = 288, kQDEmpty = 304, kQTmem = 320;
 
 struct K2Params {
   const uint8_t* codes;   // [RB][C][4][32][16 B]
@@ -113,24 +118,24 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void tc_mma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
+}
+__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(pred));
   return pred != 0;
 }
-// UMMA shared-memory descriptors (version 1): A — K-major, no swizzle, LBO
-// 128 B between the two 8-k halves, SBO 256 B between 8-row groups; B —
-// K-major SWIZZLE_128B (layout type 2), SBO 1024 B between 8-row groups.
-__device__ __forceinline__ uint64_t desc_a(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
-         (1ull << 46);
-}
+// UMMA shared-memory descriptor of B (version 1): K-major SWIZZLE_128B
+// (layout type 2), SBO 1024 B between 8-row groups.
 __device__ __forceinline__ uint64_t desc_b(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
          (2ull << 61);
@@ -153,15 +158,23 @@ template <int NT>
 __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ CUtensorMap xmap,
                                                          const __grid_constant__ K2Params P) {
   using CF = K2Cfg<NT>;
+  constexpr int XS = CF::kXStages;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t bars = sbase + CF::kOffBars;
   if (threadIdx.x == 0) {
-    for (int j = 0; j < kK2Stages; ++j) {
-      mbar_init(bars + kQFull + 8 * j, 1);
-      mbar_init(bars + kQEmpty + 8 * j, 1);
+    for (int j = 0; j < XS; ++j) {
+      mbar_init(bars + kQXFull + 8 * j, 1);
+      mbar_init(bars + kQXEmpty + 8 * j, 1);
+    }
+    for (int j = 0; j < kK2CStages; ++j) {
+      mbar_init(bars + kQCFull + 8 * j, 1);
+      mbar_init(bars + kQCEmpty + 8 * j, kK2Dq);
+    }
+    for (int j = 0; j < kK2AStages; ++j) {
       mbar_init(bars + kQAFull + 8 * j, kK2Dq);
+      mbar_init(bars + kQAEmpty + 8 * j, 1);
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(bars + kQDFull + 8 * j, 1);
@@ -181,30 +194,48 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
   const int ntiles = P.rtiles * P.ttiles;
   const int C = P.C;
 
-  if (warp == kK2Prod) {
-    // ------------------------------------------------------------ producer
+  if (warp == kK2ProdX) {
+    // ------------------------------------------------------------ x producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
       int st = 0;
       uint32_t round = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int rt = tile / P.ttiles, tt = tile - rt * P.ttiles;
-        const int nrb = min(4, P.RB - 4 * rt);
+        const int tt = tile % P.ttiles;
         for (int c = 0; c < C; ++c) {
-          if (round > 0) mbar_wait(bars + kQEmpty + 8 * st, (round - 1) & 1);
-          const uint32_t full = bars + kQFull + 8 * st;
-          mbar_expect_tx(full, CF::kB + (uint32_t)nrb * (2048 + 128));
+          if (round > 0) mbar_wait(bars + kQXEmpty + 8 * st, (round - 1) & 1);
+          const uint32_t full = bars + kQXFull + 8 * st;
+          mbar_expect_tx(full, CF::kB);
           const uint32_t b = sbase + CF::kOffB + st * CF::kB;
           tma_load_2d(b, &xmap, c * 128, tt * NT, full);
           tma_load_2d(b + CF::kBox, &xmap, c * 128 + 64, tt * NT, full);
+          if (++st == XS) {
+            st = 0;
+            ++round;
+          }
+        }
+      }
+    }
+  } else if (warp == kK2ProdC) {
+    // ------------------------------------------------------------ code producer
+    if (lane == 0) {
+      int st = 0;
+      uint32_t round = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int rt = tile / P.ttiles;
+        const int nrb = min(4, P.RB - 4 * rt);
+        for (int c = 0; c < C; ++c) {
+          if (round > 0) mbar_wait(bars + kQCEmpty + 8 * st, (round - 1) & 1);
+          const uint32_t full = bars + kQCFull + 8 * st;
+          mbar_expect_tx(full, (uint32_t)nrb * (2048 + 128));
+          const uint32_t cs = sbase + CF::kOffC + st * kK2CStage;
           const int g = c >> P.gshift;
           for (int q = 0; q < nrb; ++q) {
             const int rb = 4 * rt + q;
-            bulk_g2s(sbase + CF::kOffCodes + st * kK2Codes + q * 2048,
-                     P.codes + ((size_t)rb * C + c) * 2048, 2048, full);
-            bulk_g2s(sbase + CF::kOffAb + st * kK2Ab + q * 128, P.ab + ((size_t)rb * P.GR + g) * 32, 128, full);
+            bulk_g2s(cs + q * 2048, P.codes + ((size_t)rb * C + c) * 2048, 2048, full);
+            bulk_g2s(cs + kK2Codes + q * 128, P.ab + ((size_t)rb * P.GR + g) * 32, 128, full);
           }
-          if (++st == kK2Stages) {
+          if (++st == kK2CStages) {
             st = 0;
             ++round;
           }
@@ -213,30 +244,35 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     }
   } else if (warp == kK2Mma) {
     // ------------------------------------------------------------ MMA issue
-    int st = 0, tl = 0;
-    uint32_t round = 0;
+    int xs = 0, as = 0, tl = 0;
+    uint32_t xround = 0, around = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
       const int db = tl & 1;
       if (tl >= 2) mbar_wait(bars + kQDEmpty + 8 * db, (uint32_t)(((tl >> 1) - 1) & 1));
       const uint32_t d = tmem + (uint32_t)db * NT;
       for (int c = 0; c < C; ++c) {
-        mbar_wait(bars + kQFull + 8 * st, round & 1);
-        mbar_wait(bars + kQAFull + 8 * st, round & 1);
+        mbar_wait(bars + kQXFull + 8 * xs, xround & 1);
+        mbar_wait(bars + kQAFull + 8 * as, around & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t a = sbase + CF::kOffA + st * kK2A;
-          const uint32_t b = sbase + CF::kOffB + st * CF::kB;
+          const uint32_t a = tmem + CF::kACol0 + (uint32_t)as * 64;
+          const uint32_t b = sbase + CF::kOffB + xs * CF::kB;
 #pragma unroll
           for (int s = 0; s < 8; ++s)
-            tc_mma_ss(d, desc_a(a + s * 4096), desc_b(b + (s >> 2) * CF::kBox + (s & 3) * 32), CF::kIdesc,
+            tc_mma_ts(d, a + s * 8, desc_b(b + (s >> 2) * CF::kBox + (s & 3) * 32), CF::kIdesc,
                       (c > 0 || s > 0) ? 1u : 0u);
-          tc_commit(bars + kQEmpty + 8 * st);
+          tc_commit(bars + kQXEmpty + 8 * xs);
+          tc_commit(bars + kQAEmpty + 8 * as);
           if (c == C - 1) tc_commit(bars + kQDFull + 8 * db);
         }
         __syncwarp();
-        if (++st == kK2Stages) {
-          st = 0;
-          ++round;
+        if (++xs == XS) {
+          xs = 0;
+          ++xround;
+        }
+        if (++as == kK2AStages) {
+          as = 0;
+          ++around;
         }
       }
     }
@@ -272,11 +308,16 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     }
   } else {
     // ------------------------------------------------------------ dequant
+    // the row block's 4 warps share its per-step table (two buffers by step
+    // parity): warp j builds entries 4j..4j+3, a 128-thread named barrier
+    // (one per row block) publishes it
     const int q = warp & 3, j = warp >> 2;
-    uint16_t* tbl = reinterpret_cast<uint16_t*>(smem + CF::kOffTbl + warp * kK2Tbl);
-    const uint32_t tblw = sbase + CF::kOffTbl + warp * kK2Tbl + lane * 2;
-    int st = 0;
-    uint32_t round = 0;
+    uint16_t* tbl0 = reinterpret_cast<uint16_t*>(smem + CF::kOffTbl + q * 2 * kK2Tbl);
+    const uint32_t tblw0 = sbase + CF::kOffTbl + q * 2 * kK2Tbl + lane * 2;
+    int par = 0;
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + CF::kACol0;
+    int cs = 0, as = 0;
+    uint32_t cround = 0, around = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int rt = tile / P.ttiles;
       const int rb = 4 * rt + q;
@@ -298,45 +339,61 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
         }
       }
       for (int c = 0; c < C; ++c) {
-        // the stage's A buffer is free once its previous MMAs completed
-        if (round > 0) mbar_wait(bars + kQEmpty + 8 * st, (round - 1) & 1);
-        mbar_wait(bars + kQFull + 8 * st, round & 1);
+        mbar_wait(bars + kQCFull + 8 * cs, cround & 1);
+        uint32_t v[16];
         if (live) {
-          // bf16(alpha * T[i] + beta) for this row and step (fp32, one rounding)
-          const float2 ab = __half22float2(*reinterpret_cast<const __half2*>(
-              smem + CF::kOffAb + st * kK2Ab + q * 128 + lane * 4));
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            tbl[i * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(__fadd_rn(__fmul_rn(ab.x, T[i]), ab.y)));
+          const uint8_t* cst = smem + CF::kOffC + cs * kK2CStage;
+          const float2 ab = __half22float2(*reinterpret_cast<const __half2*>(cst + kK2Codes + q * 128 + lane * 4));
+          const uint4 w4 = *reinterpret_cast<const uint4*>(cst + q * 2048 + j * 512 + lane * 16);
           __syncwarp();
-          const uint4 w4 = *reinterpret_cast<const uint4*>(smem + CF::kOffCodes + st * kK2Codes + q * 2048 +
-                                                           j * 512 + lane * 16);
+          if (lane == 0) mbar_arrive(bars + kQCEmpty + 8 * cs);  // codes and scales are in registers
+          // bf16(alpha * T[i] + beta) for this row and step (fp32, one rounding)
+          uint16_t* tbl = tbl0 + par * (kK2Tbl / 2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            tbl[(4 * j + i) * 32 + lane] =
+                __bfloat16_as_ushort(__float2bfloat16_rn(__fadd_rn(__fmul_rn(ab.x, T[4 * j + i]), ab.y)));
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+          // entry i of row `lane` at tbl + i * 64 + lane * 2, the table 1024-B aligned: the
+          // address of nibble n of a code word is ((w >> (4n - 6)) & 0x3C0) | (tbl + lane * 2)
+          const uint32_t tblw = tblw0 + par * kK2Tbl;
           const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
-          uint32_t v[16];
 #pragma unroll
           for (int bb = 0; bb < 16; ++bb) {
-            const uint32_t byte = (wd[bb >> 2] >> (8 * (bb & 3))) & 0xFFu;
-            uint16_t lo, hi;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(lo) : "r"(tblw + ((byte & 15u) << 6)));
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hi) : "r"(tblw + ((byte >> 4) << 6)));
-            v[bb] = (uint32_t)lo | ((uint32_t)hi << 16);
+            const uint32_t w = wd[bb >> 2];
+            const int nlo = 8 * (bb & 3), nhi = nlo + 4;  // bit offsets of the two nibbles
+            const uint32_t alo = ((nlo >= 6 ? (w >> (nlo - 6)) : (w << (6 - nlo))) & 0x3C0u) | tblw;
+            const uint32_t ahi = ((w >> (nhi - 6)) & 0x3C0u) | tblw;
+            uint32_t lo, hi;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(lo) : "r"(alo));
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hi) : "r"(ahi));
+            v[bb] = __byte_perm(lo, hi, 0x5410);
           }
-          // bytes 0..7: k = 16j + 2b (+1) -> slice j; bytes 8..15: k = 64 + 16j + ... -> slice 4 + j.
-          // Row r = 32q + lane: [slice][r / 8][k half][r % 8][16 B]
-          const uint32_t rowoff = (uint32_t)(4 * q + (lane >> 3)) * 256 + (uint32_t)(lane & 7) * 16;
-          uint8_t* a = smem + CF::kOffA + st * kK2A + rowoff;
-          *reinterpret_cast<uint4*>(a + j * 4096) = make_uint4(v[0], v[1], v[2], v[3]);
-          *reinterpret_cast<uint4*>(a + j * 4096 + 128) = make_uint4(v[4], v[5], v[6], v[7]);
-          *reinterpret_cast<uint4*>(a + (4 + j) * 4096) = make_uint4(v[8], v[9], v[10], v[11]);
-          *reinterpret_cast<uint4*>(a + (4 + j) * 4096 + 128) = make_uint4(v[12], v[13], v[14], v[15]);
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bars + kQCEmpty + 8 * cs);
         }
-        // generic-proxy writes of A -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        par ^= 1;
+        // bytes 0..7: k = 16j + 2b (+1) -> slice j (A columns 8j..); bytes 8..15: k = 64 + 16j + ...
+        // -> slice 4 + j (columns 32 + 8j..)
+        if (around > 0) mbar_wait(bars + kQAEmpty + 8 * as, (around - 1) & 1);
+        tc_fence_after();
+        if (live) {
+          const uint32_t ta = tq + (uint32_t)as * 64;
+          tc_st8(ta + 8 * j, v);
+          tc_st8(ta + 32 + 8 * j, v + 8);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bars + kQAFull + 8 * st);
-        if (++st == kK2Stages) {
-          st = 0;
-          ++round;
+        if (lane == 0) mbar_arrive(bars + kQAFull + 8 * as);
+        if (++cs == kK2CStages) {
+          cs = 0;
+          ++cround;
+        }
+        if (++as == kK2AStages) {
+          as = 0;
+          ++around;
         }
       }
     }
@@ -422,8 +479,7 @@ void lutgemm_k2_run(const LutTensor* t, const void* x, int64_t m, void* y, float
     fail(ANYQ_ERR_CONFIG, "tcgen05 large-M GEMM needs K % 8 == 0 and rowwise scales or group_size = 128 * 2^j");
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) fail(ANYQ_ERR_SHAPE, "tcgen05 large-M GEMM needs 16-B aligned x");
   if (m <= 64) launch_k2<64>(t, x, m, y, y32, s);
-  else if (m <= 128) launch_k2<128>(t, x, m, y, y32, s);
-  else launch_k2<256>(t, x, m, y, y32, s);
+  else launch_k2<128>(t, x, m, y, y32, s);
 }
 
 }  // namespace anyq_b200

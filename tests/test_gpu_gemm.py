@@ -311,7 +311,8 @@ def test_auto_path_choice_and_agreement(aq, orc, cuda):
     assert long_k.auto_path(3) == aq.PATH_TC
     long_k.close()
     tall = aq.DeviceTensor(aq.quantize_any(orc.gaussian(300 * 32, 256, 10), cfg(codebook=3, max_iters=2)))
-    assert [tall.auto_path(m) for m in (1, 2, 8, 16, 17)] == [aq.PATH_GEMV] + [aq.PATH_GEMV_TC] * 3 + [aq.PATH_MMA]
+    assert [tall.auto_path(m) for m in (1, 2, 8, 16, 17, 128, 129)] == \
+        [aq.PATH_GEMV] + [aq.PATH_GEMV_TC] * 3 + [aq.PATH_K2] * 2 + [aq.PATH_DEQUANT]
     tall.close()
 
 
