@@ -235,6 +235,13 @@ typedef struct anyq_dev_tensor anyq_dev_tensor;
  * scales to fp16 exactly like narrowed(); pack.cpp:159-169). */
 anyq_status anyq_dev_tensor_create(const anyq_qtensor* qt, anyq_dev_tensor** out);
 void anyq_dev_tensor_destroy(anyq_dev_tensor* t);
+/* The inverse of the prepack: the device tensor back in the reference layout
+ * (pack.hpp:21-39; row-major codes packed at cfg.bits, LUT and alpha/beta as
+ * the fp32 values of their fp16 stores, i.e. narrowed(qt) of the tensor it was
+ * created from). out sized like any anyq_qtensor of (rows, cols, cfg). */
+anyq_status anyq_dev_tensor_export(const anyq_dev_tensor* t, anyq_qtensor* out);
+/* The config a device tensor was created (or loaded) from. */
+void anyq_dev_tensor_config(const anyq_dev_tensor* t, anyq_config* out);
 /* Bytes the GEMM must stream per call (codes + scales + LUT). */
 int64_t anyq_dev_tensor_weight_bytes(const anyq_dev_tensor* t);
 int64_t anyq_dev_tensor_rows(const anyq_dev_tensor* t);

@@ -125,6 +125,8 @@ def lib() -> C.CDLL:
         "anyq_gemm_dense": (st, [fptr, i64, fptr, i64, i64, fptr]),
         "anyq_dev_tensor_create": (st, [qt, C.POINTER(vp)]),
         "anyq_dev_tensor_destroy": (None, [vp]),
+        "anyq_dev_tensor_export": (st, [vp, qt]),
+        "anyq_dev_tensor_config": (None, [vp, cfg]),
         "anyq_dev_tensor_weight_bytes": (i64, [vp]),
         "anyq_dev_tensor_rows": (i64, [vp]),
         "anyq_dev_tensor_cols": (i64, [vp]),
@@ -178,7 +180,7 @@ EXPORTED_SYMBOLS = (
     "anyq_lut_entries", "anyq_quantize_any", "anyq_quantize_fixed", "anyq_pack_codes",
     "anyq_unpack_codes", "anyq_ktile_codes", "anyq_narrow_inplace", "anyq_dequantize",
     "anyq_gemm_fused", "anyq_gemm_dense", "anyq_dev_tensor_create", "anyq_dev_tensor_destroy",
-    "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
+    "anyq_dev_tensor_weight_bytes", "anyq_dev_tensor_export", "anyq_dev_tensor_config", "anyq_dev_tensor_rows", "anyq_dev_tensor_cols",
     "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
     "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_chain_path", "anyq_dev_gemm_auto_path",
     "anyq_dev_quantize_any", "anyq_eval_activations", "anyq_compare_formats",
@@ -595,6 +597,17 @@ class DeviceTensor:
             self.close()
         except Exception:
             pass
+
+    def export(self) -> QuantizedTensor:
+        """prepack^-1: the tensor back in the reference layout (narrowed values)."""
+        cfg = _abi.Config()
+        lib().anyq_dev_tensor_config(self._h, C.byref(cfg))
+        out = QuantizedTensor.empty(self.rows, self.cols, cfg)
+        c = out.as_c()
+        _check(lib().anyq_dev_tensor_export(self._h, C.byref(c)))
+        out.cfg = c.cfg
+        out.lut_store, out.scale_store, out.layout = c.lut_store, c.scale_store, c.layout
+        return out
 
     def auto_path(self, m: int) -> int:
         """The kernel PATH_AUTO runs at m rows of x (PATH_GEMV / PATH_TC / PATH_DEQUANT)."""

@@ -691,6 +691,14 @@ anyq_status anyq_dev_tensor_create(const anyq_qtensor* qt, anyq_dev_tensor** out
   });
 }
 
+anyq_status anyq_dev_tensor_export(const anyq_dev_tensor* t, anyq_qtensor* out) {
+  return guard([&] { lutgemm_export(reinterpret_cast<const LutTensor*>(t), out); });
+}
+
+void anyq_dev_tensor_config(const anyq_dev_tensor* t, anyq_config* out) {
+  if (t && out) *out = reinterpret_cast<const LutTensor*>(t)->cfg;
+}
+
 void anyq_dev_tensor_destroy(anyq_dev_tensor* t) {
   lutgemm_destroy(reinterpret_cast<LutTensor*>(t));
 }

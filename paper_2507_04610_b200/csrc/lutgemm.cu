@@ -674,6 +674,28 @@ __global__ void k_prepack_codes(const uint8_t* __restrict__ codes, int64_t rows,
   }
 }
 
+// prepack^-1: [RB][C][4][32][16 B] -> logical codes [rows][cols] (one byte each)
+__global__ void k_unprepack_codes(const uint8_t* __restrict__ in, int64_t rows, int64_t cols, int RB, int C,
+                                  uint8_t* __restrict__ codes) {
+  const int64_t total = (int64_t)RB * C * kChunkBytes;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e & 15);
+    const int L = (int)((e >> 4) & 31);
+    const int q = (int)((e >> 9) & 3);
+    const int64_t c = (e >> 11) % C;
+    const int64_t rb = (e >> 11) / C;
+    const int64_t row = rb * 32 + L;
+    const int64_t step = 2 * c + (b >> 3);
+    const int64_t k = 64 * step + 16 * q + 2 * (b & 7);
+    const uint8_t v = in[e];
+    if (row < rows) {
+      if (k < cols) codes[row * cols + k] = v & 15;
+      if (k + 1 < cols) codes[row * cols + k + 1] = v >> 4;
+    }
+  }
+}
+
 // LUT (fp32 narrowed values) -> fp16 [RB*32][16], alpha/beta -> [RB][GR][32]
 __global__ void k_prepack_scales(const float* __restrict__ luts, const float* __restrict__ table16,
                                  const float* __restrict__ alphas, const float* __restrict__ betas,
@@ -803,6 +825,7 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
     ANYQ_CUDA(cudaGetDevice(&dev));
     ANYQ_CUDA(cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, dev));
     t->weight_bytes = rows * ((cols * 4 + 7) / 8) + ng * 4 + rows * 16 * 2;
+    t->cfg = c;
 
     // Prepack on a private stream: no legacy-stream or device-wide
     // synchronisation, so creating a tensor never waits on other streams' work.
@@ -883,6 +906,48 @@ LutTensor* lutgemm_create(const anyq_qtensor* qt) {
     throw;
   }
   return t;
+}
+
+void lutgemm_export(const LutTensor* t, anyq_qtensor* out) {
+  if (!t || !out) fail(ANYQ_ERR_SHAPE, "dev_tensor_export: null argument");
+  const anyq_config& c = t->cfg;
+  const int64_t rows = t->rows, cols = t->cols;
+  const int64_t ng = c.granularity == ANYQ_G_ROW ? rows : rows * t->GR;
+  if (out->rows != rows || out->cols != cols || out->num_groups != ng)
+    fail(ANYQ_ERR_SHAPE, "dev_tensor_export: output sized for another tensor");
+  struct OwnStream {
+    cudaStream_t s = nullptr;
+    OwnStream() { ANYQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~OwnStream() { cudaStreamDestroy(s); }
+  } own;
+  const cudaStream_t z = own.s;
+  DevBuf<uint8_t> logical((size_t)(rows * cols), z), packed((size_t)(rows * packed_bpr(cols, c.bits)), z);
+  k_unprepack_codes<<<148 * 8, 256, 0, z>>>(t->codes, rows, cols, t->RB, t->C, logical.p);
+  ANYQ_LAUNCHED();
+  DevBuf<int> perr(1, z);
+  ANYQ_CUDA(cudaMemsetAsync(perr.p, 0, sizeof(int), z));
+  launch_pack(logical.p, rows, cols, c.bits, packed.p, perr.p, z);
+  std::vector<__half> lut((size_t)t->RB * 32 * 16);
+  std::vector<__half2> ab((size_t)t->RB * t->GR * 32);
+  ANYQ_CUDA(cudaMemcpyAsync(out->codes, packed.p, (size_t)(rows * packed_bpr(cols, c.bits)), cudaMemcpyDeviceToHost, z));
+  ANYQ_CUDA(cudaMemcpyAsync(lut.data(), t->lut, sizeof(__half) * lut.size(), cudaMemcpyDeviceToHost, z));
+  ANYQ_CUDA(cudaMemcpyAsync(ab.data(), t->ab, sizeof(__half2) * ab.size(), cudaMemcpyDeviceToHost, z));
+  ANYQ_CUDA(cudaStreamSynchronize(z));
+  if (c.codebook == ANYQ_CB_ANY && out->luts) {
+    const int L = 1 << c.bits;
+    for (int64_t r = 0; r < rows; ++r)
+      for (int i = 0; i < L; ++i) out->luts[r * L + i] = __half2float(lut[(size_t)r * 16 + i]);
+  }
+  for (int64_t r = 0; r < rows; ++r)
+    for (int g = 0; g < t->GR; ++g) {
+      const __half2 v = ab[((size_t)(r / 32) * t->GR + g) * 32 + r % 32];
+      out->alphas[r * t->GR + g] = __low2float(v);
+      out->betas[r * t->GR + g] = __high2float(v);
+    }
+  out->cfg = c;
+  out->layout = ANYQ_LAYOUT_ROWMAJOR;
+  out->lut_store = ANYQ_STORE_FP16;
+  out->scale_store = ANYQ_STORE_FP16;
 }
 
 void lutgemm_set_trace(long long* dev) { g_trace = dev; }

@@ -20,11 +20,16 @@ struct LutTensor {
   __half2* ab = nullptr;     // [RB][GR][32] (alpha, beta)
   int cmax = 0;  // tcgen05 path: most chunk ranges a row block is split into
   int sms = 148;
+  anyq_config cfg{};  // the quantisation config it was created from (for export)
   // CUDA-core GEMV (gemv.cu) work split (its counters live per stream)
   int gv_ncta = 0, gv_gshift = -1;
 };
 
 LutTensor* lutgemm_create(const anyq_qtensor* qt);
+// prepack^-1: the device layout back to the reference arrays (row-major packed
+// codes at cfg.bits, LUT / alpha / beta widened from their fp16 stores) into
+// host buffers sized for (rows, cols, cfg) (lutgemm.cu)
+void lutgemm_export(const LutTensor* t, anyq_qtensor* out);
 LutTensor* load_device_tensor(const char* path);  // ANYQ v1 file -> prepacked (anyq_file.cu)
 void lutgemm_destroy(LutTensor* t);
 void lutgemm_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), or null

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
             const uint32_t w = wd[bb >> 2];
             const int nlo = 8 * (bb & 3), nhi = nlo + 4;  // bit offsets of the two nibbles
             const uint32_t alo = ((nlo >= 6 ? (w >> (nlo - 6)) : (w << (6 - nlo))) & 0x3C0u) | tblw;
-            const uint32_t ahi = ((w >> (nhi - 6)) & 0x3C0u) | tblw;
+            const uint32_t ahi = ((nhi >= 6 ? (w >> (nhi - 6)) : (w << (6 - nhi))) & 0x3C0u) | tblw;
             uint32_t lo, hi;
             asm volatile("ld.shared.u16 %0, [%1];" : "=r"(lo) : "r"(alo));
             asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hi) : "r"(ahi));

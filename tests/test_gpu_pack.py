@@ -92,3 +92,34 @@ def test_dequantize_rejects_fp4_code_15(aq, orc):
     qt.codes[0] = 0xFF
     with pytest.raises(aq.CodeRangeError):
         aq.dequantize(qt)
+
+
+@pytest.mark.parametrize("fmt", ["any4", "any3", "any2", "int4", "nf4", "fp4"])
+@pytest.mark.parametrize("shape,gran,g", [((200, 384), 3, 128), ((33, 130), 1, 128), ((64, 1024), 3, 256),
+                                          ((5, 17), 1, 128)])
+def test_prepack_inverse_round_trip(aq, orc, cuda, fmt, shape, gran, g):
+    """unpack(prepack^-1(prepack(codes))) == codes bit for bit:
+    the device layout [RB][C][4 slabs][32 rows][16 B] exported back
+    (anyq_dev_tensor_export) equals narrowed(qt) — codes, LUT and alpha/beta."""
+    c = cfg(granularity=gran, group_size=g, seed=3)
+    aq.apply_format(c, fmt)
+    qt = orc.quantize(orc.gaussian(*shape, 11), c)
+    dt = aq.DeviceTensor(qt)
+    back = dt.export()
+    dt.close()
+    want = orc.narrowed(qt)
+    assert np.array_equal(back.codes, want.codes)
+    assert np.array_equal(aq.unpack_codes(back.codes, *shape, c.bits), aq.unpack_codes(qt.codes, *shape, c.bits))
+    assert bits_equal(back.alphas, want.alphas) and bits_equal(back.betas, want.betas)
+    if want.luts is not None:
+        assert bits_equal(back.luts, want.luts)
+
+
+def test_prepack_inverse_of_ktiled_tensor(aq, orc, cuda):
+    """A k-tiled tensor prepacks in logical order; its export is row-major."""
+    qt = orc.quantize(orc.gaussian(64, 512, 12), cfg(codebook=3, max_iters=3, seed=4))
+    kt = orc.to_ktiled(qt, 32)
+    dt = aq.DeviceTensor(kt)
+    back = dt.export()
+    dt.close()
+    assert np.array_equal(back.codes, orc.narrowed(qt).codes)
