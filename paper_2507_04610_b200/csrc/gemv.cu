@@ -1482,15 +1482,24 @@ bool gv_sbase_ok() {
   if (it != ok.end()) return it->second;
   uint32_t* d = nullptr;
   uint32_t h = 0;
-  cudaStream_t z;
-  ANYQ_CUDA(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking));
-  ANYQ_CUDA(cudaMalloc(&d, sizeof(uint32_t)));
-  k_sbase_probe<<<1, 32, 4096, z>>>(d);
-  ANYQ_LAUNCHED();
-  ANYQ_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, z));
-  ANYQ_CUDA(cudaStreamSynchronize(z));
-  ANYQ_CUDA(cudaFree(d));
-  ANYQ_CUDA(cudaStreamDestroy(z));
+  // the first GEMV may be issued while another stream is being captured:
+  // probe on a private stream in relaxed capture mode
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  ANYQ_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+  cudaStream_t z = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&d, sizeof(uint32_t));
+  if (e == cudaSuccess) {
+    k_sbase_probe<<<1, 32, 4096, z>>>(d);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, z);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(z);
+  if (d) cudaFree(d);
+  if (z) cudaStreamDestroy(z);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  ANYQ_CUDA(e);
   return ok[dev] = (h == kDynBase);
 }
 
