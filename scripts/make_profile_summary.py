@@ -60,7 +60,7 @@ def main():
         share = {k: {"ns": round(t, 0), "share": round(t / tot, 4)} for k, t in
                  sorted(share.items(), key=lambda kv: -kv[1])}
     summary = {
-        "round": 1,
+        "round": 2,
         "kernel": "k_lutgemv<1> chain (one Llama-3-8B decoder layer, 7 GEMMs, M=1): 16 compute + writer + producer warps",
         "capture": f"ncu --set full --clock-control none (cold L2, serialised) of scripts/prof_chain.py -> {os.path.basename(rep)}",
         "dram_bytes_per_launch_layer_chain": rd + wr,
