@@ -301,6 +301,33 @@ anyq_status anyq_dev_gemm_chain_path(int32_t n, const anyq_dev_tensor* const* t,
                                      float* const* y_f32, const int32_t* deps, int64_t m,
                                      int32_t path, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Tensor parallelism: W sharded by output rows over `world`
+ * ranks (one GPU each); y is all-gathered. The gather is fused into the GEMV
+ * writer: every y value of this rank's shard is stored straight into every
+ * rank's full-width y buffer (NVLink peer stores to buffers mapped with
+ * anyq_ipc_open), and each CTA then bumps flags[r][rank] on every rank r
+ * (system-scope release). anyq_dev_tp_wait makes `stream` wait until every
+ * rank's contribution of call number `epoch` (1, 2, ...) has landed here.
+ * ------------------------------------------------------------------------- */
+typedef struct anyq_tp_peers {
+  int32_t world;        /* ranks, 1..8 */
+  int32_t rank;         /* this rank */
+  int64_t rows_total;   /* rows of the unsharded weight (= columns of y) */
+  int64_t row0;         /* first row of this rank's shard */
+  void* y[8];           /* every rank's y (bf16, m x rows_total), valid on this device */
+  int32_t* flags[8];    /* every rank's flag words (int32[world], zero at start), valid here */
+} anyq_tp_peers;
+anyq_status anyq_dev_gemm_allgather(const anyq_dev_tensor* shard, const void* x_bf16, int64_t m,
+                                    const anyq_tp_peers* tp, void* stream);
+anyq_status anyq_dev_tp_wait(const anyq_dev_tensor* shard, const anyq_tp_peers* tp, int32_t epoch,
+                             void* stream);
+/* CUDA IPC for the peer buffers: a 64-byte handle of a device allocation, and
+ * its mapping in another process (close with anyq_ipc_close). */
+anyq_status anyq_ipc_handle(const void* dev_ptr, uint8_t handle[64]);
+anyq_status anyq_ipc_open(const uint8_t handle[64], void** dev_ptr);
+anyq_status anyq_ipc_close(void* dev_ptr);
+
 /* read_file straight into the prepacked device layout. */
 anyq_status anyq_dev_tensor_load(const char* path, anyq_dev_tensor** out);
 

@@ -146,3 +146,9 @@ def u8p(a):
 
 def f64p(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class TpPeers(C.Structure):
+    """anyq_tp_peers (include/anyq_b200.h): the fused tensor-parallel gather."""
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("rows_total", C.c_int64), ("row0", C.c_int64),
+                ("y", C.c_void_p * 8), ("flags", C.c_void_p * 8)]

@@ -140,6 +140,11 @@ def lib() -> C.CDLL:
         "anyq_dev_gemm_chain_path": (st, [i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                           C.POINTER(vp), C.POINTER(i32), i64, i32, vp]),
         "anyq_dev_quantize_any": (st, [vp, i64, i64, cfg, vp, i64, vp, vp, vp, vp, vp]),
+        "anyq_dev_gemm_allgather": (st, [vp, vp, i64, C.POINTER(_abi.TpPeers), vp]),
+        "anyq_dev_tp_wait": (st, [vp, C.POINTER(_abi.TpPeers), i32, vp]),
+        "anyq_ipc_handle": (st, [vp, C.POINTER(C.c_uint8)]),
+        "anyq_ipc_open": (st, [C.POINTER(C.c_uint8), C.POINTER(vp)]),
+        "anyq_ipc_close": (st, [vp]),
         "anyq_column_mean_abs": (st, [fptr, i64, i64, fptr]),
         "anyq_write_file": (st, [qt, C.c_char_p]),
         "anyq_read_file_header": (st, [C.c_char_p, qt]),
@@ -184,6 +189,7 @@ EXPORTED_SYMBOLS = (
     "anyq_dev_gemm_bf16", "anyq_dev_gemm_bf16_path", "anyq_dev_gemm_chain",
     "anyq_dev_gemm_chain_deps", "anyq_dev_gemm_chain_path", "anyq_dev_gemm_auto_path",
     "anyq_dev_quantize_any", "anyq_eval_activations", "anyq_compare_formats",
+    "anyq_dev_gemm_allgather", "anyq_dev_tp_wait", "anyq_ipc_handle", "anyq_ipc_open", "anyq_ipc_close",
     "anyq_launch_count",
     "anyq_compute_scales", "anyq_scale_weights", "anyq_dequantize_values",
     "anyq_column_mean_abs", "anyq_dev_column_mean_abs", "anyq_weight_error", "anyq_output_error",
@@ -705,6 +711,50 @@ def compare_formats(w, formats, base, exj=None, eval_rows: int = 64, eval_seed: 
     lines += [f"v1,{r['module']},{r['format']},{r['weight_mse']:.9g},{r['weight_rel_frobenius']:.9g},"
               f"{r['output_mse']:.9g},{r['bits_per_entry']:.9g}" for r in rows]
     return rows, "\n".join(lines) + "\n"
+
+
+def tp_peers(world: int, rank: int, rows_total: int, row0: int, y_ptrs, flag_ptrs) -> "_abi.TpPeers":
+    """anyq_tp_peers of this rank (device pointers valid on this device)."""
+    p = _abi.TpPeers()
+    p.world, p.rank, p.rows_total, p.row0 = world, rank, rows_total, row0
+    for r in range(world):
+        p.y[r] = y_ptrs[r]
+        p.flags[r] = flag_ptrs[r]
+    return p
+
+
+def gemm_allgather(shard: "DeviceTensor", x, peers, stream=None):
+    """y_r = x W_r^T of this rank's row shard, stored into every rank's y (fused gather)."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    _check(lib().anyq_dev_gemm_allgather(shard._h, C.c_void_p(x.data_ptr()), x.shape[0], C.byref(peers),
+                                         C.c_void_p(s.cuda_stream)))
+
+
+def tp_wait(shard: "DeviceTensor", peers, epoch: int, stream=None):
+    """Make the stream wait until every rank's contribution of call `epoch` landed."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().anyq_dev_tp_wait(shard._h, C.byref(peers), epoch, C.c_void_p(s.cuda_stream)))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    h = (C.c_uint8 * 64)()
+    _check(lib().anyq_ipc_handle(C.c_void_p(ptr), h))
+    return bytes(h)
+
+
+def ipc_open(handle: bytes) -> int:
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib().anyq_ipc_open(h, C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().anyq_ipc_close(C.c_void_p(ptr)))
 
 
 def column_mean_abs(x) -> np.ndarray:

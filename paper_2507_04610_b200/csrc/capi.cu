@@ -801,6 +801,43 @@ anyq_status anyq_dev_gemm_chain_path(int32_t n, const anyq_dev_tensor* const* t,
   });
 }
 
+anyq_status anyq_dev_gemm_allgather(const anyq_dev_tensor* shard, const void* x_bf16, int64_t m,
+                                    const anyq_tp_peers* tp, void* stream) {
+  return guard([&] {
+    lutgemv_tp_run(reinterpret_cast<const LutTensor*>(shard), x_bf16, m, tp, (cudaStream_t)stream);
+  });
+}
+
+anyq_status anyq_dev_tp_wait(const anyq_dev_tensor* shard, const anyq_tp_peers* tp, int32_t epoch,
+                             void* stream) {
+  return guard([&] {
+    if (epoch < 1) fail(ANYQ_ERR_SHAPE, "tp wait: epoch counts calls from 1");
+    // every rank's launch has one CTA per SM of its (identical) device
+    lutgemv_tp_wait(tp, epoch * lutgemv_tp_ctas(reinterpret_cast<const LutTensor*>(shard)), (cudaStream_t)stream);
+  });
+}
+
+anyq_status anyq_ipc_handle(const void* dev_ptr, uint8_t handle[64]) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof h == 64, "CUDA IPC handles are 64 bytes");
+    ANYQ_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+anyq_status anyq_ipc_open(const uint8_t handle[64], void** dev_ptr) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    ANYQ_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+anyq_status anyq_ipc_close(void* dev_ptr) {
+  return guard([&] { ANYQ_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
+}
+
 anyq_status anyq_dev_gemm_bf16(const anyq_dev_tensor* t, const void* x_bf16, int64_t m,
                                void* y_bf16, float* y_f32, void* stream) {
   return anyq_dev_gemm_bf16_path(t, x_bf16, m, y_bf16, y_f32, ANYQ_PATH_AUTO, stream);

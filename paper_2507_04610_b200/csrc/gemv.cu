@@ -76,6 +76,7 @@ constexpr uint32_t kTcGroupAb = 4 * 128u;                          // alpha/beta
 constexpr uint32_t kTcStageAb = kTcStageGroups * kTcGroupAb;
 constexpr int kTcMaxRing = 6;
 constexpr int kMaxProb = 8;
+constexpr int kMaxTp = 8;  // ranks of the fused tensor-parallel gather
 constexpr uint32_t kTblAddr = 0x10000;  // shared-window address of the pair table
 constexpr uint32_t kDynBase = 0x400;    // shared-window address of dynamic smem (sm_100)
 constexpr uint32_t kPre = kTblAddr - kDynBase;  // bytes of dynamic smem before the table
@@ -125,6 +126,13 @@ struct GvParams {
   int* done;             // [kMaxProb] per-problem release counters (self-resetting)
   int* err;              // device error word
   long long* trace;      // debug: [ncta][64] globaltimer stamps, or null
+  // tensor-parallel gather fused into the writer (single-problem launches):
+  // y also goes to every rank's full-width y buffer (NVLink peer stores), then
+  // each CTA bumps tp_flags[r][tp_rank] on every rank r (release, system scope)
+  int tp_world, tp_rank;
+  long long tp_row0, tp_N;
+  __nv_bfloat16* tp_y[kMaxTp];
+  int* tp_flags[kMaxTp];
 };
 
 // ---------------------------------------------------------------------------
@@ -460,8 +468,13 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
 #pragma unroll
         for (int m = 0; m < MP; ++m) {
           if (m < P.M) {
-            q.y[(size_t)m * q.N + row] = __float2bfloat16_rn(acc[m]);
-            if (q.y32) q.y32[(size_t)m * q.N + row] = acc[m];
+            const __nv_bfloat16 v = __float2bfloat16_rn(acc[m]);
+            if (P.tp_world == 0) {
+              q.y[(size_t)m * q.N + row] = v;
+              if (q.y32) q.y32[(size_t)m * q.N + row] = acc[m];
+            }
+            // the fused all-gather: this rank's slice straight into every rank's y
+            for (int r = 0; r < P.tp_world; ++r) P.tp_y[r][(size_t)m * P.tp_N + P.tp_row0 + row] = v;
           }
         }
       }
@@ -469,6 +482,11 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
       ++g;
     }
     __syncwarp();
+    if (P.tp_world > 0) __threadfence_system();  // every lane's peer stores before the flags
+    __syncwarp();
+    if (P.tp_world > 0 && lane < P.tp_world) {
+      asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(P.tp_flags[lane] + P.tp_rank) : "memory");
+    }
     if (lane == 0) {
       if (p < P.np - 1) {  // fire-and-forget release (this warp's y stores ordered by __syncwarp)
         asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&P.done[p]) : "memory");
@@ -1315,6 +1333,10 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
   P.ncta = ts[0]->gv_ncta;
   P.err = nullptr;  // set per launch (stream workspace)
   P.done = nullptr;
+  P.tp_world = 0;
+  P.tp_rank = 0;
+  P.tp_row0 = 0;
+  P.tp_N = 0;
   P.trace = g_gv_trace;
   // dependencies, x images and the chain's item sequence
   int tot = 0;
@@ -1601,6 +1623,83 @@ void lutgemv_tc_run(const LutTensor* t, const void* x, int64_t m, void* y, float
   void* ys[1] = {y};
   float* y32s[1] = {y32};
   lutgemv_tc_chain_run(1, ts, xs, ys, y32s, nullptr, m, s);
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-parallel GEMM with the all-gather fused into the writer
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_tp_wait(int* const* flags, int rank, int world, int expect) {
+  const int r = threadIdx.x;
+  if (r < world) {
+    const int* f = flags[rank] + r;
+    int v;
+    do {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v < expect) __nanosleep(64);
+    } while (v < expect);
+  }
+  __syncwarp();
+}
+}  // namespace
+
+void lutgemv_tp_run(const LutTensor* t, const void* x, int64_t m, const anyq_tp_peers* tp, cudaStream_t s) {
+  if (!t || !tp) fail(ANYQ_ERR_SHAPE, "tp gemm: null argument");
+  if (tp->world < 1 || tp->world > kMaxTp || tp->rank < 0 || tp->rank >= tp->world)
+    fail(ANYQ_ERR_SHAPE, "tp gemm: 1 <= world <= 8 and 0 <= rank < world");
+  if (m < 1 || m > kMaxMP) fail(ANYQ_ERR_SHAPE, "tp gemm: the fused gather runs on the GEMV (1 <= m <= 4)");
+  if (tp->row0 < 0 || tp->row0 + t->rows > tp->rows_total) fail(ANYQ_ERR_SHAPE, "tp gemm: shard outside y");
+  if (!gv_sbase_ok())
+    fail(ANYQ_ERR_CONFIG, "LUT GEMV: dynamic shared memory does not start at 0x400 on this device");
+  for (int r = 0; r < tp->world; ++r)
+    if (!tp->y[r] || !tp->flags[r]) fail(ANYQ_ERR_SHAPE, "tp gemm: every rank's y and flags must be mapped");
+  const LutTensor* ts[1] = {t};
+  const void* xs[1] = {x};
+  void* ys[1] = {tp->y[tp->rank]};  // unused: the writer stores through tp_y
+  GvParams P;
+  auto go = [&](auto mp) {
+    constexpr int MP = decltype(mp)::value;
+    const uint32_t smem_bytes = plan_chain<MP>(1, ts, xs, ys, nullptr, nullptr, m, P);
+    P.tp_world = tp->world;
+    P.tp_rank = tp->rank;
+    P.tp_row0 = tp->row0;
+    P.tp_N = tp->rows_total;
+    for (int r = 0; r < tp->world; ++r) {
+      P.tp_y[r] = static_cast<__nv_bfloat16*>(tp->y[r]);
+      P.tp_flags[r] = tp->flags[r];
+    }
+    const StreamWs ws = stream_ws(s);
+    P.done = ws.done;
+    P.err = ws.err + kErrGemv;
+    ensure_dyn_smem((const void*)k_lutgemv<MP>, (int)smem_bytes);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)P.ncta);
+    lc.blockDim = dim3(kT);
+    lc.dynamicSmemBytes = smem_bytes;
+    lc.stream = s;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_lutgemv<MP>, P));
+    ANYQ_LAUNCHED();
+    return 0;
+  };
+  if (m == 1) go(std::integral_constant<int, 1>{});
+  else if (m == 2) go(std::integral_constant<int, 2>{});
+  else if (m == 3) go(std::integral_constant<int, 3>{});
+  else go(std::integral_constant<int, 4>{});
+}
+
+int lutgemv_tp_ctas(const LutTensor* t) { return t ? t->gv_ncta : 0; }
+
+void lutgemv_tp_wait(const anyq_tp_peers* tp, int expect, cudaStream_t s) {
+  if (!tp || tp->world < 1 || tp->world > kMaxTp) fail(ANYQ_ERR_SHAPE, "tp wait: bad peers");
+  DevBuf<int*> f(tp->world, s);
+  ANYQ_CUDA(cudaMemcpyAsync(f.p, tp->flags, sizeof(int*) * tp->world, cudaMemcpyHostToDevice, s));
+  k_tp_wait<<<1, 32, 0, s>>>(f.p, tp->rank, tp->world, expect);
+  ANYQ_LAUNCHED();
 }
 
 void lutgemv_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y32,

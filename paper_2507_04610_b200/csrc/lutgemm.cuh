@@ -41,6 +41,12 @@ void lutgemv_set_trace(long long* dev);  // debug timeline ([ncta][16] int64), o
 void lutgemv_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                        float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
 bool lutgemv_fits(const LutTensor* t, int64_t m);  // GEMV applies (m <= 4, shared memory)
+// Row-sharded tensor-parallel GEMM with the all-gather fused into the GEMV
+// writer (peer stores + per-CTA system-scope flags), and the stream wait for a
+// full y (gemv.cu).
+void lutgemv_tp_run(const LutTensor* t, const void* x_bf16, int64_t m, const anyq_tp_peers* tp, cudaStream_t s);
+int lutgemv_tp_ctas(const LutTensor* t);
+void lutgemv_tp_wait(const anyq_tp_peers* tp, int expect, cudaStream_t s);
 void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                  cudaStream_t s);
 // K1t: the same chain with the products on tcgen05 (m <= 16; gemv.cu).

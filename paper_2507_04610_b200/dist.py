@@ -135,3 +135,73 @@ class RowShardedLinear:
 
     def close(self):
         self.dt.close()
+
+
+class FusedRowShardedLinear:
+    """Tensor-parallel A16W4 linear with the all-gather fused into the GEMV
+    writer (anyq_dev_gemm_allgather): every rank's kernel stores its y slice
+    straight into every rank's full-width y buffer over NVLink (CUDA IPC
+    mappings exchanged once through the process group) and signals a flag per
+    CTA; `__call__` returns this rank's full y after the flags of the call are
+    in (no NCCL call on the hot path). M <= 4 (the GEMV).
+
+    y buffers alternate between two slots by call parity, so the output of
+    call e stays valid until call e + 2 is issued; a decode loop's own data
+    dependency (every rank consumes y before the next layer's call) keeps the
+    ranks within that distance."""
+
+    def __init__(self, qt: QuantizedTensor, group=None, m_max: int = 4, align: int = 32):
+        import torch
+        import torch.distributed as dist
+
+        from . import anyq
+
+        self.group = group
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if world > 8:
+            raise ValueError("the fused gather supports up to 8 ranks")
+        self.world, self.rank, self.rows = world, rank, qt.rows
+        self.r0, self.r1 = row_range(qt.rows, world, rank, align)
+        self.dt = anyq.DeviceTensor(shard_rows(qt, self.r0, self.r1))
+        self.m_max = m_max
+        self.y = [torch.empty(m_max, qt.rows, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+        self.flags = [torch.zeros(world, dtype=torch.int32, device="cuda") for _ in range(2)]
+        mine = [(anyq.ipc_handle(self.y[s].data_ptr()), anyq.ipc_handle(self.flags[s].data_ptr())) for s in range(2)]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self.peers = []
+        for s in range(2):
+            yp, fp = [], []
+            for r in range(world):
+                if r == rank:
+                    yp.append(self.y[s].data_ptr())
+                    fp.append(self.flags[s].data_ptr())
+                else:
+                    a, b = anyq.ipc_open(allh[r][s][0]), anyq.ipc_open(allh[r][s][1])
+                    self._opened += [a, b]
+                    yp.append(a)
+                    fp.append(b)
+            self.peers.append(anyq.tp_peers(world, rank, qt.rows, self.r0, yp, fp))
+        self.calls = 0
+        dist.barrier(group=group)
+
+    def __call__(self, x):
+        from . import anyq
+
+        m = x.shape[0]
+        if m > self.m_max:
+            raise ValueError(f"at most {self.m_max} rows of x")
+        s = self.calls & 1
+        self.calls += 1
+        anyq.gemm_allgather(self.dt, x, self.peers[s])
+        anyq.tp_wait(self.dt, self.peers[s], (self.calls + 1) // 2)
+        return self.y[s][:m]
+
+    def close(self):
+        from . import anyq
+
+        for p in self._opened:
+            anyq.ipc_close(p)
+        self._opened = []
+        self.dt.close()
