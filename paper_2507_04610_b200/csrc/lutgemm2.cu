@@ -9,18 +9,19 @@
 //
 // A CTA computes 128 W rows x NT tokens tiles (persistent, round-robin over the
 // tiles, tokens innermost so concurrently running CTAs share the weight rows in
-// L2). Per 128-k step:
-//  * an x producer lane issues the x tile as two TMA tensor loads (box 64 k x
-//    NT tokens, SWIZZLE_128B: the canonical UMMA K-major layout) into a 4-6
+// L2). A pipeline step covers kK2Cps = 2 chunks of 128 k (one step per chunk
+// measured 15% slower: the per-step barriers and waits dominate). Per step:
+//  * an x producer lane issues the x tile as TMA tensor loads (box 64 k x
+//    NT tokens, SWIZZLE_128B: the canonical UMMA K-major layout) into a 2-4
 //    stage ring; a code producer lane streams the step's codes (4 row blocks x
-//    2 KB of the prepacked layout) and alpha/beta lines by bulk copies into an
-//    8-stage ring (the weight stream is the HBM-latency-bound one);
+//    2 x 2 KB, contiguous per row block in the prepacked layout) and
+//    alpha/beta lines by bulk copies into a 4-stage ring;
 //  * 16 dequant warps (row block q = warp & 3 = TMEM lane quarter, k quarter
 //    j = warp >> 2; lane = row) build a private 16-entry bf16 table
 //    bf16(alpha * T[i] + beta) of their row for the step, look each code up
 //    (one LDS.U16 per weight) and store the bf16 pairs straight into TMEM as
-//    the A operand (tcgen05.st; 4 A stages of 64 columns);
-//  * one thread issues 8 tcgen05.mma kind::f16 (bf16 x bf16, M = 128, N = NT,
+//    the A operand (tcgen05.st; 2 A stages of 128 columns);
+//  * one thread issues 16 tcgen05.mma kind::f16 (bf16 x bf16, M = 128, N = NT,
 //    K = 16; A from TMEM, B from shared memory, D in TMEM) and commits;
 //  * 4 epilogue warps read the finished tile from TMEM (two accumulator
 //    buffers, so the next tile's MMAs overlap) and store y (bf16, optionally
@@ -44,25 +45,31 @@ constexpr int kK2Mma = 20;
 constexpr int kK2ProdX = 21;    // x tiles (TMA tensor loads)
 constexpr int kK2ProdC = 22;    // codes + alpha/beta (bulk copies)
 constexpr int kK2T = 23 * 32;
-constexpr int kK2CStages = 8;             // code ring
-constexpr int kK2AStages = 4;             // A stages in TMEM (64 columns each)
-constexpr uint32_t kK2Codes = 4 * 2048;   // codes of one step: 4 row blocks x one chunk
-constexpr uint32_t kK2Ab = 4 * 128;       // alpha/beta lines of one step
+#ifndef K2_CPS
+#define K2_CPS 2
+#endif
+constexpr int kK2Cps = K2_CPS;                     // 128-k chunks per pipeline step
+constexpr int kK2CStages = 8 / kK2Cps;             // code ring
+constexpr int kK2AStages = 4 / kK2Cps;             // A stages in TMEM (64 columns per chunk)
+constexpr uint32_t kK2Codes = 4 * kK2Cps * 2048;   // codes of one step: 4 row blocks x kK2Cps chunks
+constexpr uint32_t kK2Ab = 4 * kK2Cps * 128;       // alpha/beta lines of one step (at most one per chunk)
 constexpr uint32_t kK2CStage = kK2Codes + kK2Ab;
-constexpr uint32_t kK2Tbl = 16 * 64;      // a row block's table: 16 entries x 32 rows x bf16 (x2 buffers)
+constexpr uint32_t kK2Tbl = 16 * 64;      // one chunk's table of a row block: 16 entries x 32 rows x bf16
 
 template <int NT>
 struct K2Cfg {
-  static constexpr int kXStages = NT >= 128 ? 4 : 6;
+  static constexpr int kXStages = kK2Cps == 1 ? (NT >= 128 ? 4 : 6) : (NT >= 128 ? 2 : 4);
   static constexpr uint32_t kBox = NT * 128;           // one 64-k x NT box of x (bf16), 1024-aligned
-  static constexpr uint32_t kB = 2 * kBox;             // x of one 128-k step
+  static constexpr uint32_t kB = 2 * kK2Cps * kBox;    // x of one step
   static constexpr uint32_t kOffB = 0;
   static constexpr uint32_t kOffC = kOffB + kXStages * kB;
   static constexpr uint32_t kOffTbl = kOffC + kK2CStages * kK2CStage;
-  static constexpr uint32_t kOffBars = kOffTbl + 4 * 2 * kK2Tbl;
+  static constexpr uint32_t kOffBars = kOffTbl + 4 * 2 * kK2Cps * kK2Tbl;
   static constexpr uint32_t kSmem = kOffBars + 512;
   static constexpr uint32_t kACol0 = 2 * NT;            // D buffers at columns [0, 2 NT), A after
   static constexpr int kTmemCols = 512;
+  static_assert(kACol0 + kK2AStages * 64 * kK2Cps <= kTmemCols, "TMEM budget");
+  static_assert(kSmem <= 227 * 1024, "shared memory budget");
   // kind::f16 instruction descriptor: D f32 (bit 4), A and B bf16 (format 1 at
   // bits 7 and 10), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   static constexpr uint32_t kIdesc =
@@ -194,6 +201,8 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
   const int ntiles = P.rtiles * P.ttiles;
   const int C = P.C;
 
+  const int S = (C + kK2Cps - 1) / kK2Cps;  // steps per tile
+
   if (warp == kK2ProdX) {
     // ------------------------------------------------------------ x producer
     if (lane == 0) {
@@ -202,13 +211,16 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       uint32_t round = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int tt = tile % P.ttiles;
-        for (int c = 0; c < C; ++c) {
+        for (int sp = 0; sp < S; ++sp) {
+          const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
           if (round > 0) mbar_wait(bars + kQXEmpty + 8 * st, (round - 1) & 1);
           const uint32_t full = bars + kQXFull + 8 * st;
-          mbar_expect_tx(full, CF::kB);
+          mbar_expect_tx(full, (uint32_t)nc * 2 * CF::kBox);
           const uint32_t b = sbase + CF::kOffB + st * CF::kB;
-          tma_load_2d(b, &xmap, c * 128, tt * NT, full);
-          tma_load_2d(b + CF::kBox, &xmap, c * 128 + 64, tt * NT, full);
+          for (int h = 0; h < nc; ++h) {
+            tma_load_2d(b + 2 * h * CF::kBox, &xmap, (c0 + h) * 128, tt * NT, full);
+            tma_load_2d(b + (2 * h + 1) * CF::kBox, &xmap, (c0 + h) * 128 + 64, tt * NT, full);
+          }
           if (++st == XS) {
             st = 0;
             ++round;
@@ -224,16 +236,18 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int rt = tile / P.ttiles;
         const int nrb = min(4, P.RB - 4 * rt);
-        for (int c = 0; c < C; ++c) {
+        for (int sp = 0; sp < S; ++sp) {
+          const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
+          const int g0 = c0 >> P.gshift, ng = ((c0 + nc - 1) >> P.gshift) - g0 + 1;
           if (round > 0) mbar_wait(bars + kQCEmpty + 8 * st, (round - 1) & 1);
           const uint32_t full = bars + kQCFull + 8 * st;
-          mbar_expect_tx(full, (uint32_t)nrb * (2048 + 128));
+          mbar_expect_tx(full, (uint32_t)nrb * (nc * 2048 + ng * 128));
           const uint32_t cs = sbase + CF::kOffC + st * kK2CStage;
-          const int g = c >> P.gshift;
           for (int q = 0; q < nrb; ++q) {
             const int rb = 4 * rt + q;
-            bulk_g2s(cs + q * 2048, P.codes + ((size_t)rb * C + c) * 2048, 2048, full);
-            bulk_g2s(cs + kK2Codes + q * 128, P.ab + ((size_t)rb * P.GR + g) * 32, 128, full);
+            // a row block's chunks are contiguous in the prepacked layout
+            bulk_g2s(cs + q * kK2Cps * 2048, P.codes + ((size_t)rb * C + c0) * 2048, nc * 2048, full);
+            bulk_g2s(cs + kK2Codes + q * kK2Cps * 128, P.ab + ((size_t)rb * P.GR + g0) * 32, ng * 128, full);
           }
           if (++st == kK2CStages) {
             st = 0;
@@ -250,20 +264,26 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       const int db = tl & 1;
       if (tl >= 2) mbar_wait(bars + kQDEmpty + 8 * db, (uint32_t)(((tl >> 1) - 1) & 1));
       const uint32_t d = tmem + (uint32_t)db * NT;
-      for (int c = 0; c < C; ++c) {
+      for (int sp = 0; sp < S; ++sp) {
+        const int nc = min(kK2Cps, C - sp * kK2Cps);
         mbar_wait(bars + kQXFull + 8 * xs, xround & 1);
         mbar_wait(bars + kQAFull + 8 * as, around & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t a = tmem + CF::kACol0 + (uint32_t)as * 64;
+          const uint32_t a = tmem + CF::kACol0 + (uint32_t)as * (64 * kK2Cps);
           const uint32_t b = sbase + CF::kOffB + xs * CF::kB;
 #pragma unroll
-          for (int s = 0; s < 8; ++s)
-            tc_mma_ts(d, a + s * 8, desc_b(b + (s >> 2) * CF::kBox + (s & 3) * 32), CF::kIdesc,
-                      (c > 0 || s > 0) ? 1u : 0u);
+          for (int h = 0; h < kK2Cps; ++h) {
+            if (h < nc) {  // a missing last chunk: its A and B are stale, skip its MMAs
+#pragma unroll
+              for (int s = 0; s < 8; ++s)
+                tc_mma_ts(d, a + h * 64 + s * 8, desc_b(b + (2 * h + (s >> 2)) * CF::kBox + (s & 3) * 32),
+                          CF::kIdesc, (sp > 0 || h > 0 || s > 0) ? 1u : 0u);
+            }
+          }
           tc_commit(bars + kQXEmpty + 8 * xs);
           tc_commit(bars + kQAEmpty + 8 * as);
-          if (c == C - 1) tc_commit(bars + kQDFull + 8 * db);
+          if (sp == S - 1) tc_commit(bars + kQDFull + 8 * db);
         }
         __syncwarp();
         if (++xs == XS) {
@@ -308,12 +328,12 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     }
   } else {
     // ------------------------------------------------------------ dequant
-    // the row block's 4 warps share its per-step table (two buffers by step
+    // the row block's 4 warps share its per-chunk tables (two sets by step
     // parity): warp j builds entries 4j..4j+3, a 128-thread named barrier
-    // (one per row block) publishes it
+    // (one per row block) publishes them
     const int q = warp & 3, j = warp >> 2;
-    uint16_t* tbl0 = reinterpret_cast<uint16_t*>(smem + CF::kOffTbl + q * 2 * kK2Tbl);
-    const uint32_t tblw0 = sbase + CF::kOffTbl + q * 2 * kK2Tbl + lane * 2;
+    uint16_t* tbl0 = reinterpret_cast<uint16_t*>(smem + CF::kOffTbl + q * 2 * kK2Cps * kK2Tbl);
+    const uint32_t tblw0 = sbase + CF::kOffTbl + q * 2 * kK2Cps * kK2Tbl + lane * 2;
     int par = 0;
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + CF::kACol0;
     int cs = 0, as = 0;
@@ -338,50 +358,76 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
           T[2 * i + 1] = f.y;
         }
       }
-      for (int c = 0; c < C; ++c) {
+      for (int sp = 0; sp < S; ++sp) {
+        const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
         mbar_wait(bars + kQCFull + 8 * cs, cround & 1);
-        uint32_t v[16];
+        uint32_t v[16 * kK2Cps];
         if (live) {
           const uint8_t* cst = smem + CF::kOffC + cs * kK2CStage;
-          const float2 ab = __half22float2(*reinterpret_cast<const __half2*>(cst + kK2Codes + q * 128 + lane * 4));
-          const uint4 w4 = *reinterpret_cast<const uint4*>(cst + q * 2048 + j * 512 + lane * 16);
+          const int g0 = c0 >> P.gshift;
+          float2 ab[kK2Cps];
+          uint4 w4[kK2Cps];
+#pragma unroll
+          for (int h = 0; h < kK2Cps; ++h) {
+            if (h < nc) {
+              const int gl = ((c0 + h) >> P.gshift) - g0;
+              ab[h] = __half22float2(
+                  *reinterpret_cast<const __half2*>(cst + kK2Codes + (q * kK2Cps + gl) * 128 + lane * 4));
+              w4[h] = *reinterpret_cast<const uint4*>(cst + (q * kK2Cps + h) * 2048 + j * 512 + lane * 16);
+            }
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(bars + kQCEmpty + 8 * cs);  // codes and scales are in registers
-          // bf16(alpha * T[i] + beta) for this row and step (fp32, one rounding)
-          uint16_t* tbl = tbl0 + par * (kK2Tbl / 2);
+          // bf16(alpha * T[i] + beta) for this row and chunk (fp32, one rounding)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            tbl[(4 * j + i) * 32 + lane] =
-                __bfloat16_as_ushort(__float2bfloat16_rn(__fadd_rn(__fmul_rn(ab.x, T[4 * j + i]), ab.y)));
+          for (int h = 0; h < kK2Cps; ++h) {
+            if (h < nc) {
+              uint16_t* tbl = tbl0 + (par * kK2Cps + h) * (kK2Tbl / 2);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                tbl[(4 * j + i) * 32 + lane] = __bfloat16_as_ushort(
+                    __float2bfloat16_rn(__fadd_rn(__fmul_rn(ab[h].x, T[4 * j + i]), ab[h].y)));
+            }
+          }
           asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
           // entry i of row `lane` at tbl + i * 64 + lane * 2, the table 1024-B aligned: the
           // address of nibble n of a code word is ((w >> (4n - 6)) & 0x3C0) | (tbl + lane * 2)
-          const uint32_t tblw = tblw0 + par * kK2Tbl;
-          const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-          for (int bb = 0; bb < 16; ++bb) {
-            const uint32_t w = wd[bb >> 2];
-            const int nlo = 8 * (bb & 3), nhi = nlo + 4;  // bit offsets of the two nibbles
-            const uint32_t alo = ((nlo >= 6 ? (w >> (nlo - 6)) : (w << (6 - nlo))) & 0x3C0u) | tblw;
-            const uint32_t ahi = ((nhi >= 6 ? (w >> (nhi - 6)) : (w << (6 - nhi))) & 0x3C0u) | tblw;
-            uint32_t lo, hi;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(lo) : "r"(alo));
-            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hi) : "r"(ahi));
-            v[bb] = __byte_perm(lo, hi, 0x5410);
+          for (int h = 0; h < kK2Cps; ++h) {
+            if (h < nc) {
+              const uint32_t tblw = tblw0 + (par * kK2Cps + h) * kK2Tbl;
+              const uint32_t wd[4] = {w4[h].x, w4[h].y, w4[h].z, w4[h].w};
+#pragma unroll
+              for (int bb = 0; bb < 16; ++bb) {
+                const uint32_t w = wd[bb >> 2];
+                const int nlo = 8 * (bb & 3), nhi = nlo + 4;  // bit offsets of the two nibbles
+                const uint32_t alo = ((nlo >= 6 ? (w >> (nlo - 6)) : (w << (6 - nlo))) & 0x3C0u) | tblw;
+                const uint32_t ahi = ((nhi >= 6 ? (w >> (nhi - 6)) : (w << (6 - nhi))) & 0x3C0u) | tblw;
+                uint32_t lo, hi;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(lo) : "r"(alo));
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hi) : "r"(ahi));
+                v[16 * h + bb] = __byte_perm(lo, hi, 0x5410);
+              }
+            }
           }
         } else {
           __syncwarp();
           if (lane == 0) mbar_arrive(bars + kQCEmpty + 8 * cs);
         }
         par ^= 1;
-        // bytes 0..7: k = 16j + 2b (+1) -> slice j (A columns 8j..); bytes 8..15: k = 64 + 16j + ...
-        // -> slice 4 + j (columns 32 + 8j..)
+        // chunk h, bytes 0..7: k = 16j + 2b (+1) -> slice j (A columns 64h + 8j..); bytes 8..15:
+        // k = 64 + 16j + ... -> slice 4 + j (columns 64h + 32 + 8j..)
         if (around > 0) mbar_wait(bars + kQAEmpty + 8 * as, (around - 1) & 1);
         tc_fence_after();
         if (live) {
-          const uint32_t ta = tq + (uint32_t)as * 64;
-          tc_st8(ta + 8 * j, v);
-          tc_st8(ta + 32 + 8 * j, v + 8);
+          const uint32_t ta = tq + (uint32_t)as * (64 * kK2Cps);
+#pragma unroll
+          for (int h = 0; h < kK2Cps; ++h) {
+            if (h < nc) {
+              tc_st8(ta + 64 * h + 8 * j, v + 16 * h);
+              tc_st8(ta + 64 * h + 32 + 8 * j, v + 16 * h + 8);
+            }
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
