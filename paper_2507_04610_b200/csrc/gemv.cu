@@ -5,8 +5,12 @@
 // is the reference's gemm_fused (qgemm.cpp:71-128) with the per-group scale
 // factored out of the k loop. Per 128-k chunk c:
 //   y[m][n] += alpha_g * 2^-e * sum_{k in c} xh[m][k] * T_n[c[n][k]] + beta_g * sum_{k in c} x[m][k]
-// where xh = fp16(x * 2^e) is EXACT (bf16 has 8 significant bits, fp16 11;
-// e puts max|x| of the chunk in [2^14, 2^15)). Every product xh * T
+// where xh = fp16(x * 2^e), e putting max|x| of the chunk in [2^14, 2^15),
+// is exact for every |x| >= 2^-32 max|x| (bf16 has 8 significant bits; fp16
+// keeps them down to 2^-17, inside its subnormal range); smaller values round
+// to the fp16 subnormal grid (error <= 2^-40 max|x| per element, far inside
+// the tolerance; tests/test_gpu_headline.py::test_gemv_wide_dynamic_range_x).
+// Every product xh * T
 // (fp16 x fp16) is formed exactly by FHFMA (fma.rn.f32.f16) and accumulated in
 // fp32, so the result differs from the fp32 reference only by summation order
 // (tolerance 1e-5 * sum|x*w|, tests/test_gpu_gemm.py).

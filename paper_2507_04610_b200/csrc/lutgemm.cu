@@ -22,8 +22,10 @@
 //  * Per scale group a fresh accumulator (4 TMEM slots); the owning team
 //    drains it one chunk later (tcgen05.ld), applies alpha (and beta * sum x)
 //    in fp32 registers. x enters as fp16 scaled by 2^e per (group, row of x):
-//    bf16 -> fp16 is then exact, so products are exact and accumulation is
-//    fp32 — results match the fp32 reference to accumulation-order rounding.
+//    bf16 -> fp16 is then exact down to 2^-32 of the chunk's max|x| (below,
+//    the fp16 subnormal grid rounds by <= 2^-40 max|x|), products are exact
+//    and accumulation is fp32 — results match the fp32 reference to
+//    accumulation-order rounding.
 //  * A producer warp streams 128-k code chunks (2 KB per 32 rows) and the x
 //    images with cp.async.bulk into a 4-stage mbarrier ring; one thread of
 //    the MMA warp issues tcgen05.mma and tcgen05.commit.
@@ -245,7 +247,8 @@ __global__ void __launch_bounds__(128) k_xprep(const __nv_bfloat16* __restrict__
                                                float* __restrict__ xsum) {
   // one block per 128-k chunk; warp w handles rows m = w, w+4, ...; lane owns
   // k = 128c + 4*lane + [0,4). Scale 2^e per (chunk, m) puts max|x| in
-  // [2^14, 2^15): bf16 -> fp16 is then exact (8 significant bits).
+  // [2^14, 2^15): bf16 -> fp16 is then exact (8 significant bits) for every
+  // |x| >= 2^-32 max|x|; smaller values land on the fp16 subnormal grid.
   constexpr int NB = 4 * MP;
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
