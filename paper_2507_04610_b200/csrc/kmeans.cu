@@ -820,6 +820,7 @@ struct WarpKm {
   long long vkeys[2 * kWK], vvals[2 * kWK];
   Rng rng;
   int ncen;
+  double closs[kWK];      // per-cluster loss under the updated centroid
   double redd[kMaxG];  // cross-warp reduction slots
   long long redl[kMaxG], redl2[kMaxG];
   int redi[kMaxG];
@@ -1175,7 +1176,7 @@ __device__ void w_init_random(const WRow& R, const float* sk, WarpKm& S, int k, 
 // iteration i+1 (a pure function of the updated centroids) runs first,
 // speculatively; when the stop test then fires, its results are simply not
 // used. Rows with repairs in the iteration take separate passes.
-__device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* FP, double* LP,
+__device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* CT,
                           const int* svals_row, const Grp& g, bool need_loss, int* bail) {
   const int n = R.n, C = R.C, k = P.k, lo = R.lo, hi = R.hi;
   const double xmax = fmax(fabs((double)R.x_at(0)), fabs((double)R.x_at(n - 1)));
@@ -1268,82 +1269,6 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     KM_PHASE(4);
     return true;
   };
-  // ---- M-step sums over seg/so (per-thread runs, combined later in chunk
-  // order); with fused = true also the loss of the previous labels pseg/pso
-  // under the current centroids (no exceptions), returned as this thread's part
-  auto mpass = [&](bool fused) -> double {
-    long long tph = clock64();
-    double lb[4] = {0.0, 0.0, 0.0, 0.0};
-    int ro = 0, end_o = 0;
-    double c_o = 0.0;
-    if (fused) {
-      while (ro < k - 1 && S.pseg[ro + 1] <= lo) ++ro;
-      end_o = S.pseg[ro + 1];
-      c_o = S.cen[S.pso[ro]];
-    }
-    auto loss_term = [&](int pp, double w, double x, int u) {
-      while (pp >= end_o) {  // next run of the previous labels
-        ++ro;
-        end_o = S.pseg[ro + 1];
-        c_o = S.cen[S.pso[ro]];
-      }
-      lb[u] = __dadd_rn(lb[u], __dmul_rn(w, dcost(x, c_o)));
-    };
-      int r = 0, nr = 0;
-      for (int p = lo; p < hi;) {
-        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
-        const int pend = min(hi, S.seg[r + 1]);
-        const int q = S.so[r];
-        // four interleaved partial sums per quantity (fixed order), folded per run
-        double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0}, b2[4] = {0.0, 0.0, 0.0, 0.0};
-        int j = p - lo;
-        const int je = pend - lo;
-        for (; j + 8 <= je; j += 8) {  // loads first, then the sums
-          float xv[8], wq[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            xv[u] = R.xs[R.idx(g.t, j + u)];
-            wq[u] = R.wv[R.idx(g.t, j + u)];
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const double w = (double)wq[u], x = (double)xv[u];
-            b0[u & 3] = __dadd_rn(b0[u & 3], __dmul_rn(w, x));
-            b1[u & 3] = __dadd_rn(b1[u & 3], w);
-            b2[u & 3] = __dadd_rn(b2[u & 3], x);
-            if (fused) loss_term(lo + j + u, w, x, u & 3);
-          }
-        }
-        for (; j < je; ++j) {  // remainder (< 8) into the first partials: small code
-          const double w = (double)R.wv[R.idx(g.t, j)], x = (double)R.xs[R.idx(g.t, j)];
-          b0[0] = __dadd_rn(b0[0], __dmul_rn(w, x));
-          b1[0] = __dadd_rn(b1[0], w);
-          b2[0] = __dadd_rn(b2[0], x);
-          if (fused) loss_term(lo + j, w, x, 0);
-        }
-        const double a0 = __dadd_rn(__dadd_rn(b0[0], b0[1]), __dadd_rn(b0[2], b0[3]));
-        const double a1 = __dadd_rn(__dadd_rn(b1[0], b1[1]), __dadd_rn(b1[2], b1[3]));
-        const double a2 = __dadd_rn(__dadd_rn(b2[0], b2[1]), __dadd_rn(b2[2], b2[3]));
-        if (nr == 0) {
-          FP[g.t * 3 + 0] = a0;
-          FP[g.t * 3 + 1] = a1;
-          FP[g.t * 3 + 2] = a2;
-        } else if (pend < hi) {  // interior run: the whole cluster lies in this chunk
-          S.swx[q] = a0;
-          S.sw[q] = a1;
-          S.sx[q] = a2;
-        } else {
-          LP[g.t * 3 + 0] = a0;
-          LP[g.t * 3 + 1] = a1;
-          LP[g.t * 3 + 2] = a2;
-        }
-        ++nr;
-        p = pend;
-      }
-      __syncthreads();
-    KM_PHASE(9);
-    return __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
-  };
   // ---- loss of the labels pseg/pso (+ the exceptions pexc) under the current
   // centroids (chunk order, then fixed tree)
   auto losspass = [&]() -> double {
@@ -1381,51 +1306,129 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     return __dadd_rn(__dadd_rn(lb[0], lb[1]), __dadd_rn(lb[2], lb[3]));
   };
 
+  // ---- M-step sums without a pass over the row: a cluster is one segment
+  // [a, z) of the sorted row, i.e. a head run in chunk a / C, whole chunks, and
+  // a tail run in chunk (z - 1) / C. Whole-chunk sums (CT, once per row) and
+  // the head / tail runs are formed exactly as the per-thread run sums of a
+  // full pass (four interleaved partials per quantity from the run start,
+  // folded), and combined in chunk order: the same values as summing every
+  // run of the row each iteration, at O(C + T) per cluster instead of O(n).
+  // w x x rides along for the cluster loss.
+  auto runsum = [&](int t, int j0, int j1, double (&o)[4]) {
+    double b0[4] = {0.0, 0.0, 0.0, 0.0}, b1[4] = {0.0, 0.0, 0.0, 0.0}, b2[4] = {0.0, 0.0, 0.0, 0.0};
+    double b3[4] = {0.0, 0.0, 0.0, 0.0};
+    int j = j0;
+    for (; j + 8 <= j1; j += 8) {
+      float xv[8], wq[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        xv[u] = R.xs[R.idx(t, j + u)];
+        wq[u] = R.wv[R.idx(t, j + u)];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double w = (double)wq[u], x = (double)xv[u];
+        const double wx = __dmul_rn(w, x);
+        b0[u & 3] = __dadd_rn(b0[u & 3], wx);
+        b1[u & 3] = __dadd_rn(b1[u & 3], w);
+        b2[u & 3] = __dadd_rn(b2[u & 3], x);
+        b3[u & 3] = __fma_rn(wx, x, b3[u & 3]);
+      }
+    }
+    for (; j < j1; ++j) {
+      const double w = (double)R.wv[R.idx(t, j)], x = (double)R.xs[R.idx(t, j)];
+      const double wx = __dmul_rn(w, x);
+      b0[0] = __dadd_rn(b0[0], wx);
+      b1[0] = __dadd_rn(b1[0], w);
+      b2[0] = __dadd_rn(b2[0], x);
+      b3[0] = __fma_rn(wx, x, b3[0]);
+    }
+    o[0] = __dadd_rn(__dadd_rn(b0[0], b0[1]), __dadd_rn(b0[2], b0[3]));
+    o[1] = __dadd_rn(__dadd_rn(b1[0], b1[1]), __dadd_rn(b1[2], b1[3]));
+    o[2] = __dadd_rn(__dadd_rn(b2[0], b2[1]), __dadd_rn(b2[2], b2[3]));
+    o[3] = __dadd_rn(__dadd_rn(b3[0], b3[1]), __dadd_rn(b3[2], b3[3]));
+  };
+  {
+    double o[4];
+    runsum(g.t, 0, hi - lo, o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) CT[g.t * 4 + i] = o[i];
+    __syncthreads();
+  }
   if (!estep()) return 0.0;
-  mpass(false);
   double prev = INFINITY;
   for (int iter = 0; iter < P.max_iters; ++iter) {
     long long tph = clock64();
-    // ---- M-step: combine the chunk partials, update the centroids
+    // ---- M-step; each cluster's loss under its updated centroid (used by the
+    // stop test when the iteration has no repairs)
     {
-      if (g.t < k) {
-        const int q = g.t;
-        const int rq = S.rank_of[q];
-        const int a = S.seg[rq], z = S.seg[rq + 1];
-        S.cnt[q] = z - a;
-        if (z > a) {
-          const int t0 = a / C, t1 = (z - 1) / C;
-          const bool starts_chunk = a == t0 * C;
-          const bool ends_chunk = z == min(n, (t0 + 1) * C);
-          if (t0 == t1) {
-            if (starts_chunk) {
-              S.swx[q] = FP[t0 * 3 + 0];
-              S.sw[q] = FP[t0 * 3 + 1];
-              S.sx[q] = FP[t0 * 3 + 2];
-            } else if (ends_chunk) {
-              S.swx[q] = LP[t0 * 3 + 0];
-              S.sw[q] = LP[t0 * 3 + 1];
-              S.sx[q] = LP[t0 * 3 + 2];
-            }  // else: interior run, already complete
-          } else {
-            const double* f0 = starts_chunk ? &FP[t0 * 3] : &LP[t0 * 3];
-            double s0 = f0[0], s1 = f0[1], s2 = f0[2];
-            for (int t = t0 + 1; t <= t1; ++t) {
-              s0 = __dadd_rn(s0, FP[t * 3 + 0]);
-              s1 = __dadd_rn(s1, FP[t * 3 + 1]);
-              s2 = __dadd_rn(s2, FP[t * 3 + 2]);
+      // warp 0: lane q < k sums cluster q's head run and whole chunks, lane
+      // 16 + q its tail run (k <= 16), added last as in chunk order
+      if (g.warp == 0) {
+        const int q = g.lane & 15;
+        const bool tail_lane = g.lane >= 16;
+        int a = 0, z = 0, t0 = 0, t1 = 0;
+        double d[4] = {0.0, 0.0, 0.0, 0.0};
+        // one run per lane (head or tail), one runsum call for the whole warp
+        int rt = 0, rj0 = 0, rj1 = 0;
+        if (q < k) {
+          const int rq = S.rank_of[q];
+          a = S.seg[rq];
+          z = S.seg[rq + 1];
+          t0 = a / C;
+          t1 = z > a ? (z - 1) / C : t0;
+          if (z > a) {
+            if (t0 == t1) {
+              if (!tail_lane) {
+                rt = t0;
+                rj0 = a - t0 * C;
+                rj1 = z - t0 * C;
+              }
+            } else if (tail_lane) {
+              rt = t1;
+              rj1 = z - t1 * C;
+            } else {
+              rt = t0;
+              rj0 = a - t0 * C;
+              rj1 = min(C, n - t0 * C);
             }
-            S.swx[q] = s0;
-            S.sw[q] = s1;
-            S.sx[q] = s2;
           }
         }
-      }
-      __syncthreads();
-      if (g.t < k && S.cnt[g.t] > 0) {
-        const int q = g.t;
-        if (S.sw[q] > 0.0) S.cen[q] = __ddiv_rn(S.swx[q], S.sw[q]);
-        else S.cen[q] = __ddiv_rn(S.sx[q], (double)S.cnt[q]);
+        runsum(rt, rj0, rj1, d);
+        if (!tail_lane && q < k && z > a) {
+          for (int t = t0 + 1; t < t1; ++t) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[i] = __dadd_rn(d[i], CT[t * 4 + i]);
+          }
+        }
+        double e[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e[i] = __shfl_down_sync(kFull, d[i], 16);
+        if (!tail_lane && q < k) {
+          double cl = 0.0;
+          S.cnt[q] = z - a;
+          if (z > a) {
+            if (t1 > t0) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) d[i] = __dadd_rn(d[i], e[i]);
+            }
+            S.swx[q] = d[0];
+            S.sw[q] = d[1];
+            S.sx[q] = d[2];
+            const double c = d[1] > 0.0 ? __ddiv_rn(d[0], d[1]) : __ddiv_rn(d[2], (double)(z - a));
+            S.cen[q] = c;
+            const double xa = (double)R.x_at(a), xz = (double)R.x_at(z - 1);
+            if (xa == xz) {
+              cl = __dmul_rn(d[1], dcost(xa, c));  // exactly 0 iff every sample sits on c
+            } else {
+              // sum w (x - c)^2 = swxx - 2 c swx + c^2 sw; its rounding only reaches the
+              // rel_tol test (relative error ~1e-12 against rel_tol 1e-6)
+              cl = fmax(0.0, __dadd_rn(__dsub_rn(d[3], __dmul_rn(2.0 * c, d[0])),
+                                       __dmul_rn(__dmul_rn(c, c), d[1])));
+            }
+          }
+          S.closs[q] = cl;
+        }
       }
       if (g.t == 0) S.nexc = 0;
       __syncthreads();
@@ -1561,17 +1564,15 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     }
     __syncthreads();
     KM_PHASE(10);
-    // ---- loss of this iteration, fused with the next iteration's E/M-step
-    const bool last = iter + 1 >= P.max_iters;
-    if (!last && !estep()) return 0.0;
-    double local;
-    if (!last && S.pnexc == 0) {
-      local = mpass(true);
+    // ---- loss of this iteration: per-cluster sums when nothing was repaired,
+    // else a pass over the repaired labels (pseg/pso + exceptions)
+    double loss_m;
+    if (S.pnexc == 0) {
+      loss_m = 0.0;
+      for (int r = 0; r < k; ++r) loss_m = __dadd_rn(loss_m, S.closs[S.so[r]]);  // rank order
     } else {
-      local = losspass();
-      if (!last) mpass(false);
+      loss_m = g_sum(losspass(), S, g);
     }
-    const double loss_m = g_sum(local, S, g);
     KM_PHASE(7);
     if (g.t == 0) {
       const bool stable = !S.chg && iter > 0;
@@ -1583,6 +1584,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* F
     const int stop = S.bci;
     __syncthreads();
     if (stop) break;
+    if (iter + 1 < P.max_iters && !estep()) return 0.0;
   }
   if (!need_loss) return 0.0;
   // final reassignment and loss (learner.cpp:305-311)
@@ -1606,8 +1608,7 @@ __global__ void __launch_bounds__(256, 2) k_kmeans_warp(WkParams P) {
   g.G = blockDim.x >> 5;
   g.T = blockDim.x;
   WarpKm& S = *reinterpret_cast<WarpKm*>(dsmem);
-  double* FP = reinterpret_cast<double*>(dsmem + ((sizeof(WarpKm) + 15) & ~size_t(15)));
-  double* LP = FP + 3 * g.T;
+  double* CT = reinterpret_cast<double*>(dsmem + ((sizeof(WarpKm) + 15) & ~size_t(15)));
   float* xs = reinterpret_cast<float*>(dsmem + P.state_bytes);
   const int n = P.n, C = P.C, k = P.k;
   float* wv = xs + (size_t)C * (g.T + 1);
@@ -1670,7 +1671,7 @@ __global__ void __launch_bounds__(256, 2) k_kmeans_warp(WkParams P) {
       });
       __syncthreads();
       const long long t1 = clock64();
-      const double loss = w_lloyd(P, R, S, FP, LP, sv_row, g, P.restarts > 1, &bail);
+      const double loss = w_lloyd(P, R, S, CT, sv_row, g, P.restarts > 1, &bail);
       if (P.dbg && g.t == 0) {
         atomicAdd((unsigned long long*)&P.dbg[0], (unsigned long long)(t1 - t0));
         atomicAdd((unsigned long long*)&P.dbg[1], (unsigned long long)(clock64() - t1));
@@ -1857,7 +1858,7 @@ void launch_kmeans(const float* ws, const float* sw, int64_t rows, int64_t cols,
   const int T = 32 * G;
   const int64_t Cw = (cols + T - 1) / T;
   const uint32_t state_bytes =
-      (uint32_t)(((sizeof(WarpKm) + 15) & ~size_t(15)) + 2 * 3 * sizeof(double) * T);
+      (uint32_t)(((sizeof(WarpKm) + 15) & ~size_t(15)) + 4 * sizeof(double) * T);
   const size_t cta_smem = state_bytes + ((2 * sizeof(float) * Cw * (T + 1) + 15) & ~size_t(15));
   const bool use_warp = P.k <= kWK && !P.check_inv && cta_smem <= (size_t)max_optin &&
                         cols < (int64_t(1) << 30);
