@@ -808,6 +808,7 @@ __global__ void __launch_bounds__(kThreads) k_kmeans_rows(KmParams P) {
 constexpr int kWK = 16;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxG = 8;
+constexpr int kCmdDone = 0, kCmdRepair = 1, kCmdLoss = 2;  // w_lloyd's collective steps
 
 // Per-row state of one row group (one CTA of G warps works one row at a time).
 struct WarpKm {
@@ -821,6 +822,9 @@ struct WarpKm {
   Rng rng;
   int ncen;
   double closs[kWK];      // per-cluster loss under the updated centroid
+  unsigned empties;       // clusters to repair (command kCmdRepair)
+  int cmd;                // warp 0 -> the row group's other warps
+  int bailf;              // the E-step found near-duplicate centroids
   double redd[kMaxG];  // cross-warp reduction slots
   long long redl[kMaxG], redl2[kMaxG];
   int redi[kMaxG];
@@ -1020,39 +1024,52 @@ __device__ double w_distinct_value(const float* sk, int n, int64_t m) {
 
 // Cumulative-mass sampling (learner.cpp:64-75) over this thread's chunk of
 // ORIGINAL indices: first hit over the group, else the last positive index.
+// Thread t's running mass goes from excl (the group scan) up by its chunk's
+// masses (part = their sum); only a chunk whose range can hold r is walked:
+// below it (r < excl) the hit is the chunk's first positive sample, above it
+// (r beyond excl + part with a margin far wider than the walk's rounding)
+// there is none. The last positive index is only looked for when no chunk hit.
 template <int kMode>  // 0: mass = w, 1: mass = w * d2, 2: mass = d2
 __device__ __forceinline__ long long w_sample(const WRow& R, const double* d2, WarpKm& S,
-                                              const Grp& g, double excl, double r) {
-  long long cand = LLONG_MAX, lastpos = -1;
-  double acc = excl;
+                                              const Grp& g, double excl, double part, double r) {
+  long long cand = LLONG_MAX;
   const int cnt = R.hi - R.lo;
   auto mass = [&](int j) {
     if (kMode == 0) return (double)R.wv[R.idx(g.t, j)];
     if (kMode == 1) return __dmul_rn((double)R.wv[R.idx(g.t, j)], d2[j * R.T + g.t]);
     return d2[j * R.T + g.t];
   };
-  for (int j0 = 0; j0 < cnt && cand == LLONG_MAX; j0 += 8) {
-    double mv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) mv[u] = (j0 + u < cnt) ? mass(j0 + u) : 0.0;  // loads first
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (cand != LLONG_MAX || !(mv[u] > 0.0)) continue;
-      acc = __dadd_rn(acc, mv[u]);
-      lastpos = R.lo + j0 + u;
-      if (r < acc) cand = R.lo + j0 + u;
-    }
-  }
-  if (cand != LLONG_MAX) {  // lastpos = last positive index of the chunk
-    for (int j = cnt - 1; j >= 0; --j)
+  if (r < excl) {
+    for (int j = 0; j < cnt; ++j)
       if (mass(j) > 0.0) {
-        lastpos = R.lo + j;
+        cand = R.lo + j;
         break;
       }
+  } else if (!(r > __dmul_rn(__dadd_rn(excl, part), 1.0 + 0x1p-30))) {
+    double acc = excl;
+    for (int j0 = 0; j0 < cnt && cand == LLONG_MAX; j0 += 8) {
+      double mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = (j0 + u < cnt) ? mass(j0 + u) : 0.0;  // loads first
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (cand != LLONG_MAX || !(mv[u] > 0.0)) continue;
+        acc = __dadd_rn(acc, mv[u]);
+        if (r < acc) cand = R.lo + j0 + u;
+      }
+    }
   }
   long long c, lp;
-  g_minmax_ll(cand, lastpos, S, g, &c, &lp);
-  return c != LLONG_MAX ? c : (lp >= 0 ? lp : 0);
+  g_minmax_ll(cand, -1, S, g, &c, &lp);
+  if (c != LLONG_MAX) return c;
+  long long lastpos = -1;  // no hit anywhere: the last positive index of the row
+  for (int j = cnt - 1; j >= 0; --j)
+    if (mass(j) > 0.0) {
+      lastpos = R.lo + j;
+      break;
+    }
+  g_minmax_ll(LLONG_MAX, lastpos, S, g, &c, &lp);
+  return lp >= 0 ? lp : 0;
 }
 
 // k-means++ (learner.cpp:132-174): R holds the row in ORIGINAL order; D^2 in
@@ -1067,7 +1084,7 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
   }
   double u;
   double excl = g_scan_excl_draw(part, S, g, &total, &u, true);
-  long long pick = w_sample<0>(R, d2, S, g, excl, __dmul_rn(u, total));
+  long long pick = w_sample<0>(R, d2, S, g, excl, part, __dmul_rn(u, total));
   for (int j = 0; j < cnt; ++j) d2[j * R.T + g.t] = INFINITY;
   if (g.t == 0) {
     S.cen[0] = (double)R.x_at((int)pick);
@@ -1094,7 +1111,7 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
     }
     excl = g_scan_excl_draw(part, S, g, &total, &u, false);  // draws iff total > 0
     if (total > 0.0) {
-      pick = w_sample<1>(R, d2, S, g, excl, __dmul_rn(u, total));
+      pick = w_sample<1>(R, d2, S, g, excl, part, __dmul_rn(u, total));
       if (g.t == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
       __syncthreads();
       continue;
@@ -1106,7 +1123,7 @@ __device__ void w_init_kmpp(const WRow& R, const float* sk, double* d2, WarpKm& 
     }
     excl = g_scan_excl_draw(part, S, g, &total, &u, false);  // draws iff total > 0
     if (total > 0.0) {
-      pick = w_sample<2>(R, d2, S, g, excl, __dmul_rn(u, total));
+      pick = w_sample<2>(R, d2, S, g, excl, part, __dmul_rn(u, total));
       if (g.t == 0) S.cen[S.ncen++] = (double)R.x_at((int)pick);
       __syncthreads();
       continue;
@@ -1183,7 +1200,23 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
   // ---- E-step: segment boundaries of the sorted row by the exact predicate
   auto estep = [&]() -> bool {
     long long tph = clock64();
-    w_sort(S, k, g);
+    // rank the centroids (lanes < k; ties to the smaller index)
+    __syncwarp();
+    if (g.lane < k) {
+      const double v = S.cen[g.lane];
+      int r = 0;
+#pragma unroll
+      for (int p = 0; p < kWK; ++p) {
+        if (p < k) {
+          const double u = S.cen[p];
+          r += (u < v) || (u == v && p < g.lane);
+        }
+      }
+      S.rank_of[g.lane] = r;
+      S.sv[r] = v;
+      S.so[r] = g.lane;
+    }
+    __syncwarp();
     KM_PHASE(8);
     {
       double svr[kWK];
@@ -1201,8 +1234,9 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
           near_dup |= (gap > 0.0 && gap < thresh) || !(gap >= 0.0);
         }
       }
-      if (near_dup) {  // uniform: every thread sees the same centroids
-        *bail = 1;
+      if (near_dup) {  // uniform: every lane sees the same centroids
+        if (g.lane == 0) S.bailf = 1;
+        __syncwarp();
         return false;
       }
     }
@@ -1265,7 +1299,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
       S.seg[0] = 0;
       S.seg[k] = n;
     }
-    __syncthreads();
+    __syncwarp();
     KM_PHASE(4);
     return true;
   };
@@ -1353,9 +1387,95 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
     runsum(g.t, 0, hi - lo, o);
 #pragma unroll
     for (int i = 0; i < 4; ++i) CT[g.t * 4 + i] = o[i];
+    if (g.t == 0) S.bailf = 0;
     __syncthreads();
   }
-  if (!estep()) return 0.0;
+  // ---- collective steps (every warp of the row group): empty-cluster repair
+  // and the loss over repaired labels; the other warps wait for warp 0's
+  // command at named barrier 1 while warp 0 runs the iterations alone
+  auto repair_all = [&]() {
+    const unsigned empties = S.empties;
+    for (unsigned em = empties; em; em &= em - 1) {
+      const int q = __ffs(em) - 1;
+      double worst = -1.0;
+      int wp = -1;
+      long long wo_i = LLONG_MAX;
+      int r = 0;
+      for (int p = lo, j = 0; p < hi; ++p, ++j) {
+        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
+        int lab = S.so[r];
+        for (int e = 0; e < S.nexc; ++e)
+          if (S.exc_pos[e] == p) lab = S.exc_q[e];
+        const double err = __dmul_rn((double)R.wv[R.idx(g.t, j)], dcost((double)R.xs[R.idx(g.t, j)], S.cen[lab]));
+        if (err > worst) {
+          worst = err;
+          wp = p;
+          wo_i = LLONG_MAX;
+        } else if (err == worst) {
+          if (wo_i == LLONG_MAX) wo_i = svals_row[wp];
+          const long long oi = svals_row[p];
+          if (oi < wo_i) {
+            wp = p;
+            wo_i = oi;
+          }
+        }
+      }
+      if (wp >= 0 && wo_i == LLONG_MAX) wo_i = svals_row[wp];
+      // argmax (err), ties to the smallest original index: warp tree, then warps in order
+      for (int off = 16; off; off >>= 1) {
+        const double oe = __shfl_down_sync(kFull, worst, off);
+        const long long oo = __shfl_down_sync(kFull, wo_i, off);
+        const int op = __shfl_down_sync(kFull, wp, off);
+        if (g.lane + off < 32 && (oe > worst || (oe == worst && oo < wo_i))) {
+          worst = oe;
+          wo_i = oo;
+          wp = op;
+        }
+      }
+      if (g.lane == 0) {
+        S.redd[g.warp] = worst;
+        S.redl[g.warp] = wo_i;
+        S.redi[g.warp] = wp;
+      }
+      __syncthreads();
+      if (g.t == 0) {
+        double be = S.redd[0];
+        long long bo = S.redl[0];
+        int bp = S.redi[0];
+        for (int w = 1; w < g.G; ++w)
+          if (S.redd[w] > be || (S.redd[w] == be && S.redl[w] < bo)) {
+            be = S.redd[w];
+            bo = S.redl[w];
+            bp = S.redi[w];
+          }
+        S.cen[q] = (double)R.x_at(bp);
+        int e = 0;
+        while (e < S.nexc && S.exc_pos[e] != bp) ++e;
+        S.exc_pos[e] = bp;
+        S.exc_q[e] = q;
+        if (e == S.nexc) ++S.nexc;
+      }
+      __syncthreads();
+    }
+  };
+  auto signal = [&](int cmd) {
+    __syncwarp();
+    if (g.lane == 0) S.cmd = cmd;
+    __syncwarp();
+    if (g.G > 1) asm volatile("bar.sync 1, %0;" ::"r"(g.T) : "memory");
+  };
+  if (g.warp > 0) {
+    while (true) {
+      asm volatile("bar.sync 1, %0;" ::"r"(g.T) : "memory");
+      const int cmd = S.cmd;
+      if (cmd == kCmdDone) break;
+      if (cmd == kCmdRepair) repair_all();
+      else (void)g_sum(losspass(), S, g);
+    }
+  } else {
+  if (!estep()) {
+    signal(kCmdDone);
+  } else {
   double prev = INFINITY;
   for (int iter = 0; iter < P.max_iters; ++iter) {
     long long tph = clock64();
@@ -1431,73 +1551,15 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
         }
       }
       if (g.t == 0) S.nexc = 0;
-      __syncthreads();
+      __syncwarp();
     }
     KM_PHASE(5);
-    // ---- empty-cluster repair (learner.cpp:260-274), in cluster order
-    unsigned empties = 0;
-    for (int q = 0; q < k; ++q) empties |= (S.cnt[q] == 0 ? 1u : 0u) << q;
-    for (unsigned em = empties; em; em &= em - 1) {
-      const int q = __ffs(em) - 1;
-      double worst = -1.0;
-      int wp = -1;
-      long long wo_i = LLONG_MAX;
-      int r = 0;
-      for (int p = lo, j = 0; p < hi; ++p, ++j) {
-        while (r < k - 1 && S.seg[r + 1] <= p) ++r;
-        int lab = S.so[r];
-        for (int e = 0; e < S.nexc; ++e)
-          if (S.exc_pos[e] == p) lab = S.exc_q[e];
-        const double err = __dmul_rn((double)R.wv[R.idx(g.t, j)], dcost((double)R.xs[R.idx(g.t, j)], S.cen[lab]));
-        if (err > worst) {
-          worst = err;
-          wp = p;
-          wo_i = LLONG_MAX;
-        } else if (err == worst) {
-          if (wo_i == LLONG_MAX) wo_i = svals_row[wp];
-          const long long oi = svals_row[p];
-          if (oi < wo_i) {
-            wp = p;
-            wo_i = oi;
-          }
-        }
-      }
-      if (wp >= 0 && wo_i == LLONG_MAX) wo_i = svals_row[wp];
-      // argmax (err), ties to the smallest original index: warp tree, then warps in order
-      for (int off = 16; off; off >>= 1) {
-        const double oe = __shfl_down_sync(kFull, worst, off);
-        const long long oo = __shfl_down_sync(kFull, wo_i, off);
-        const int op = __shfl_down_sync(kFull, wp, off);
-        if (g.lane + off < 32 && (oe > worst || (oe == worst && oo < wo_i))) {
-          worst = oe;
-          wo_i = oo;
-          wp = op;
-        }
-      }
-      if (g.lane == 0) {
-        S.redd[g.warp] = worst;
-        S.redl[g.warp] = wo_i;
-        S.redi[g.warp] = wp;
-      }
-      __syncthreads();
-      if (g.t == 0) {
-        double be = S.redd[0];
-        long long bo = S.redl[0];
-        int bp = S.redi[0];
-        for (int w = 1; w < g.G; ++w)
-          if (S.redd[w] > be || (S.redd[w] == be && S.redl[w] < bo)) {
-            be = S.redd[w];
-            bo = S.redl[w];
-            bp = S.redi[w];
-          }
-        S.cen[q] = (double)R.x_at(bp);
-        int e = 0;
-        while (e < S.nexc && S.exc_pos[e] != bp) ++e;
-        S.exc_pos[e] = bp;
-        S.exc_q[e] = q;
-        if (e == S.nexc) ++S.nexc;
-      }
-      __syncthreads();
+    // ---- empty-cluster repair (learner.cpp:260-274), in cluster order: every warp
+    const unsigned empties = __ballot_sync(kFull, g.lane < k && S.cnt[g.lane] == 0);
+    if (empties) {
+      if (g.lane == 0) S.empties = empties;
+      signal(kCmdRepair);
+      repair_all();
     }
     KM_PHASE(6);
     // ---- changed: this iteration's E-step labels vs the previous iteration's
@@ -1562,29 +1624,33 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
         S.prank[g.lane] = S.rank_of[g.lane];
       }
     }
-    __syncthreads();
+    __syncwarp();
     KM_PHASE(10);
     // ---- loss of this iteration: per-cluster sums when nothing was repaired,
     // else a pass over the repaired labels (pseg/pso + exceptions)
     double loss_m;
     if (S.pnexc == 0) {
-      loss_m = 0.0;
-      for (int r = 0; r < k; ++r) loss_m = __dadd_rn(loss_m, S.closs[S.so[r]]);  // rank order
+      // fixed tree over the clusters (lane r holds the cluster of rank r)
+      loss_m = g.lane < k ? S.closs[S.so[g.lane]] : 0.0;
+      for (int off = 16; off; off >>= 1) loss_m = __dadd_rn(loss_m, __shfl_xor_sync(kFull, loss_m, off));
     } else {
+      signal(kCmdLoss);
       loss_m = g_sum(losspass(), S, g);
     }
     KM_PHASE(7);
-    if (g.t == 0) {
-      const bool stable = !S.chg && iter > 0;
-      const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
-      S.bci = stable || tol || loss_m == 0.0;
-    }
+    const bool stable = !S.chg && iter > 0;
+    const bool tol = isfinite(prev) && __dsub_rn(prev, loss_m) <= __dmul_rn((double)P.rel_tol, prev);
     prev = loss_m;
-    __syncthreads();
-    const int stop = S.bci;
-    __syncthreads();
-    if (stop) break;
-    if (iter + 1 < P.max_iters && !estep()) return 0.0;
+    if (stable || tol || loss_m == 0.0) break;
+    if (iter + 1 < P.max_iters && !estep()) break;
+  }
+  signal(kCmdDone);
+  }
+  }
+  __syncthreads();
+  if (S.bailf) {
+    *bail = 1;
+    return 0.0;
   }
   if (!need_loss) return 0.0;
   // final reassignment and loss (learner.cpp:305-311)
