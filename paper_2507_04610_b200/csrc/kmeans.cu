@@ -1200,21 +1200,26 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
   // ---- E-step: segment boundaries of the sorted row by the exact predicate
   auto estep = [&]() -> bool {
     long long tph = clock64();
-    // rank the centroids (lanes < k; ties to the smaller index)
+    // rank the centroids (lanes < k; ties to the smaller index) on order-
+    // preserving integer keys of the (finite) values, -0 folded onto +0 so that
+    // key equality is double equality: integer compares and shuffles instead
+    // of FP64 compares on shared-memory loads
     __syncwarp();
-    if (g.lane < k) {
-      const double v = S.cen[g.lane];
+    {
+      const double v = g.lane < k ? S.cen[g.lane] : 0.0;
+      long long key = __double_as_longlong(__dadd_rn(v, 0.0));
+      key ^= (key >> 63) & 0x7fffffffffffffffLL;
       int r = 0;
 #pragma unroll
       for (int p = 0; p < kWK; ++p) {
-        if (p < k) {
-          const double u = S.cen[p];
-          r += (u < v) || (u == v && p < g.lane);
-        }
+        const long long kp = __shfl_sync(kFull, key, p);
+        r += p < k && (kp < key || (kp == key && p < g.lane));
       }
-      S.rank_of[g.lane] = r;
-      S.sv[r] = v;
-      S.so[r] = g.lane;
+      if (g.lane < k) {
+        S.rank_of[g.lane] = r;
+        S.sv[r] = v;
+        S.so[r] = g.lane;
+      }
     }
     __syncwarp();
     KM_PHASE(8);
@@ -1251,10 +1256,12 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
         // locate it by value (chunk starts, then inside the chunk), then settle
         // it with the exact predicate
         const double mid = 0.5 * S.sv[t - 1] + 0.5 * S.sv[t];
+        // float x < mid  <=>  x < (the smallest float >= mid): float compares
+        const float midf = __double2float_ru(mid);
         int la = 0, lb = R.nch;
         while (la < lb) {
           const int m = (la + lb) >> 1;
-          if ((double)R.xs[R.idx(m, 0)] < mid) la = m + 1;
+          if (R.xs[R.idx(m, 0)] < midf) la = m + 1;
           else lb = m;
         }
         int p = 0;
@@ -1263,7 +1270,7 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
           int ja = 0, jb = cntc;
           while (ja < jb) {
             const int m = (ja + jb) >> 1;
-            if ((double)R.xs[R.idx(c0, m)] < mid) ja = m + 1;
+            if (R.xs[R.idx(c0, m)] < midf) ja = m + 1;
             else jb = m;
           }
           p = c0 * C + ja;
