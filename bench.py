@@ -294,7 +294,8 @@ def kmeans_roofline():
         return None
     return {"bound": "fp64 pipe", "frac": round(fp64, 4), "issue_active": round(issue, 4),
             "source": "profiles/ncu_kmeans.json (k_kmeans_warp, config 1): FP64 pipe busy fraction; "
-                      "the kernel is latency/barrier bound (stalls: wait, barrier)"}
+                      "the kernel is latency bound: each row's Lloyd iteration is a serial chain in one "
+                      "warp (~10K cycles) while the row group's other warps wait at a named barrier"}
 
 
 def cpu_baseline_sample():
