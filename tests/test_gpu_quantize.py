@@ -175,3 +175,19 @@ def test_config4_down_proj_with_stats(aq, ref):
     codes_a = np.concatenate([aq.unpack_codes(p.codes, 256, K, 4) for p in parts])
     codes_b = aq.unpack_codes(want.codes, 512, K, 4)
     assert np.array_equal(codes_a[same_rows], codes_b[same_rows])
+
+
+def test_near_duplicate_centroids_take_the_cta_kernel(aq, orc):
+    """Rows whose centroids end within 2^-40 of the data range of each other
+    (16 distinct values, two of them 0 and ~1e-30: k-means++ has to take the
+    tiny one last) leave the warp-per-row k-means for the CTA kernel
+    (kmeans.cu bail list); the result is still the reference's, bit for bit."""
+    rng = np.random.default_rng(17)
+    vals = np.array([0.0, 1e-30] + [float(v) for v in range(1, 15)], np.float32)
+    w = np.stack([rng.permutation(np.repeat(vals, 6)) for _ in range(8)]).astype(np.float32)
+    c = cfg(codebook=3, granularity=1, seed=3)
+    a = aq.quantize_any(w, c)
+    b = orc.quantize(w, c)
+    assert a.same_as(b), "LUT/codes differ from the oracle"
+    lut0 = np.asarray(a.luts, np.float32).reshape(w.shape[0], -1)[0]
+    assert np.unique(lut0).size == 16  # both near-duplicate centroids survive
