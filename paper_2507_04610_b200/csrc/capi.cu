@@ -156,6 +156,27 @@ StreamWs stream_ws(cudaStream_t s) {
   return w;
 }
 
+float* stream_scratch_f32(cudaStream_t s, size_t n) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<float*, size_t>> table;
+  int dev = 0;
+  ANYQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = table[{dev, s}];
+  if (e.second >= n) return e.first;
+  // grow: allocate in relaxed capture mode (the call may come while s is being
+  // captured); the previous buffer is not freed (graphs may still use it)
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  ANYQ_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+  float* p = nullptr;
+  const size_t want = std::max(n, e.second * 2);
+  const cudaError_t err = cudaMalloc(&p, want * sizeof(float));
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  ANYQ_CUDA(err);
+  e = {p, want};
+  return p;
+}
+
 // First recorded stage error of the stream (stage order = the reference's
 // check order), cleared; synchronises the stream.
 void check_stream_errors(cudaStream_t s, const char* what) {
@@ -723,7 +744,9 @@ int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
   const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
   const bool many_rows = lt->RB >= 2 * lt->sms;
   try {
-    if (m >= 2 && m <= 16 && (many_rows || (m >= 3 && m <= 4)) && lutgemv_tc_fits(lt, m))
+    // K1t only when one x image fits: its K-sliced form (a grid-wide wait per
+    // slice) measured slower than the fallbacks below (gate m = 9: 65 vs 31 us)
+    if (m >= 2 && m <= 16 && (many_rows || (m >= 3 && m <= 4)) && lutgemv_tc_slices(lt, m) == 1)
       return ANYQ_PATH_GEMV_TC;
     if (lutgemv_fits(lt, m)) return ANYQ_PATH_GEMV;
   } catch (...) {

@@ -54,6 +54,9 @@ struct StreamWs {
   int* err;
 };
 StreamWs stream_ws(cudaStream_t s);
+// Per-(device, stream) fp32 scratch of at least n floats (grow-only; a grown
+// buffer keeps the old one alive, so graphs captured earlier stay valid).
+float* stream_scratch_f32(cudaStream_t s, size_t n);
 // Synchronises s; raises the first recorded stage error (and clears the words).
 void check_stream_errors(cudaStream_t s, const char* what);
 

@@ -115,6 +115,12 @@ struct GvProb {
   int newimg;            // first problem of its image
   int tma;               // x rows staged by cp.async.bulk into the image region
   int rboff;             // first item of this problem in the chain's item sequence
+  // K1t K-slices of one GEMM (lutgemv_tc_run when the whole x image does not
+  // fit): chunks [c0, c0 + C) of the tensor; codes/ab/x point at chunk c0
+  int cstride;           // chunks per row block in the code layout (the tensor's C)
+  int xstride;           // elements between x rows (the tensor's K)
+  const float* acc_in;   // y32 partial of the previous slice (added first), or null
+  float* acc_out;        // this slice's partial (y32 of the running sum), or null: final slice
 };
 
 struct GvParams {
@@ -725,6 +731,11 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
 //  * Producer, writer, item schedule, dependencies, pair table and its
 //    buffers are those of K1a; alpha/beta come through their own ring so
 //    the code ring is released as soon as the dequant warps read it.
+//  * A single GEMM whose x image does not fit (m x K too large) runs as up to
+//    8 K-slices in one launch: slice s is a problem over chunks [c0, c0 + nc)
+//    (codes, scales and x offset, row strides of the whole tensor) that waits
+//    for slice s - 1 and adds its fp32 partial (the caller's y32, else stream
+//    scratch) before its own: deterministic. Image rows m >= M are zero.
 // ===========================================================================
 // debug trace of K1t: [ncta][8 events][64 chunk groups] behind K1a's [ncta][64]
 #ifdef TC_TRACE_ON  // experiment builds only: the stamps perturb the pipeline
@@ -837,13 +848,14 @@ template <int MP>
 __device__ __forceinline__ void prep_x_tc(const GvProb& q, int M, uint8_t* smem, int idx, int lane) {
   const int sub = lane & 7;
   const int m = idx / q.C, c = idx - m * q.C;
-  const bool live = idx < M * q.C;
+  const bool live = idx < M * q.C;   // a real x row: load it
+  const bool img = idx < MP * q.C;   // an image row (rows m >= M are written as zeros)
   const int k0 = c * 128 + sub * 16;
   float v[16];
 #pragma unroll
   for (int t = 0; t < 16; ++t) v[t] = 0.0f;
   if (live) {
-    const __nv_bfloat16* xr = q.x + (size_t)m * q.K;
+    const __nv_bfloat16* xr = q.x + (size_t)m * q.xstride;
     if (q.tma && k0 + 16 <= q.K) {  // 16-B aligned rows (K % 128 == 0, x 16-B aligned)
       const uint4 r0 = __ldcg(reinterpret_cast<const uint4*>(xr + k0));
       const uint4 r1 = __ldcg(reinterpret_cast<const uint4*>(xr + k0 + 8));
@@ -881,7 +893,7 @@ __device__ __forceinline__ void prep_x_tc(const GvProb& q, int M, uint8_t* smem,
     const __half2 p2 = __floats2half2_rn(v[2 * t] * sc, v[2 * t + 1] * sc);
     h[t] = *reinterpret_cast<const uint32_t*>(&p2);
   }
-  if (live) {
+  if (img) {
     // k = 16 sub + t: MMA step 2 sub (sub < 4) or 2 (sub - 4) + 1, row n = q' MP + m
     const int st = sub < 4 ? 2 * sub : 2 * (sub - 4) + 1;
     const int n = (c & 3) * MP + m;
@@ -911,6 +923,8 @@ __device__ __forceinline__ void writer_loop_tc(const GvParams& P, const float* r
       __syncwarp();
       staged = q.img;
     }
+    // K-slices: every lane acquires the earlier slices' partials it adds
+    if (it.p == p && q.acc_in) asm volatile("fence.acq_rel.gpu;" ::: "memory");
     while (it.p == p) {
       const int par = g & 1;
       mbar_wait_sleep(bar_full + 8 * par, (uint32_t)((g >> 1) & 1));
@@ -928,8 +942,16 @@ __device__ __forceinline__ void writer_loop_tc(const GvParams& P, const float* r
 #pragma unroll
         for (int m = 0; m < MP; ++m) {
           if (m < P.M) {
-            q.y[(size_t)m * q.N + row] = __float2bfloat16_rn(acc[m]);
-            if (q.y32) q.y32[(size_t)m * q.N + row] = acc[m];
+            const size_t o = (size_t)m * q.N + row;
+            // K-slices: the earlier slices' sum first (written by the problem this
+            // one waits for), then this slice's
+            if (q.acc_in) acc[m] = __fadd_rn(__ldcg(q.acc_in + o), acc[m]);
+            if (q.acc_out) {
+              q.acc_out[o] = acc[m];
+            } else {
+              q.y[o] = __float2bfloat16_rn(acc[m]);
+              if (q.y32) q.y32[o] = acc[m];
+            }
           }
         }
       }
@@ -971,7 +993,7 @@ __device__ __forceinline__ void producer_loop_tc(const GvParams& P, uint32_t bar
 #ifndef TC_NOPREFETCH
     if (x.p >= P.np) return;
     const GvProb& q = P.p[x.p];
-    const uint8_t* c = reinterpret_cast<const uint8_t*>(q.codes) + (size_t)x.rb * q.C * 2048;
+    const uint8_t* c = reinterpret_cast<const uint8_t*>(q.codes) + (size_t)x.rb * q.cstride * 2048;
     for (uint32_t o = 0, n = (uint32_t)q.C * 2048; o < n; o += 32768) prefetch_l2(c + o, min(32768u, n - o));
     prefetch_l2(reinterpret_cast<const uint8_t*>(q.ab) + (size_t)x.rb * q.GR * 128, (uint32_t)q.GR * 128);
 #endif
@@ -997,7 +1019,7 @@ __device__ __forceinline__ void producer_loop_tc(const GvParams& P, uint32_t bar
       }
       const int c0 = 4 * gi, n = min(4, q.C - c0);
       const int g0 = c0 >> q.gshift, g1 = (c0 + n - 1) >> q.gshift;
-      src[ng] = reinterpret_cast<const uint8_t*>(q.codes) + ((size_t)it.rb * q.C + c0) * 2048;
+      src[ng] = reinterpret_cast<const uint8_t*>(q.codes) + ((size_t)it.rb * q.cstride + c0) * 2048;
       nb[ng] = (uint32_t)n * 2048;
       asrc[ng] = reinterpret_cast<const uint8_t*>(q.ab) + ((size_t)it.rb * q.GR + g0) * 128;
       anb[ng] = (uint32_t)(g1 - g0 + 1) * 128;
@@ -1247,7 +1269,7 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
       if (q.img != cur_img) {  // convert the new x image (x may be an earlier problem's y)
         mbar_wait_sleep(bars + kTbX, (uint32_t)(xbatch & 1));
         ++xbatch;
-        for (int i0 = warp * 4; i0 < P.M * q.C; i0 += kTcDq * 4)
+        for (int i0 = warp * 4; i0 < MP * q.C; i0 += kTcDq * 4)  // padding rows m >= M as zeros
           prep_x_tc<MP>(q, P.M, smem, i0 + (lane >> 3), lane);
         // generic-proxy writes of the image -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1328,9 +1350,16 @@ long long* g_gv_trace = nullptr;
 // Per-problem parameters, batches and shared-memory placement; returns the
 // dynamic shared memory bytes. TC: the K1t layout (x images in the UMMA
 // layout, 4 quarter partials, the alpha/beta ring).
+struct KSlice {   // one K-slice of a sliced single GEMM (K1t)
+  int c0, nc;      // chunks [c0, c0 + nc)
+  const float* acc_in;
+  float* acc_out;
+};
+
 template <int MP, bool TC = false>
 uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
-                    float* const* y32s, const int32_t* deps, int64_t m, GvParams& P) {
+                    float* const* y32s, const int32_t* deps, int64_t m, GvParams& P,
+                    const KSlice* slices = nullptr) {
   if (n < 1 || n > kMaxProb) fail(ANYQ_ERR_SHAPE, "LUT GEMV chain: 1..8 problems");
   P.np = n;
   P.M = (int)m;
@@ -1363,10 +1392,24 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
     q.GR = t->GR;
     q.RB = t->RB;
     q.gshift = t->gv_gshift;
+    q.cstride = t->C;
+    q.xstride = (int)t->cols;
+    q.acc_in = nullptr;
+    q.acc_out = nullptr;
+    if (slices) {
+      const KSlice& sl = slices[i];
+      q.codes += (size_t)sl.c0 * 128;  // 2048-B chunks of uint4
+      if (t->GR > 1) q.ab += (size_t)(sl.c0 >> q.gshift) * 32;
+      q.x += (size_t)sl.c0 * 128;
+      q.K = std::min((int)t->cols - sl.c0 * 128, sl.nc * 128);
+      q.C = sl.nc;
+      q.acc_in = sl.acc_in;
+      q.acc_out = sl.acc_out;
+    }
     q.dep = deps ? deps[i] : -1;
     if (q.dep < -1 || q.dep >= i) fail(ANYQ_ERR_SHAPE, "chain dependency must name an earlier problem");
     // raw x rows are staged in place of their image: needs K = 128 * C
-    q.tma = (q.K % 128 == 0) && ((reinterpret_cast<uintptr_t>(xs[i]) & 15) == 0);
+    q.tma = (q.K % 128 == 0) && ((reinterpret_cast<uintptr_t>(q.x) & 15) == 0);
     // a problem shares the previous problem's x image when it reads the same x
     // after the same dependency
     q.newimg = !(i > 0 && P.p[i - 1].x == q.x && P.p[i - 1].K == q.K && P.p[i - 1].dep == q.dep);
@@ -1442,9 +1485,10 @@ uint32_t plan_chain(int n, const LutTensor* const* ts, const void* const* xs, vo
 
 template <int MP, bool TC = false>
 void launch_gv(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
-               float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s) {
+               float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s,
+               const KSlice* slices = nullptr) {
   GvParams P;
-  const uint32_t smem_bytes = plan_chain<MP, TC>(n, ts, xs, ys, y32s, deps, m, P);
+  const uint32_t smem_bytes = plan_chain<MP, TC>(n, ts, xs, ys, y32s, deps, m, P, slices);
   // release counters of this stream: launches on one stream are ordered and
   // leave them at zero; launches on other streams use their own
   const StreamWs ws = stream_ws(s);
@@ -1603,30 +1647,83 @@ void lutgemv_chain_run_auto(int n, const LutTensor* const* ts, const void* const
   lutgemv_chain_run(n, ts, xs, ys, y32s, deps, m, s);
 }
 
+// K-slices of one K1t GEMM whose x image does not fit: the fewest slices (of
+// whole chunk groups and whole scale groups, at most kMaxProb) whose plan
+// fits, run as a chain in which slice s waits for slice s - 1 and adds its
+// fp32 partial to the running sum (fixed order: deterministic). Returns the
+// slice count (0: none fits); sl[] gets the chunk ranges.
+int tc_slices(const LutTensor* t, int64_t m, KSlice* sl) {
+  const int unit = t->GR > 1 ? std::max(4, 1 << std::min(t->gv_gshift, 20)) : 4;
+  const LutTensor* ts[kMaxProb];
+  const void* xs[kMaxProb];
+  void* ys[kMaxProb];
+  int32_t deps[kMaxProb];
+  for (int S = 1; S <= kMaxProb; ++S) {
+    const int nc = (((t->C + S - 1) / S) + unit - 1) / unit * unit;
+    const int ns = (t->C + nc - 1) / nc;
+    if (ns != S && S > 1) continue;  // rounding to whole groups made it another count
+    for (int i = 0; i < ns; ++i) {
+      sl[i] = KSlice{i * nc, std::min(nc, t->C - i * nc), nullptr, nullptr};
+      ts[i] = t;
+      xs[i] = nullptr;
+      ys[i] = nullptr;
+      deps[i] = i - 1;
+    }
+    GvParams P;
+    try {
+      tc_dispatch(m, [&](auto mp) {
+        return plan_chain<decltype(mp)::value, true>(ns, ts, xs, ys, nullptr, deps, m, P, sl);
+      });
+      return ns;
+    } catch (const Failure&) {
+    }
+  }
+  return 0;
+}
+
 bool lutgemv_tc_fits(const LutTensor* t, int64_t m) {
   if (!t || m < 1 || m > kTcMaxMP || t->gv_gshift < 0 || !gv_sbase_ok()) return false;
-  const LutTensor* ts[1] = {t};
-  const void* xs[1] = {nullptr};
-  void* ys[1] = {nullptr};
-  GvParams P;
-  try {
-    tc_dispatch(m, [&](auto mp) {
-      return plan_chain<decltype(mp)::value, true>(1, ts, xs, ys, nullptr, nullptr, m, P);
-    });
-  } catch (const Failure&) {
-    return false;
-  }
-  return true;
+  KSlice sl[kMaxProb];
+  return tc_slices(t, m, sl) > 0;
+}
+
+int lutgemv_tc_slices(const LutTensor* t, int64_t m) {
+  if (!t || m < 1 || m > kTcMaxMP || t->gv_gshift < 0 || !gv_sbase_ok()) return 0;
+  KSlice sl[kMaxProb];
+  return tc_slices(t, m, sl);
 }
 
 void lutgemv_tc_run(const LutTensor* t, const void* x, int64_t m, void* y, float* y32,
                     cudaStream_t s) {
   if (!t) fail(ANYQ_ERR_SHAPE, "null device tensor");
-  const LutTensor* ts[1] = {t};
-  const void* xs[1] = {x};
-  void* ys[1] = {y};
-  float* y32s[1] = {y32};
-  lutgemv_tc_chain_run(1, ts, xs, ys, y32s, nullptr, m, s);
+  if (m < 1 || m > kTcMaxMP) fail(ANYQ_ERR_SHAPE, "tcgen05 LUT GEMV supports 1 <= m <= 16");
+  if (t->gv_gshift < 0) fail(ANYQ_ERR_CONFIG, "LUT GEMV needs rowwise scales or group_size = 128 * 2^j");
+  if (!gv_sbase_ok())
+    fail(ANYQ_ERR_CONFIG, "LUT GEMV: dynamic shared memory does not start at 0x400 on this device");
+  KSlice sl[kMaxProb];
+  const int ns = tc_slices(t, m, sl);
+  if (ns == 0) fail(ANYQ_ERR_SHAPE, "tcgen05 LUT GEMV: the x image does not fit in 8 K-slices");
+  const LutTensor* ts[kMaxProb];
+  const void* xs[kMaxProb];
+  void* ys[kMaxProb];
+  float* y32s[kMaxProb];
+  int32_t deps[kMaxProb];
+  // the running sum lives in y32 when the caller wants it, else in stream scratch
+  float* acc = ns > 1 ? (y32 ? y32 : stream_scratch_f32(s, (size_t)m * t->rows)) : nullptr;
+  for (int i = 0; i < ns; ++i) {
+    ts[i] = t;
+    xs[i] = x;
+    ys[i] = y;
+    y32s[i] = y32;
+    deps[i] = i - 1;
+    sl[i].acc_in = i > 0 ? acc : nullptr;
+    sl[i].acc_out = i + 1 < ns ? acc : nullptr;
+  }
+  tc_dispatch(m, [&](auto mp) {
+    constexpr int MP = decltype(mp)::value;
+    launch_gv<MP, true>(ns, ts, xs, ys, y32s, ns > 1 ? deps : nullptr, m, s, sl);
+    return 0;
+  });
 }
 
 // ---------------------------------------------------------------------------

@@ -52,7 +52,9 @@ void lutgemv_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16
 // K1t: the same chain with the products on tcgen05 (m <= 16; gemv.cu).
 void lutgemv_tc_chain_run(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                           float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
-bool lutgemv_tc_fits(const LutTensor* t, int64_t m);
+bool lutgemv_tc_fits(const LutTensor* t, int64_t m);  // with up to 8 K-slices
+// K-slices a single K1t GEMM at m x rows needs (1: whole; 0: does not fit)
+int lutgemv_tc_slices(const LutTensor* t, int64_t m);
 void lutgemv_chain_run_auto(int n, const LutTensor* const* ts, const void* const* xs, void* const* ys,
                             float* const* y32s, const int32_t* deps, int64_t m, cudaStream_t s);
 void lutgemv_tc_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,

@@ -39,8 +39,8 @@ def test_formats_and_m(aq, orc, cuda, fmt, m):
                                    (96, 1280, 1280), (33, 128, 128), (151 * 32 - 5, 512, 128),
                                    (70, 200, 128), (300, 1000, 128)])
 def test_shapes(aq, orc, cuda, m, n, k, g):
-    if m * k > 4 * 4096:
-        pytest.skip("x image beyond shared memory (split-K not built yet)")
+    """m * k beyond one x image in shared memory (M = 16 at K = 4096) runs as
+    K-slices chained through the fp32 running sum."""
     w = orc.gaussian(n, k, 41)
     gran = 1 if g == k else 3
     c = cfg(codebook=3, granularity=gran, group_size=g, seed=1, max_iters=8)
@@ -146,3 +146,33 @@ def test_chain_edge_cases(aq, orc, cuda):
             assert torch.equal(r, y32[i]), (m, i)
     for d in base + [dts[7]]:
         d.close()
+
+
+@pytest.mark.parametrize("m,k,g", [(3, 14336, 128), (4, 14336, 128), (8, 14336, 512), (16, 4096, 256),
+                                   (12, 6144, 128)])
+def test_k_slices(aq, orc, cuda, m, k, g):
+    """x images beyond shared memory: the GEMM runs as up to 8 K-slices (whole
+    chunk groups and scale groups) in one launch, slice s waiting for s - 1 and
+    adding to its fp32 partial; with and without a caller y32 (the running sum
+    then lives in stream scratch); deterministic."""
+    import torch
+
+    n = 300
+    w = orc.gaussian(n, k, 51)
+    qt = aq.quantize_any(w, cfg(codebook=3, granularity=3, group_size=g, seed=1, max_iters=3))
+    dt = aq.DeviceTensor(qt)
+    x = bf16(orc.gaussian(m, k, 52))
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16).contiguous()
+    y = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    y32 = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    dt.gemm(xt, y, y32, path=TC)
+    y2 = torch.empty_like(y)
+    dt.gemm(xt, y2, None, path=TC)
+    y3 = torch.empty_like(y)
+    dt.gemm(xt, y3, None, path=TC)
+    torch.cuda.synchronize()
+    ref = orc.gemm_reference(x, orc.narrowed(qt))
+    tol = tc_tolerance(orc, x, qt)
+    assert np.all(np.abs(y32.cpu().numpy() - ref) <= tol)
+    assert torch.equal(y, y2) and torch.equal(y2, y3)
+    dt.close()
