@@ -1,7 +1,11 @@
-"""profiles/round1.md from the round's bench line (gpurun_out/bench.log), the
-reference arm (gpurun_out/bench_ref.log) and profiles/ncu_summary.json."""
+"""profiles/roundN.md from the round's bench line, the reference arm and
+profiles/ncu_summary.json.
+
+usage: python scripts/make_round_report.py [N [bench.log [bench_ref.log]]]
+(defaults: 1, gpurun_out/bench.log, gpurun_out/bench_ref.log)"""
 import json
 import os
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -16,11 +20,12 @@ def last_json(path):
 
 
 def main():
-    b = last_json(os.path.join(ROOT, "gpurun_out", "bench.log"))
-    r = last_json(os.path.join(ROOT, "gpurun_out", "bench_ref.log"))
+    rnd = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    b = last_json(sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "bench.log"))
+    r = last_json(sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "bench_ref.log"))
     n = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-    L = ["# Round 1 — measured on one B200 (sm_100a, 148 SMs)", ""]
-    L += ["Source: `python bench.py` (defaults: N=1, 50 steps, 5 warm-up, CUDA graphs, weights rotated "
+    L = [f"# Round {rnd} — measured on one B200 (sm_100a, 148 SMs)", ""]
+    L += ["Source: `python bench.py` (defaults: N=1, 200 steps, 5 warm-up, CUDA graphs, weights rotated "
           "over 4 layers > L2) and `python bench.py --impl reference`; ncu: "
           "`ncu --set full --clock-control none` of `scripts/prof_chain.py` (cold L2, serialised).", ""]
     L += ["## Headline (decoder-layer chain, M=1)", "", "| key | value |", "|---|---|"]
@@ -61,7 +66,7 @@ def main():
             L.append(f"| {k} | {v['value']} {v['unit']} |")
         L += ["", "Stalls per issued instruction: " +
               ", ".join(f"{k} {v}" for k, v in sorted(kn["stalls_per_issue"].items(), key=lambda kv: -kv[1])[:8])]
-    with open(os.path.join(ROOT, "profiles", "round1.md"), "w") as f:
+    with open(os.path.join(ROOT, "profiles", f"round{rnd}.md"), "w") as f:
         f.write("\n".join(L) + "\n")
 
 
