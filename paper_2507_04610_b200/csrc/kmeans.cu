@@ -1003,6 +1003,45 @@ __device__ __forceinline__ void w_load_row(const WRow& R, const Grp& g, F&& put)
   }
 }
 
+// Whole-row load xs[.] = xa[p], wv[.] = wa[perm ? perm[p] : p] in batches of
+// 8 per thread: all global loads of a batch (the permutation first, then the
+// gathers) are issued before any shared-memory store. One load-store pair at
+// a time serialised 2 x 32 global round trips per thread and row.
+__device__ __forceinline__ void w_load_row_batched(const WRow& R, const Grp& g, float* xs, float* wv,
+                                                   const float* __restrict__ xa,
+                                                   const float* __restrict__ wa,
+                                                   const int* __restrict__ perm) {
+  constexpr int B = 8;
+  int t = g.t / R.C, j = g.t - (g.t / R.C) * R.C;
+  for (int p0 = g.t; p0 < R.n; p0 += B * R.T) {
+    int si[B], wi[B];
+    float xv[B], wq[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      si[u] = R.idx(t, j);
+      j += R.T;
+      while (j >= R.C) {
+        j -= R.C;
+        ++t;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int p = p0 + u * R.T;
+      wi[u] = p < R.n ? (perm ? __ldg(perm + p) : p) : 0;
+      xv[u] = p < R.n ? __ldg(xa + p) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) wq[u] = p0 + u * R.T < R.n ? __ldg(wa + wi[u]) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (p0 + u * R.T < R.n) {
+        xs[si[u]] = xv[u];
+        wv[si[u]] = wq[u];
+      }
+  }
+}
+
 // label of sorted position p under segments seg/so
 __device__ __forceinline__ int w_label_seg(const int* seg, const int* so, int k, int p) {
   int r = 0;
@@ -1722,10 +1761,7 @@ __global__ void __launch_bounds__(256, MINB) k_kmeans_warp(WkParams P) {
       const long long t0 = clock64();
       if (P.init == ANYQ_INIT_KMPP || P.init == ANYQ_INIT_RANDOM) {
         // seeding works on the row in ORIGINAL order
-        w_load_row(R, g, [&](int p, int si) {
-          xs[si] = xo[p];
-          wv[si] = wo[p];
-        });
+        w_load_row_batched(R, g, xs, wv, xo, wo, nullptr);
         __syncthreads();
         if (P.init == ANYQ_INIT_KMPP) w_init_kmpp(R, sk_row, d2, S, k, g);
         else w_init_random(R, sk_row, S, k, g);
@@ -1742,10 +1778,7 @@ __global__ void __launch_bounds__(256, MINB) k_kmeans_warp(WkParams P) {
       }
       __syncthreads();
       // Lloyd works on the sorted row
-      w_load_row(R, g, [&](int p, int si) {
-        xs[si] = sk_row[p];
-        wv[si] = wo[sv_row[p]];
-      });
+      w_load_row_batched(R, g, xs, wv, sk_row, wo, sv_row);
       __syncthreads();
       const long long t1 = clock64();
       const double loss = w_lloyd(P, R, S, CT, sv_row, g, P.restarts > 1, &bail);
@@ -1767,9 +1800,16 @@ __global__ void __launch_bounds__(256, MINB) k_kmeans_warp(WkParams P) {
     if (g.t < k) S.cen[g.t] = S.best_cen[g.t];
     w_sort(S, k, g);
     if (g.t < k) P.luts[(size_t)row * k + g.t] = (float)S.sv[g.t];
-    for (int p = R.lo, j = 0; p < R.hi; ++p, ++j) {
-      const int q = w_nearest((double)xs[R.idx(g.t, j)], S, k);
-      P.codes[(size_t)row * n + sv_row[p]] = (uint8_t)S.rank_of[q];
+    for (int p0 = R.lo; p0 < R.hi; p0 += 8) {  // original positions loaded 8 at a time, then stores
+      int ov[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ov[u] = p0 + u < R.hi ? __ldg(sv_row + p0 + u) : 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (p0 + u >= R.hi) break;
+        const int q = w_nearest((double)xs[R.idx(g.t, p0 + u - R.lo)], S, k);
+        P.codes[(size_t)row * n + ov[u]] = (uint8_t)S.rank_of[q];
+      }
     }
   }
 }
