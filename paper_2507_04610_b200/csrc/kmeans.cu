@@ -809,6 +809,11 @@ constexpr int kWK = 16;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxG = 8;
 constexpr int kCmdDone = 0, kCmdRepair = 1, kCmdLoss = 2;  // w_lloyd's collective steps
+// named barrier 1 over the row group: warp 0's command hand-off and the other
+// warps' wait meet at this one instruction (one call site for both sides)
+__device__ __noinline__ void km_bar1(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 
 // Per-row state of one row group (one CTA of G warps works one row at a time).
 struct WarpKm {
@@ -1508,11 +1513,11 @@ __device__ double w_lloyd(const WkParams& P, const WRow& R, WarpKm& S, double* C
     __syncwarp();
     if (g.lane == 0) S.cmd = cmd;
     __syncwarp();
-    if (g.G > 1) asm volatile("bar.sync 1, %0;" ::"r"(g.T) : "memory");
+    if (g.G > 1) km_bar1(g.T);
   };
   if (g.warp > 0) {
     while (true) {
-      asm volatile("bar.sync 1, %0;" ::"r"(g.T) : "memory");
+      km_bar1(g.T);
       const int cmd = S.cmd;
       if (cmd == kCmdDone) break;
       if (cmd == kCmdRepair) repair_all();
