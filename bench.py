@@ -435,8 +435,9 @@ def gpu_arm(args):
                 run_layer(i % len(layers), stream)
         torch.cuda.synchronize()
 
-    # let the clocks ramp, then the untimed warm-up steps
-    t_end = time.time() + 0.3
+    # let the clocks ramp (1 s: a fresh box measured one 15 %-slow run after 0.3 s), then the
+    # untimed warm-up steps
+    t_end = time.time() + 1.0
     while time.time() < t_end:
         with torch.cuda.stream(stream):
             for i in range(len(layers)):
