@@ -323,10 +323,11 @@ def cpu_baseline_sample():
 # (the GEMMs of a Llama decoder layer with the non-GEMM ops between them elided)
 X_SRC = [-1, -1, -1, 0, 3, 3, 5]
 WAITS = [0, 0, 0, 1, 1, 0, 1]
-# the single-launch chain runs the layer in its natural order; each problem waits
-# only for the problem its x comes from (anyq_dev_gemm_chain_deps). (Scheduling
-# o before k/v and up before gate measured no faster: scripts/gemv_probe.py.)
-CHAIN_ORDER = [0, 1, 2, 3, 4, 5, 6]
+# the single-launch chain: each problem waits only for the problem its x comes
+# from (anyq_dev_gemm_chain_deps); o is dealt before k/v and up before gate, so
+# the CTAs that finish q early take o while the others still run k/v (measured
+# 0.3-0.5 us per layer faster than the natural order: scripts/gemv_probe.py --chain)
+CHAIN_ORDER = [0, 3, 1, 2, 5, 4, 6]
 CHAIN_DEPS = [-1 if X_SRC[j] < 0 else CHAIN_ORDER.index(X_SRC[j]) for j in CHAIN_ORDER]
 BATCHES = [[0, 1, 2], [3], [4, 5], [6]]
 

@@ -29,7 +29,8 @@ LAYER_8B = [(4096, 4096), (1024, 4096), (1024, 4096), (4096, 4096), (14336, 4096
             (4096, 14336)]
 LAYER_70B = [(8192, 8192), (1024, 8192), (1024, 8192), (8192, 8192), (28672, 8192), (28672, 8192),
              (8192, 28672)]
-DEPS = [-1, -1, -1, 0, 3, 3, 5]  # bench.py CHAIN_DEPS
+DEPS = [-1, -1, -1, 0, 3, 3, 5]  # the layer in its natural order
+ORDER_SCHED = [0, 3, 1, 2, 5, 4, 6]  # bench.py CHAIN_ORDER (o before k/v, up before gate)
 
 
 def synthetic_qt(n, k, seed):
@@ -77,7 +78,7 @@ def check_rows(orc, qt, x, y32, rows, what):
         assert np.all(err <= tol), (what, r0, float(np.max(err / tol)))
 
 
-def run_chain(aq, torch, qts, m, seed, path=None):
+def run_chain(aq, torch, qts, m, seed, path=None, order=None):
     dts = [aq.DeviceTensor(q) for q in qts]
     x0 = torch.from_numpy(np.random.default_rng(seed).standard_normal((m, qts[0].cols),
                                                                        dtype=np.float32))
@@ -85,7 +86,10 @@ def run_chain(aq, torch, qts, m, seed, path=None):
     ys = [torch.empty(m, q.rows, device="cuda", dtype=torch.bfloat16) for q in qts]
     y32 = [torch.empty(m, q.rows, device="cuda", dtype=torch.float32) for q in qts]
     xs = [x0 if d < 0 else ys[d] for d in DEPS]
-    aq.gemm_chain(dts, xs, ys, y32s=y32, deps=DEPS, path=path)
+    order = order or list(range(len(qts)))
+    deps = [-1 if DEPS[j] < 0 else order.index(DEPS[j]) for j in order]
+    aq.gemm_chain([dts[j] for j in order], [xs[j] for j in order], [ys[j] for j in order],
+                  y32s=[y32[j] for j in order], deps=deps, path=path)
     torch.cuda.synchronize()
     out = [(xs[i].float().cpu().numpy(), y32[i].cpu().numpy()) for i in range(len(qts))]
     for d in dts:
@@ -98,10 +102,11 @@ def sample_rows(n):
     return sorted({0, max(0, (n // 2) // 32 * 32), max(0, n - 2048)})
 
 
+@pytest.mark.parametrize("order", [None, ORDER_SCHED], ids=["natural", "bench"])
 @pytest.mark.parametrize("m", [1, 2])
-def test_llama3_8b_layer_chain(aq, orc, cuda, m):
+def test_llama3_8b_layer_chain(aq, orc, cuda, m, order):
     qts = [synthetic_qt(n, k, 100 + i) for i, (n, k) in enumerate(LAYER_8B)]
-    for i, (x, y) in enumerate(run_chain(aq, cuda, qts, m, 7 + m)):
+    for i, (x, y) in enumerate(run_chain(aq, cuda, qts, m, 7 + m, order=order)):
         check_rows(orc, qts[i], x, y, range(0, qts[i].rows, 2048), f"8b chain m={m} problem {i}")
 
 
