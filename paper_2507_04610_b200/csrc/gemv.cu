@@ -764,7 +764,7 @@ constexpr int kTcWriter = 21;
 constexpr int kTcProducer = 22;
 constexpr int kTcBuilder = 23;            // builds every item's pair table, one item ahead
 constexpr int kTcT = 24 * 32;
-constexpr int kTcNA = 4;                  // A slots (one chunk group = 64 TMEM columns each)
+constexpr int kTcNA = 8;                  // A-slot barriers (one chunk group = 64 TMEM columns each)
 constexpr int kTcND = 4;                  // accumulator slots
 constexpr int kTcAbRing = 4;              // alpha/beta ring stages (2 KB each)
 constexpr int kTcTmemCols = 512;
@@ -1122,7 +1122,12 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t kDCol0 = kTcNA * 64;
+  // A slots: as many 64-column slots as TMEM leaves next to the 4 accumulator
+  // slots (MP 2/4: 7, MP 8: 6, MP 16: 4), round-robin over the CTA's groups, so
+  // a team starts its next group while the MMA still reads its previous one
+  constexpr int NA = (512 - kTcND * NB) / 64 > 7 ? 7 : (512 - kTcND * NB) / 64;
+  static_assert(NA >= 4 && NA <= kTcNA, "A slots");
+  constexpr uint32_t kDCol0 = NA * 64;
   float* red = reinterpret_cast<float*>(smem + P.red);
 
   if (warp == kTcProducer) {
@@ -1166,8 +1171,8 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
       const int ngrp = (q.C + 3) >> 2;
       const uint32_t xb = sbase + q.xh;
       for (int gi = 0; gi < ngrp; ++gi, ++cg) {
-        const int a = cg % kTcNA, d = cg % kTcND;
-        mbar_wait(bars + kTbAFull + 8 * a, (uint32_t)((cg / kTcNA) & 1));
+        const int a = cg % NA, d = cg % kTcND;
+        mbar_wait(bars + kTbAFull + 8 * a, (uint32_t)((cg / NA) & 1));
         if (lane == 0) TC_TRACE(4, cg);
         if (cg >= kTcND) mbar_wait(bars + kTbDFree + 8 * d, (uint32_t)(((cg / kTcND) - 1) & 1));
         if (need_x) {
@@ -1268,7 +1273,7 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
     // (k in {16j..16j+15, 64+16j..}) into A columns 16j..16j+15 of TMEM lane
     // quarter q. Every warp still builds its slice of every item's table.
     const int qq = warp & 3, team = warp >> 2;
-    const uint32_t tq = tmem + ((uint32_t)(32 * qq) << 16) + (uint32_t)team * 64;
+    const uint32_t tq0 = tmem + ((uint32_t)(32 * qq) << 16);
     const uint32_t tready = bars + kTbTReady, tfree = bars + kTbTFree;
     Item s = item_begin(P, b);
     int xbatch = 0, cur_img = -1, g = 0, base = 0, slot = 0, k = 0;
@@ -1293,6 +1298,9 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
         const uint32_t tb = kTblAddr | ((uint32_t)(g & 1) << 7) | laneoff;
         mbar_wait(tready + 8 * (g & 1), (uint32_t)((g >> 1) & 1));
         for (; gi < ngrp; gi += 4, ++k) {
+          const int cga = team + 4 * k;  // this group's CTA-wide index
+          const int as = cga % NA;
+          const uint32_t tq = tq0 + (uint32_t)as * 64;
           mbar_wait(bars + kTbSFull + 8 * slot, round & 1);
           const bool live = 4 * gi + qq < q.C;
           if (live) {
@@ -1302,7 +1310,7 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
             for (int jj = 0; jj < 4; ++jj) w[jj] = lds128(ra + jj * 512);
             __syncwarp();
             if (lane == 0) mbar_arrive(bars + kTbSEmpty + 8 * slot);  // codes are in registers
-            if (k > 0) mbar_wait(bars + kTbAFree + 8 * team, (uint32_t)((k - 1) & 1));
+            if (cga >= NA) mbar_wait(bars + kTbAFree + 8 * as, (uint32_t)(((cga / NA) - 1) & 1));
             tc_fence_after();
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
@@ -1327,11 +1335,11 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
           } else {
             __syncwarp();
             if (lane == 0) mbar_arrive(bars + kTbSEmpty + 8 * slot);
-            if (k > 0) mbar_wait(bars + kTbAFree + 8 * team, (uint32_t)((k - 1) & 1));
+            if (cga >= NA) mbar_wait(bars + kTbAFree + 8 * as, (uint32_t)(((cga / NA) - 1) & 1));
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bars + kTbAFull + 8 * team);
+          if (lane == 0) mbar_arrive(bars + kTbAFull + 8 * as);
           if (++slot == P.nring) {
             slot = 0;
             ++round;
