@@ -765,7 +765,7 @@ constexpr int kTcProducer = 22;
 constexpr int kTcBuilder = 23;            // builds every item's pair table, one item ahead
 constexpr int kTcT = 24 * 32;
 constexpr int kTcNA = 8;                  // A-slot barriers (one chunk group = 64 TMEM columns each)
-constexpr int kTcND = 4;                  // accumulator slots
+constexpr int kTcND = 8;                  // accumulator-slot barriers
 constexpr int kTcAbRing = 4;              // alpha/beta ring stages (2 KB each)
 constexpr int kTcTmemCols = 512;
 constexpr int kTcMaxMP = 16;
@@ -1122,10 +1122,13 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // A slots: as many 64-column slots as TMEM leaves next to the 4 accumulator
-  // slots (MP 2/4: 7, MP 8: 6, MP 16: 4), round-robin over the CTA's groups, so
-  // a team starts its next group while the MMA still reads its previous one
-  constexpr int NA = (512 - kTcND * NB) / 64 > 7 ? 7 : (512 - kTcND * NB) / 64;
+  // A slots: as many 64-column slots as TMEM leaves next to the accumulator
+  // slots (MP 2: 7, MP 4: 6, MP 8: 6, MP 16: 4), round-robin over the CTA's
+  // groups, so a team starts its next group while the MMA still reads its last
+  // accumulator slots: 8 where they are narrow (MP <= 4: the MMA runs further
+  // ahead of the epilogue, 1-2 % faster), else 4
+  constexpr int ND = NB <= 16 ? 8 : 4;
+  constexpr int NA = (512 - ND * NB) / 64 > 7 ? 7 : (512 - ND * NB) / 64;
   static_assert(NA >= 4 && NA <= kTcNA, "A slots");
   constexpr uint32_t kDCol0 = NA * 64;
   float* red = reinterpret_cast<float*>(smem + P.red);
@@ -1171,10 +1174,10 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
       const int ngrp = (q.C + 3) >> 2;
       const uint32_t xb = sbase + q.xh;
       for (int gi = 0; gi < ngrp; ++gi, ++cg) {
-        const int a = cg % NA, d = cg % kTcND;
+        const int a = cg % NA, d = cg % ND;
         mbar_wait(bars + kTbAFull + 8 * a, (uint32_t)((cg / NA) & 1));
         if (lane == 0) TC_TRACE(4, cg);
-        if (cg >= kTcND) mbar_wait(bars + kTbDFree + 8 * d, (uint32_t)(((cg / kTcND) - 1) & 1));
+        if (cg >= ND) mbar_wait(bars + kTbDFree + 8 * d, (uint32_t)(((cg / ND) - 1) & 1));
         if (need_x) {
           mbar_wait(bars + kTbXReady, (uint32_t)(xr & 1));
           ++xr;
@@ -1219,8 +1222,8 @@ __global__ void __launch_bounds__(kTcT, 1) k_lutgemv_tc(const __grid_constant__ 
       for (int gi = 0; gi < ngrp; ++gi, ++cg) {
         const int c0 = 4 * gi;
         if ((cg & 3) == 0) mbar_wait(bars + kTbAbFull + 8 * aslot, around & 1);
-        const int d = cg % kTcND;
-        mbar_wait(bars + kTbDFull + 8 * d, (uint32_t)((cg / kTcND) & 1));
+        const int d = cg % ND;
+        mbar_wait(bars + kTbDFull + 8 * d, (uint32_t)((cg / ND) & 1));
         if (qq == 0 && lane == 0) TC_TRACE(6, cg);
         tc_fence_after();
         float r[MP];
