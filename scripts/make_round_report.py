@@ -25,7 +25,7 @@ def main():
     r = last_json(sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "bench_ref.log"))
     n = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
     L = [f"# Round {rnd} — measured on one B200 (sm_100a, 148 SMs)", ""]
-    L += ["Source: `python bench.py` (defaults: N=1, 200 steps, 5 warm-up, CUDA graphs, weights rotated "
+    L += ["Source: `python bench.py` (defaults: N=1, 500 steps, 5 warm-up, CUDA graphs, weights rotated "
           "over 4 layers > L2) and `python bench.py --impl reference`; ncu: "
           "`ncu --set full --clock-control none` of `scripts/prof_chain.py` (cold L2, serialised).", ""]
     L += ["## Headline (decoder-layer chain, M=1)", "", "| key | value |", "|---|---|"]
