@@ -738,7 +738,7 @@ int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
   // measured crossovers on B200 (profiles/round2_k1t.md): the CUDA-core GEMV
   // at m = 1 (and m = 2 for fewer than 2 row blocks per SM); K1t (tcgen05
   // GEMV) for 3 <= m <= 4, and up to m = 16 with at least 2 row blocks per
-  // SM, while its shared-memory plan fits; K2 for 17 <= m <= 128 on tall
+  // SM, while its shared-memory plan fits; K2 for 16 <= m <= 128 on tall
   // tensors; the fused dequant-to-shared-memory mma.sync kernel up to m = 32
   // (it splits K over every SM, which wins on small N); dequant + cuBLAS above
   const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
@@ -752,9 +752,10 @@ int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
   } catch (...) {
   }
   if (m <= 4) return ANYQ_PATH_TC;
-  // K2 (tcgen05, bf16 dequantisation in shared memory) for 17 <= m <= 128 on
-  // tensors with >= 2 row blocks per SM (its tiles are 128 rows)
-  if (m >= 17 && m <= 128 && many_rows && lutgemm_k2_supports(lt, m)) return ANYQ_PATH_K2;
+  // K2 (tcgen05, bf16 dequantisation in shared memory) for 16 <= m <= 128 on
+  // tensors with >= 2 row blocks per SM (its tiles are 128 rows; at m = 16 on
+  // gate 31.8 us against the fused mma kernel's 33.4 us)
+  if (m >= 16 && m <= 128 && many_rows && lutgemm_k2_supports(lt, m)) return ANYQ_PATH_K2;
   if (m <= 32 && lutmma_supports(lt, m)) return ANYQ_PATH_MMA;
   return m <= 8 ? ANYQ_PATH_TC : ANYQ_PATH_DEQUANT;
 }
