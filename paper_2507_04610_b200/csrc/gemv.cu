@@ -101,14 +101,17 @@ constexpr uint32_t kBarTReady = 40;    // [2] pair-table buffer written (kW)
 constexpr uint32_t kBarTFree = 56;     // [2] pair-table buffer no longer read (kW)
 constexpr uint32_t kBarLFull = 72;     // [2] LUT rows of an item landed (producer + tx)
 constexpr uint32_t kBarLFree = 88;     // [2] LUT rows consumed (kW)
-constexpr uint32_t kBarSFull = 104;    // [kMaxRing] code stage landed (producer + tx)
-constexpr uint32_t kBarSEmpty = kBarSFull + 8 * kMaxRing;  // [kMaxRing] stage consumed (kW)
-// compute warps 0-7 and 8-15 consume two independent half rings (each 32-KB
-// stage buffer holds both halves' 8 chunks; barriers per half): a lagging half
-// no longer holds back the other half's refills (gate 14.1 -> 13.85 us)
-constexpr uint32_t kBarSFullB = kBarSEmpty + 8 * kMaxRing;   // [kMaxRing] half B landed
-constexpr uint32_t kBarSEmptyB = kBarSFullB + 8 * kMaxRing;  // [kMaxRing] half B consumed
-constexpr uint32_t kBarBytes = kBarSEmptyB + 8 * kMaxRing;
+#ifndef GV_RING_PARTS
+#define GV_RING_PARTS 2
+#endif
+constexpr int kRingParts = GV_RING_PARTS;           // independent part rings of a stage
+constexpr int kPartChunks = kStageChunks / kRingParts;  // chunks (= compute warps) per part
+constexpr uint32_t kBarSFull = 104;    // [kRingParts][kMaxRing] part of a stage landed (producer + tx)
+constexpr uint32_t kBarSEmpty = kBarSFull + 8 * kRingParts * kMaxRing;  // [..] part consumed
+// compute warps consume kRingParts independent part rings (each 32-KB stage
+// buffer holds every part's chunks; barriers per part): a lagging part no
+// longer holds back the other parts' refills (2 parts: gate 14.1 -> 13.85 us)
+constexpr uint32_t kBarBytes = kBarSEmpty + 8 * kRingParts * kMaxRing;
 
 struct GvProb {
   const uint4* codes;    // [RB][C][4][32] uint4
@@ -526,8 +529,8 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
 __device__ __forceinline__ void producer_loop(const GvParams& P, uint32_t bars, uint32_t sbase,
                                               int b, int half) {
   const uint32_t lfull = bars + kBarLFull, lfree = bars + kBarLFree;
-  const uint32_t sfull = bars + (half == 1 ? kBarSFullB : kBarSFull);
-  const uint32_t sempty = bars + (half == 1 ? kBarSEmptyB : kBarSEmpty);
+  const uint32_t sfull = bars + kBarSFull + 8u * kMaxRing * half;
+  const uint32_t sempty = bars + kBarSEmpty + 8u * kMaxRing * half;
   const uint32_t abring = sbase + P.abring, lutbuf = sbase + P.lutbuf;
   Item it = item_begin(P, b);
   int g = 0, slot = 0;
@@ -545,9 +548,9 @@ __device__ __forceinline__ void producer_loop(const GvParams& P, uint32_t bars, 
     const uint8_t* ag = reinterpret_cast<const uint8_t*>(q.ab) + (size_t)it.rb * q.GR * 128;
     for (int cs = 0; cs < q.C; cs += kStageChunks) {
       // this half's 8 chunks of the stage (possibly none: the slot still turns)
-      const int c0 = cs + 8 * half;
-      const int n = max(0, min(8, q.C - c0));
-      const uint32_t hoff = (uint32_t)half * 8u * 2048u, aoff = (uint32_t)half * (kStageAb / 2);
+      const int c0 = cs + kPartChunks * half;
+      const int n = max(0, min(kPartChunks, q.C - c0));
+      const uint32_t hoff = (uint32_t)half * kPartChunks * 2048u, aoff = (uint32_t)half * (kStageAb / kRingParts);
       if (n == 0) {
         if (round > 0) mbar_wait(sempty + 8 * slot, (round - 1) & 1);
         mbar_arrive(sfull + 8 * slot);
@@ -612,17 +615,17 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
     }
     mbar_init(bars + kBarX, 1);
     for (int j = 0; j < kMaxRing; ++j) {
-      mbar_init(bars + kBarSFull + 8 * j, 1);
-      mbar_init(bars + kBarSEmpty + 8 * j, kW / 2);
-      mbar_init(bars + kBarSFullB + 8 * j, 1);
-      mbar_init(bars + kBarSEmptyB + 8 * j, kW / 2);
+      for (int h = 0; h < kRingParts; ++h) {
+        mbar_init(bars + kBarSFull + 8 * (h * kMaxRing + j), 1);
+        mbar_init(bars + kBarSEmpty + 8 * (h * kMaxRing + j), kW / kRingParts);
+      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   float* red = reinterpret_cast<float*>(smem + P.red);
   if (warp == kProducerWarp) {
-    if (lane < 2) producer_loop(P, bars, sbase, b, lane);  // lane h feeds half ring h
+    if (lane < kRingParts) producer_loop(P, bars, sbase, b, lane);  // lane h feeds part ring h
     return;
   }
   if (warp == kWriterWarp) {
@@ -656,9 +659,9 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
 
   // ---- compute warps: shared memory only ------------------------------------
   const uint32_t tready = bars + kBarTReady, tfree = bars + kBarTFree;
-  const int half = warp >> 3;  // half ring
-  const uint32_t sfull = bars + (half ? kBarSFullB : kBarSFull), sempty = bars + (half ? kBarSEmptyB : kBarSEmpty);
-  const uint32_t abring = sbase + P.abring + laneoff + (uint32_t)half * (kStageAb / 2);
+  const int half = warp / kPartChunks;  // part ring
+  const uint32_t sfull = bars + kBarSFull + 8u * kMaxRing * half, sempty = bars + kBarSEmpty + 8u * kMaxRing * half;
+  const uint32_t abring = sbase + P.abring + laneoff + (uint32_t)half * (kStageAb / kRingParts);
   const uint32_t bar_full = bars + kBarRedFull, bar_empty = bars + kBarRedEmpty;
   const uint32_t ring = sbase + (uint32_t)warp * 2048 + lane * 16;
   Item s = item_begin(P, b);
@@ -703,7 +706,7 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
 #pragma unroll
         for (int j = 0; j < 4; ++j) ch.w[j] = lds128(a + j * 512);
         ch.ab = lds32(abring + slot * kStageAb +
-                      (uint32_t)(((c >> q.gshift) - ((c0 + 8 * half) >> q.gshift)) << 7));
+                      (uint32_t)(((c >> q.gshift) - ((c0 + kPartChunks * half) >> q.gshift)) << 7));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(sempty + 8 * slot);  // release orders the reads above
