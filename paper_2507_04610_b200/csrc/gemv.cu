@@ -457,17 +457,23 @@ __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red,
   for (int p = 0; p < P.np; ++p) {
     const GvProb& q = P.p[p];
     if (it.p == p && q.img != staged) {  // this CTA needs image q.img next
-      if (lane == 0) {
-        if (q.dep >= 0) {
-          GV_TRACE_W(16 + p);
-          wait_geq(&P.done[q.dep], P.ncta);
-          GV_TRACE_W(24 + p);
+      // a hand-off only for the CTA's first image (earlier kernels' memory,
+      // after griddepcontrol.wait) and for images that are another problem's y;
+      // an input x needs none, so the compute warps do not wait for this warp
+      // to catch up with their items (compute warps apply the same rule)
+      if (q.dep >= 0 || staged < 0) {
+        if (lane == 0) {
+          if (q.dep >= 0) {
+            GV_TRACE_W(16 + p);
+            wait_geq(&P.done[q.dep], P.ncta);
+            GV_TRACE_W(24 + p);
+          }
+          // the compute warps read x straight from global (measured faster than
+          // staging the rows by cp.async.bulk first: chain -0.8 %, q -2.4 %)
+          mbar_arrive(bar_x);
         }
-        // the compute warps read x straight from global (measured faster than
-        // staging the rows by cp.async.bulk first: chain -0.8 %, q -2.4 %)
-        mbar_arrive(bar_x);
+        __syncwarp();
       }
-      __syncwarp();
       staged = q.img;
     }
     while (it.p == p) {
@@ -679,8 +685,10 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
     const int p = s.p;
     const GvProb& q = P.p[p];
     if (q.img != cur_img) {  // first item on a new x image: load and convert it
-      mbar_wait(bars + kBarX, (uint32_t)(xbatch & 1));
-      ++xbatch;
+      if (q.dep >= 0 || cur_img < 0) {  // the writer's hand-off (see writer_loop)
+        mbar_wait(bars + kBarX, (uint32_t)(xbatch & 1));
+        ++xbatch;
+      }
       // each warp converts exactly the chunks it reads (c = warp + 16 i, lane
       // group i % 4 per pass): the image needs no CTA barrier
       const int nmine = (q.C - warp + kW - 1) / kW;  // chunks of this warp
