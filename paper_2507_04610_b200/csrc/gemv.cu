@@ -15,8 +15,9 @@
 // fp32, so the result differs from the fp32 reference only by summation order
 // (tolerance 1e-5 * sum|x*w|, tests/test_gpu_gemm.py).
 //
-// One persistent CTA per SM: 16 compute warps, 1 writer warp, 1 producer warp,
-// 1 builder warp (each item's pair table, one item ahead).
+// One persistent CTA per SM: 16 compute warps, 1 writer warp, 1 producer warp
+// (two lanes, one per half ring), 1 builder warp (each item's pair table, one
+// item ahead), 1 dependency warp (the x hand-offs).
 //  * Work items are whole 32-row blocks. A launch runs a chain of up to 8
 //    GEMMs; problem i may depend on one earlier problem dep[i] (its x is that
 //    problem's y). The chain's row blocks, concatenated in problem order, are
@@ -48,11 +49,11 @@
 //    the image; images alternate between two banks.
 //  * The writer warp reduces the 16 warp partials of an item in a fixed order,
 //    stores y, and after its items of a problem releases that problem
-//    grid-wide (done[p], in problem order). It also releases x to the compute
-//    warps (bar_x): for a dependent problem it first waits until every CTA
-//    released the problem x comes from, while the weights already stream in.
-//    The grid is co-resident (cooperative launch) and dependencies point
-//    backwards, so the waits cannot deadlock.
+//    grid-wide (done[p], in problem order). A dependency warp releases x to
+//    the compute warps (bar_x): for a dependent problem it first waits until
+//    every CTA released the problem x comes from, while the weights already
+//    stream in. The grid is co-resident (cooperative launch) and dependencies
+//    point backwards, so the waits cannot deadlock.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -72,7 +73,8 @@ constexpr int kW = 16;                // compute warps per CTA (one table slice 
 constexpr int kWriterWarp = kW;
 constexpr int kProducerWarp = kW + 1;
 constexpr int kBuilderWarp = kW + 2;  // every item's pair table, one item ahead
-constexpr int kT = (kW + 3) * 32;
+constexpr int kDepWarp = kW + 3;      // the x hand-offs (dependency waits), off the writer
+constexpr int kT = (kW + 4) * 32;
 constexpr int kMaxMP = 4;  // MP in {1, 2, 3, 4}: one template instance per x-row count
 constexpr int kStageChunks = kW;      // chunks per ring stage: one per compute warp
 constexpr uint32_t kStageBytes = kStageChunks * 2048u;
@@ -440,42 +442,18 @@ __device__ __forceinline__ void prep_x(const GvProb& q, int M, uint8_t* smem, in
   }
 }
 
-// Writer warp, per problem in order: releases the problem's x to the compute
-// warps when this CTA has items of it and the image is new to this CTA (first
-// waiting until every CTA released the problem x comes from: x may be an
-// earlier y), reduces
-// the kW warp partials of each item in a fixed order and stores y, then
-// releases the problem grid-wide (done[p]; in order, so done[p] == ncta
-// implies every earlier problem is complete too).
+// Writer warp, per problem in order: reduces the kW warp partials of each
+// item in a fixed order and stores y, then releases the problem grid-wide
+// (done[p]; in order, so done[p] == ncta implies every earlier problem is
+// complete too). The x hand-offs are the dependency warp's.
 template <int MP>
 __device__ __forceinline__ void writer_loop(const GvParams& P, const float* red, uint32_t bars,
                                             uint32_t sbase, int b, int lane) {
   const uint32_t bar_full = bars + kBarRedFull, bar_empty = bars + kBarRedEmpty;
-  const uint32_t bar_x = bars + kBarX;
   Item it = item_begin(P, b);
-  int g = 0, staged = -1;
+  int g = 0;
   for (int p = 0; p < P.np; ++p) {
     const GvProb& q = P.p[p];
-    if (it.p == p && q.img != staged) {  // this CTA needs image q.img next
-      // a hand-off only for the CTA's first image (earlier kernels' memory,
-      // after griddepcontrol.wait) and for images that are another problem's y;
-      // an input x needs none, so the compute warps do not wait for this warp
-      // to catch up with their items (compute warps apply the same rule)
-      if (q.dep >= 0 || staged < 0) {
-        if (lane == 0) {
-          if (q.dep >= 0) {
-            GV_TRACE_W(16 + p);
-            wait_geq(&P.done[q.dep], P.ncta);
-            GV_TRACE_W(24 + p);
-          }
-          // the compute warps read x straight from global (measured faster than
-          // staging the rows by cp.async.bulk first: chain -0.8 %, q -2.4 %)
-          mbar_arrive(bar_x);
-        }
-        __syncwarp();
-      }
-      staged = q.img;
-    }
     while (it.p == p) {
       const int par = g & 1;
       mbar_wait_sleep(bar_full + 8 * par, (uint32_t)((g >> 1) & 1));
@@ -643,6 +621,32 @@ __global__ void __launch_bounds__(kT, 1) k_lutgemv(const __grid_constant__ GvPar
   // released item g - 2's (tfree) and the LUT rows landed; the compute warps no
   // longer build slices between items, so they never wait for each other there
   // (chain 51.6 -> 50.2 us, gate 15.0 -> 14.7 us)
+  // Dependency warp: the compute warps' x hand-offs (bar_x), one per image that
+  // needs one — the CTA's first image (earlier kernels' memory, after
+  // griddepcontrol.wait) and every image that is another problem's y (after
+  // every CTA released that problem); an input x needs none, the compute warps
+  // apply the same rule. In its own warp the wait no longer queues behind the
+  // writer's last items (8B chain 47.0 -> 42.9 us).
+  if (warp == kDepWarp) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    Item it = item_begin(P, b);
+    int staged = -1;
+    for (int p = 0; p < P.np; ++p) {
+      const GvProb& q = P.p[p];
+      if (it.p == p && q.img != staged) {
+        if (q.dep >= 0 || staged < 0) {
+          if (lane == 0) {
+            if (q.dep >= 0) wait_geq(&P.done[q.dep], P.ncta);
+            mbar_arrive(bars + kBarX);
+          }
+          __syncwarp();
+        }
+        staged = q.img;
+      }
+      while (it.p == p) item_next(P, b, it);
+    }
+    return;
+  }
   if (warp == kBuilderWarp) {
     const uint32_t lutrow = sbase + P.lutbuf + (uint32_t)lane * 32;
     Item it = item_begin(P, b);
