@@ -94,7 +94,8 @@ class ClockSampler:
     }
 
     def __init__(self, dev_index=0, period=0.0002):
-        self.samples, self.reasons = [], set()
+        self.samples, self.reasons, self.timed = [], set(), []
+        self.t_start, self.t_end = None, None
         self.max_mhz = None
         self.period = period
         self._stop = threading.Event()
@@ -111,14 +112,21 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
+                self.timed.append((time.perf_counter(), mhz, r))
             except Exception:
                 pass
             time.sleep(self.period)
+
+    def wait_running(self, n=3, timeout=2.0):
+        """Block until the sampler has taken n samples (its first NVML calls are slow)."""
+        t_end = time.time() + timeout
+        while self.nv is not None and len(self.timed) < n and time.time() < t_end:
+            time.sleep(0.001)
+
+    def mark(self, which):
+        setattr(self, "t_" + which, time.perf_counter())
 
     def __enter__(self):
         if self.nv is not None:
@@ -132,6 +140,15 @@ class ClockSampler:
             self.t.join()
 
     def summary(self):
+        # the samples taken while the timed region ran (host marks around it)
+        lo = self.t_start if self.t_start is not None else -1e30
+        hi = self.t_end if self.t_end is not None else 1e30
+        for t, mhz, r in self.timed:
+            if lo <= t <= hi:
+                self.samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
@@ -455,6 +472,8 @@ def gpu_arm(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.wait_running()  # sampling before the region starts: its samples cover all of it
+        clk.mark("start")
         with torch.cuda.stream(stream):
             ev0.record(stream)
             if steps_graph is not None:
@@ -464,6 +483,7 @@ def gpu_arm(args):
                     step(i)
             ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("end")
     ms = ev0.elapsed_time(ev1) / args.steps
     if P > 1:
         t = torch.tensor([ms], device=dev)
