@@ -61,7 +61,7 @@ def main():
                  sorted(share.items(), key=lambda kv: -kv[1])}
     summary = {
         "round": 2,
-        "kernel": "k_lutgemv<1> chain (one Llama-3-8B decoder layer, 7 GEMMs, M=1): 16 compute + writer + producer + builder warps",
+        "kernel": "k_lutgemv<1> chain (one Llama-3-8B decoder layer, 7 GEMMs, M=1): 16 compute + writer + producer + builder + dependency warps",
         "capture": f"ncu --set full --clock-control none (cold L2, serialised) of scripts/prof_chain.py -> {os.path.basename(rep)}",
         "dram_bytes_per_launch_layer_chain": rd + wr,
         "algorithmic_bytes_per_launch": 117383168,
