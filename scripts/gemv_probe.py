@@ -134,6 +134,12 @@ def main():
             # natural order (q,k,v,o,gate,up,down) and the scheduled order of bench.py
             orders = {"": ([0, 1, 2, 3, 4, 5, 6], [-1, -1, -1, 0, 3, 3, 5]),
                       "_sched": ([0, 3, 1, 2, 5, 4, 6], [-1, 0, -1, -1, 1, 1, 4])}
+            # extra orders to try: CHAIN_ORDERS="0,3,5,4,6,1,2;..." (indices of q,k,v,o,gate,up,down)
+            x_src = [-1, -1, -1, 0, 3, 3, 5]
+            for spec in filter(None, os.environ.get("CHAIN_ORDERS", "").split(";")):
+                order = [int(v) for v in spec.split(",")]
+                orders["_" + "".join(map(str, order))] = (
+                    order, [-1 if x_src[j] < 0 else order.index(x_src[j]) for j in order])
             for tag, (order, deps) in orders.items():
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
