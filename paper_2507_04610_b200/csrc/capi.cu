@@ -142,16 +142,17 @@ StreamWs stream_ws(cudaStream_t s) {
   // during a global-mode capture) and zero on a private stream.
   cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
   ANYQ_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
-  cudaError_t e = cudaMalloc(&block, sizeof(int) * (kWsDone + kWsErr));
+  cudaError_t e = cudaMalloc(&block, sizeof(int) * (kWsDone + kWsErr + kWsK2));
   cudaStream_t z = nullptr;
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMemsetAsync(block, 0, sizeof(int) * (kWsDone + kWsErr), z);
+  if (e == cudaSuccess) e = cudaMemsetAsync(block, 0, sizeof(int) * (kWsDone + kWsErr + kWsK2), z);
   if (e == cudaSuccess) e = cudaStreamSynchronize(z);
   if (z) cudaStreamDestroy(z);
   cudaThreadExchangeStreamCaptureMode(&mode);
   ANYQ_CUDA(e);
   w.done = block;
   w.err = block + kWsDone;
+  w.k2flags = block + kWsDone + kWsErr;
   table.emplace(std::make_pair(dev, s), w);
   return w;
 }
@@ -754,8 +755,11 @@ int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
   if (m <= 4) return ANYQ_PATH_TC;
   // K2 (tcgen05, bf16 dequantisation in shared memory) for 16 <= m <= 128 on
   // tensors with >= 2 row blocks per SM (its tiles are 128 rows; at m = 16 on
-  // gate 31.8 us against the fused mma kernel's 33.4 us)
-  if (m >= 16 && m <= 128 && many_rows && lutgemm_k2_supports(lt, m)) return ANYQ_PATH_K2;
+  // gate 29.7 us against the fused mma kernel's 32.5 us), and on long-K
+  // tensors with few row tiles, split stream-K over every SM with >= 8 steps
+  // per CTA (down, m = 32 / 64: 32.9 / 38.9 us against 43.2 / 57.1 us)
+  if (m >= 16 && m <= 128 && (many_rows || lutgemm_k2_long_k(lt, m)) && lutgemm_k2_supports(lt, m))
+    return ANYQ_PATH_K2;
   if (m <= 32 && lutmma_supports(lt, m)) return ANYQ_PATH_MMA;
   return m <= 8 ? ANYQ_PATH_TC : ANYQ_PATH_DEQUANT;
 }

@@ -47,11 +47,14 @@ void ensure_dyn_smem(const void* kernel, int bytes);
 // stage error words of the stream-ordered entries.
 constexpr int kWsDone = 8;  // GEMV chain release counters (one per problem)
 constexpr int kWsErr = 8;   // stage error words, checked in index order
+constexpr int kK2FlagStride = 32;  // one K2 stream-K counter per 128-B line
+constexpr int kWsK2 = 256 * kK2FlagStride;  // K2 stream-K partial-ready counters (one per CTA, self-resetting)
 constexpr int kErrFinite = 0, kErrStats = 1, kErrRows = 2, kErrLearn = 3, kErrPack = 4,
               kErrGemv = 5;
 struct StreamWs {
   int* done;
   int* err;
+  int* k2flags;
 };
 StreamWs stream_ws(cudaStream_t s);
 // Per-(device, stream) fp32 scratch of at least n floats (grow-only; a grown

@@ -65,6 +65,7 @@ void lutmma_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16,
                 cudaStream_t s);
 // K2, large M: dequantise to bf16 in shared memory -> tcgen05 (lutgemm2.cu).
 bool lutgemm_k2_supports(const LutTensor* t, int64_t m);
+bool lutgemm_k2_long_k(const LutTensor* t, int64_t m);  // AUTO: K2 split stream-K pays (few row tiles, long K)
 void lutgemm_k2_run(const LutTensor* t, const void* x_bf16, int64_t m, void* y_bf16, float* y_f32,
                     cudaStream_t s);
 // Large M: bf16 dequantization in row slices + cuBLAS GEMM (dequant_gemm.cu).

@@ -88,7 +88,47 @@ struct K2Params {
   float* y32;
   int64_t M, N;
   int RB, C, GR, gshift, rtiles, ttiles;
+  // stream-K (one token tile): CTA b takes the steps [b U / G, (b+1) U / G)
+  // of the U = tiles x steps units; a tile split over CTAs is finished by the
+  // CTA holding its step 0, which adds the later CTAs' fp32 partials in k order
+  int sk;
+  float* part;            // [G][NT][128] partial tiles (stream-K)
+  int* flags;             // [G][kK2FlagStride] partial-ready flags of the 4 epilogue warps (self-resetting)
 };
+
+// A segment: steps [s0, s1) of one tile.
+struct Seg {
+  int tile, s0, s1;
+};
+struct SegIt {
+  int u, uend;  // stream-K units
+  int t;        // round-robin tile
+};
+__device__ __forceinline__ int sk_begin(long long U, int b, int G) { return (int)(U * b / G); }
+__device__ __forceinline__ SegIt seg_begin(const K2Params& P, int S, int ntiles) {
+  SegIt it;
+  const long long U = (long long)ntiles * S;
+  it.u = sk_begin(U, blockIdx.x, gridDim.x);
+  it.uend = sk_begin(U, blockIdx.x + 1, gridDim.x);
+  it.t = blockIdx.x;
+  return it;
+}
+__device__ __forceinline__ bool seg_next(const K2Params& P, int S, int ntiles, SegIt& it, Seg& sg) {
+  if (P.sk) {
+    if (it.u >= it.uend) return false;
+    sg.tile = it.u / S;
+    sg.s0 = it.u - sg.tile * S;
+    sg.s1 = min(S, sg.s0 + (it.uend - it.u));
+    it.u += sg.s1 - sg.s0;
+    return true;
+  }
+  if (it.t >= ntiles) return false;
+  sg.tile = it.t;
+  sg.s0 = 0;
+  sg.s1 = S;
+  it.t += gridDim.x;
+  return true;
+}
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
@@ -209,9 +249,11 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
       int st = 0;
       uint32_t round = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tt = tile % P.ttiles;
-        for (int sp = 0; sp < S; ++sp) {
+      SegIt it = seg_begin(P, S, ntiles);
+      Seg sg;
+      while (seg_next(P, S, ntiles, it, sg)) {
+        const int tt = sg.tile % P.ttiles;
+        for (int sp = sg.s0; sp < sg.s1; ++sp) {
           const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
           if (round > 0) mbar_wait(bars + kQXEmpty + 8 * st, (round - 1) & 1);
           const uint32_t full = bars + kQXFull + 8 * st;
@@ -233,10 +275,12 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     if (lane == 0) {
       int st = 0;
       uint32_t round = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int rt = tile / P.ttiles;
+      SegIt it = seg_begin(P, S, ntiles);
+      Seg sg;
+      while (seg_next(P, S, ntiles, it, sg)) {
+        const int rt = sg.tile / P.ttiles;
         const int nrb = min(4, P.RB - 4 * rt);
-        for (int sp = 0; sp < S; ++sp) {
+        for (int sp = sg.s0; sp < sg.s1; ++sp) {
           const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
           const int g0 = c0 >> P.gshift, ng = ((c0 + nc - 1) >> P.gshift) - g0 + 1;
           if (round > 0) mbar_wait(bars + kQCEmpty + 8 * st, (round - 1) & 1);
@@ -260,11 +304,13 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     // ------------------------------------------------------------ MMA issue
     int xs = 0, as = 0, tl = 0;
     uint32_t xround = 0, around = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
+    SegIt it = seg_begin(P, S, ntiles);
+    Seg sg;
+    for (; seg_next(P, S, ntiles, it, sg); ++tl) {
       const int db = tl & 1;
       if (tl >= 2) mbar_wait(bars + kQDEmpty + 8 * db, (uint32_t)(((tl >> 1) - 1) & 1));
       const uint32_t d = tmem + (uint32_t)db * NT;
-      for (int sp = 0; sp < S; ++sp) {
+      for (int sp = sg.s0; sp < sg.s1; ++sp) {
         const int nc = min(kK2Cps, C - sp * kK2Cps);
         mbar_wait(bars + kQXFull + 8 * xs, xround & 1);
         mbar_wait(bars + kQAFull + 8 * as, around & 1);
@@ -278,12 +324,12 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
 #pragma unroll
               for (int s = 0; s < 8; ++s)
                 tc_mma_ts(d, a + h * 64 + s * 8, desc_b(b + (2 * h + (s >> 2)) * CF::kBox + (s & 3) * 32),
-                          CF::kIdesc, (sp > 0 || h > 0 || s > 0) ? 1u : 0u);
+                          CF::kIdesc, (sp > sg.s0 || h > 0 || s > 0) ? 1u : 0u);
             }
           }
           tc_commit(bars + kQXEmpty + 8 * xs);
           tc_commit(bars + kQAEmpty + 8 * as);
-          if (sp == S - 1) tc_commit(bars + kQDFull + 8 * db);
+          if (sp == sg.s1 - 1) tc_commit(bars + kQDFull + 8 * db);
         }
         __syncwarp();
         if (++xs == XS) {
@@ -300,17 +346,60 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
     int tl = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tl) {
-      const int rt = tile / P.ttiles, tt = tile - rt * P.ttiles;
+    const long long U = (long long)ntiles * S;
+    const int b = blockIdx.x, G = gridDim.x;
+    SegIt it = seg_begin(P, S, ntiles);
+    Seg sg;
+    for (; seg_next(P, S, ntiles, it, sg); ++tl) {
+      const int rt = sg.tile / P.ttiles, tt = sg.tile - rt * P.ttiles;
       const int db = tl & 1;
+      // stream-K: a segment past the tile's step 0 leaves an fp32 partial; the
+      // segment holding step 0 (and not the last step) adds the partials of the
+      // CTAs b+1.. whose ranges start inside the tile, in k order
+      const bool partial = sg.s0 > 0;
+      const bool finish = sg.s0 == 0 && sg.s1 < S;
+      int cend = b + 1;
+      if (finish) {
+        const int tend = (sg.tile + 1) * S;
+        while (cend < G && sk_begin(U, cend, G) < tend) ++cend;
+        // partial rows 32q.. of CTA c are epilogue warp q's: one flag per (c, q)
+        if (lane == 0)
+          for (int c = b + 1; c < cend; ++c) {
+            int v;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];"
+                           : "=r"(v)
+                           : "l"(P.flags + kK2FlagStride * c + q)
+                           : "memory");
+              if (!v) __nanosleep(32);
+            } while (!v);
+          }
+        __syncwarp();
+      }
       mbar_wait(bars + kQDFull + 8 * db, (uint32_t)((tl >> 1) & 1));
       tc_fence_after();
       const int64_t row = (int64_t)rt * 128 + 32 * q + lane;
       const int64_t t0 = (int64_t)tt * NT;
       for (int c0 = 0; c0 < NT; c0 += 32) {
+        if (t0 + c0 >= P.M) break;  // no token of this column block (warp-uniform)
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)db * NT + c0, r);
-        if (row < P.N) {
+        // partials move whole 32-column blocks, unpredicated (a load under a
+        // per-column branch would wait one round trip per column); columns past
+        // M are never stored
+        if (partial) {
+          float* pp = P.part + ((size_t)b * NT + c0) * 128 + 32 * q + lane;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcg(pp + j * 128, __uint_as_float(r[j]));
+        } else if (row < P.N) {
+          for (int c = b + 1; c < cend; ++c) {
+            const float* pp = P.part + ((size_t)c * NT + c0) * 128 + 32 * q + lane;
+            float pv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) pv[j] = __ldcg(pp + j * 128);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + pv[j]);
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t m = t0 + c0 + j;
@@ -324,7 +413,15 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bars + kQDEmpty + 8 * db);
+      if (lane == 0) {
+        mbar_arrive(bars + kQDEmpty + 8 * db);
+        if (partial) {  // this warp's rows of the partial are out (release)
+          __threadfence();
+          asm volatile("st.relaxed.gpu.global.s32 [%0], 1;" ::"l"(P.flags + kK2FlagStride * b + q) : "memory");
+        }
+        for (int c = b + 1; c < cend; ++c)  // consumed: reset for the next launch (kernel-ordered)
+          asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(P.flags + kK2FlagStride * c + q) : "memory");
+      }
     }
   } else {
     // ------------------------------------------------------------ dequant
@@ -338,8 +435,10 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + CF::kACol0;
     int cs = 0, as = 0;
     uint32_t cround = 0, around = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int rt = tile / P.ttiles;
+    SegIt it = seg_begin(P, S, ntiles);
+    Seg sg;
+    while (seg_next(P, S, ntiles, it, sg)) {
+      const int rt = sg.tile / P.ttiles;
       const int rb = 4 * rt + q;
       const bool live = rb < P.RB;
       // the row's 16 fp16 LUT values
@@ -358,7 +457,7 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
           T[2 * i + 1] = f.y;
         }
       }
-      for (int sp = 0; sp < S; ++sp) {
+      for (int sp = sg.s0; sp < sg.s1; ++sp) {
         const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
         mbar_wait(bars + kQCFull + 8 * cs, cround & 1);
         uint32_t v[16 * kK2Cps];
@@ -470,6 +569,15 @@ EncodeTiled encode_tiled() {
   return fn;
 }
 
+// Stream-K when the tiles are one token tile wide and do not fill the SMs in
+// whole waves. Its cost is one fp32 partial (128 x NT) per split tile, so at
+// NT = 128 only for at most half a wave of tiles (gate, m = 128: 112 tiles,
+// round-robin 36.7 us against 40.4 us split; down: 32 tiles, 95 -> 52 us).
+bool k2_stream_k(int ntiles, int ttiles, int S, int NT, int sms) {
+  const long long U = (long long)ntiles * S;
+  return ttiles == 1 && ntiles % sms != 0 && U >= sms && U <= INT32_MAX && (NT == 64 || 2 * ntiles <= sms);
+}
+
 template <int NT>
 void launch_k2(const LutTensor* t, const void* x, int64_t m, void* y, float* y32, cudaStream_t s) {
   using CF = K2Cfg<NT>;
@@ -497,23 +605,35 @@ void launch_k2(const LutTensor* t, const void* x, int64_t m, void* y, float* y32
   P.rtiles = (t->RB + 3) / 4;
   P.ttiles = (int)((m + NT - 1) / NT);
   const int ntiles = P.rtiles * P.ttiles;
-  const int grid = std::min(ntiles, t->sms);
+  const int S = (P.C + kK2Cps - 1) / kK2Cps;
+  P.sk = k2_stream_k(ntiles, P.ttiles, S, NT, t->sms);
+  const int grid = P.sk ? t->sms : std::min(ntiles, t->sms);
+  P.part = P.sk ? stream_scratch_f32(s, (size_t)grid * NT * 128) : nullptr;
+  P.flags = P.sk ? stream_ws(s).k2flags : nullptr;
   ensure_dyn_smem((const void*)k_lutgemm_k2<NT>, (int)CF::kSmem);
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 0;
+  attr[1].id = cudaLaunchAttributeCooperative;  // stream-K: finishers wait on other CTAs
+  attr[1].val.cooperative = 1;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)grid);
   lc.blockDim = dim3(kK2T);
   lc.dynamicSmemBytes = CF::kSmem;
   lc.stream = s;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = P.sk ? 2 : 1;
   ANYQ_CUDA(cudaLaunchKernelEx(&lc, k_lutgemm_k2<NT>, map, P));
   ANYQ_LAUNCHED();
 }
 
 }  // namespace
+
+bool lutgemm_k2_long_k(const LutTensor* t, int64_t m) {
+  if (!t || m < 1 || m > 128) return false;
+  const int NT = m <= 64 ? 64 : 128, ntiles = (t->RB + 3) / 4, S = (t->C + kK2Cps - 1) / kK2Cps;
+  return k2_stream_k(ntiles, 1, S, NT, t->sms) && (long long)ntiles * S >= 8LL * t->sms;
+}
 
 bool lutgemm_k2_supports(const LutTensor* t, int64_t m) {
   return t && m >= 1 && t->gv_gshift >= 0 && (t->cols % 8) == 0 && m <= (int64_t)INT32_MAX;

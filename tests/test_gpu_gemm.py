@@ -314,6 +314,10 @@ def test_auto_path_choice_and_agreement(aq, orc, cuda):
     assert [tall.auto_path(m) for m in (1, 2, 8, 16, 17, 128, 129)] == \
         [aq.PATH_GEMV] + [aq.PATH_GEMV_TC] * 3 + [aq.PATH_K2] * 2 + [aq.PATH_DEQUANT]
     tall.close()
+    # down-shaped (32 row tiles, K = 14336): K2 split stream-K over every SM from m = 16
+    down = aq.DeviceTensor(aq.quantize_any(orc.gaussian(4096, 14336, 11), cfg(codebook=3, max_iters=1)))
+    assert [down.auto_path(m) for m in (16, 64, 128, 129)] == [aq.PATH_K2] * 3 + [aq.PATH_DEQUANT]
+    down.close()
 
 
 def test_gemm_chain_deps_decoder_pattern(aq, orc, cuda):

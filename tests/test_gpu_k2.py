@@ -54,3 +54,23 @@ def test_k2_deterministic(aq, orc, cuda):
     a, _ = tc_gemm(aq, cuda, qt, x, K2)
     b, _ = tc_gemm(aq, cuda, qt, x, K2)
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+# stream-K (one token tile, tiles not a whole number of waves): a tile split
+# over CTAs is finished by the CTA holding its step 0, adding the later CTAs'
+# fp32 partials in k order. (512, 14336): 4 tiles x 56 steps on 148 CTAs, every
+# tile split over ~37 CTAs; (14336, 4096): the gate shape, 112 tiles x 16 steps.
+@pytest.mark.parametrize("n,k,m", [(4096, 4096, 16), (4096, 4096, 128), (512, 14336, 64), (14336, 4096, 33),
+                                   (4224, 1024, 100)])
+def test_k2_stream_k(aq, orc, cuda, n, k, m):
+    qt = aq.quantize_any(orc.gaussian(n, k, 51), cfg(codebook=3, granularity=3, group_size=128, seed=1, max_iters=2))
+    check(aq, orc, cuda, qt, bf16(orc.gaussian(m, k, 53)))
+
+
+def test_k2_stream_k_deterministic(aq, orc, cuda):
+    qt = aq.quantize_any(orc.gaussian(512, 14336, 7), cfg(codebook=3, granularity=3, group_size=128, max_iters=2))
+    x = bf16(orc.gaussian(64, 14336, 8))
+    a, _ = tc_gemm(aq, cuda, qt, x, K2)
+    for _ in range(3):
+        b, _ = tc_gemm(aq, cuda, qt, x, K2)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
