@@ -702,11 +702,11 @@ def gpu_arm(args):
                 d.close()
 
     # ---- M sweep (per-GEMM launches, AUTO path: GEMV for m <= 4 while its x image fits,
-    # else tcgen05; fused mma for 5..32; dequant + cuBLAS above)
+    # else tcgen05; K2 for 16..128 on tall or long-K tensors; fused mma for 5..32; dequant + cuBLAS above)
     sweep = {}
     tpeak = hbm_peak_tflops()
     if not args.quick and P == 1:
-        for mm in (1, 2, 3, 4, 8, 16, 32, 64, 256, 1024, 4096):
+        for mm in (1, 2, 3, 4, 8, 16, 32, 64, 128, 256, 1024, 4096):
             xm = {k: torch.randn(mm, k, device=dev).to(torch.bfloat16) for k in (D, FF)}
             for j, (name, n, k) in enumerate(LAYER):
                 if name not in ("q", "gate", "down"):

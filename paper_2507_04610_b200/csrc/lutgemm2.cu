@@ -9,7 +9,13 @@
 //
 // A CTA computes 128 W rows x NT tokens tiles (persistent, round-robin over the
 // tiles, tokens innermost so concurrently running CTAs share the weight rows in
-// L2). A pipeline step covers kK2Cps = 2 chunks of 128 k (one step per chunk
+// L2). When the tiles are one token tile wide and leave SMs idle in the last
+// wave (14336 rows = 112 tiles on 148 SMs; 4096 rows = 32), the launch is split
+// stream-K: every CTA takes an equal run of the tiles' k-steps; a segment that
+// starts past a tile's step 0 stores its fp32 partial and raises a ready flag
+// per epilogue warp (release), and the CTA whose segment holds step 0 adds the
+// later CTAs' partials in k order (acquire) before storing y — deterministic,
+// and every CTA is co-resident (cooperative launch, one CTA per SM). A pipeline step covers kK2Cps = 2 chunks of 128 k (one step per chunk
 // measured 15% slower: the per-step barriers and waits dominate). Per step:
 //  * an x producer lane issues the x tile as TMA tensor loads (box 64 k x
 //    NT tokens, SWIZZLE_128B: the canonical UMMA K-major layout) into a 2-4
