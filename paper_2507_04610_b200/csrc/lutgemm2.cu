@@ -60,6 +60,7 @@ constexpr int kK2AStages = 4 / kK2Cps;             // A stages in TMEM (64 colum
 constexpr uint32_t kK2Codes = 4 * kK2Cps * 2048;   // codes of one step: 4 row blocks x kK2Cps chunks
 constexpr uint32_t kK2Ab = 4 * kK2Cps * 128;       // alpha/beta lines of one step (at most one per chunk)
 constexpr uint32_t kK2CStage = kK2Codes + kK2Ab;
+constexpr int kK2SkStage = 4;  // stream-K contributors staged per round (4 KB each per epilogue warp)
 constexpr uint32_t kK2Tbl = 16 * 64;      // one chunk's table of a row block: 16 entries x 32 rows x bf16
 
 template <int NT>
@@ -76,6 +77,7 @@ struct K2Cfg {
   static constexpr int kTmemCols = 512;
   static_assert(kACol0 + kK2AStages * 64 * kK2Cps <= kTmemCols, "TMEM budget");
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
+  static_assert(4u * kK2SkStage * 4096u <= kXStages * kB, "stream-K staging fits the x ring");
   // kind::f16 instruction descriptor: D f32 (bit 4), A and B bf16 (format 1 at
   // bits 7 and 10), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   static constexpr uint32_t kIdesc =
@@ -165,6 +167,10 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
           dst),
       "l"(map), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -388,6 +394,24 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       const int64_t t0 = (int64_t)tt * NT;
       for (int c0 = 0; c0 < NT; c0 += 32) {
         if (t0 + c0 >= P.M) break;  // no token of this column block (warp-uniform)
+        // finisher: this warp's 32 x 32 block of every contributor's partial is
+        // staged in the x ring (idle once the CTA's last segment is committed)
+        // by cp.async, all contributors in flight at once (a register load per
+        // contributor costs one L2 round trip each); 4 contributors per round
+        float* stg = reinterpret_cast<float*>(smem + CF::kOffB) + q * (kK2SkStage * 1024);
+        int cs0 = b + 1;
+        if (finish) {
+          const int n0 = min(cend - cs0, kK2SkStage);
+          for (int cc = 0; cc < n0; ++cc) {
+            const float* src = P.part + ((size_t)(cs0 + cc) * NT + c0) * 128 + 32 * q;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {  // 256 16-B pieces: column (i*32+lane)/8, piece %8
+              const int idx = i * 32 + lane, col = idx >> 3, pc = idx & 7;
+              cp_async16(stg + cc * 1024 + col * 32 + pc * 4, src + (size_t)col * 128 + pc * 4);
+            }
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)db * NT + c0, r);
         // partials move whole 32-column blocks, unpredicated (a load under a
@@ -397,15 +421,32 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
           float* pp = P.part + ((size_t)b * NT + c0) * 128 + 32 * q + lane;
 #pragma unroll
           for (int j = 0; j < 32; ++j) __stcg(pp + j * 128, __uint_as_float(r[j]));
-        } else if (row < P.N) {
-          for (int c = b + 1; c < cend; ++c) {
-            const float* pp = P.part + ((size_t)c * NT + c0) * 128 + 32 * q + lane;
-            float pv[32];
+        } else {
+          while (cs0 < cend) {  // in k order
+            const int n0 = min(cend - cs0, kK2SkStage);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            for (int cc = 0; cc < n0; ++cc)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) pv[j] = __ldcg(pp + j * 128);
+              for (int j = 0; j < 32; ++j)
+                r[j] = __float_as_uint(__uint_as_float(r[j]) + stg[cc * 1024 + j * 32 + lane]);
+            cs0 += n0;
+            if (cs0 < cend) {  // more than kK2SkStage contributors: next round
+              __syncwarp();
+              const int n1 = min(cend - cs0, kK2SkStage);
+              for (int cc = 0; cc < n1; ++cc) {
+                const float* src = P.part + ((size_t)(cs0 + cc) * NT + c0) * 128 + 32 * q;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + pv[j]);
+                for (int i = 0; i < 8; ++i) {
+                  const int idx = i * 32 + lane, col = idx >> 3, pc = idx & 7;
+                  cp_async16(stg + cc * 1024 + col * 32 + pc * 4, src + (size_t)col * 128 + pc * 4);
+                }
+              }
+              asm volatile("cp.async.commit_group;" ::: "memory");
+            }
           }
+          __syncwarp();
+          if (row < P.N) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t m = t0 + c0 + j;
@@ -414,6 +455,7 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
               P.y[m * P.N + row] = __float2bfloat16_rn(v);
               if (P.y32) P.y32[m * P.N + row] = v;
             }
+          }
           }
         }
       }
