@@ -619,11 +619,13 @@ EncodeTiled encode_tiled() {
 
 // Stream-K when the tiles are one token tile wide and do not fill the SMs in
 // whole waves. Its cost is one fp32 partial (128 x NT) per split tile, so at
-// NT = 128 only for at most half a wave of tiles (gate, m = 128: 112 tiles,
-// round-robin 36.7 us against 40.4 us split; down: 32 tiles, 95 -> 52 us).
+// NT = 128 only for at most half a wave of tiles or >= 24 steps per CTA (gate,
+// m = 128, 12 steps per CTA: round-robin 38.6 us against 39.6 us split; down,
+// 32 tiles: 95 -> 46 us; 70B gate, 224 tiles x 32 steps: 116 -> 100 us).
 bool k2_stream_k(int ntiles, int ttiles, int S, int NT, int sms) {
   const long long U = (long long)ntiles * S;
-  return ttiles == 1 && ntiles % sms != 0 && U >= sms && U <= INT32_MAX && (NT == 64 || 2 * ntiles <= sms);
+  return ttiles == 1 && ntiles % sms != 0 && U >= sms && U <= INT32_MAX &&
+         (NT == 64 || 2 * ntiles <= sms || U >= 24LL * sms);
 }
 
 template <int NT>
