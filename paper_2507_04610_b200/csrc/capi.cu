@@ -744,6 +744,15 @@ int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
   // (it splits K over every SM, which wins on small N); dequant + cuBLAS above
   const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
   const bool many_rows = lt->RB >= 2 * lt->sms;
+  // K2's cost is flat in m up to its 64-token tile, so it takes over below
+  // m = 16 where the GEMV kernels' per-row cost has grown past it: from m = 9
+  // on tall tensors (gate m = 12: 30.4 us against K1t's 32.0), from m = 5 on
+  // tall tensors with K >= 8192 (70B gate m = 8: 85 against 110), from m = 8 on
+  // long-K tensors it splits stream-K (70B q / down m = 12: 32.7 / 32.0 us
+  // against 35.9 / 34.8)
+  if (m >= 5 && m < 16 && lutgemm_k2_supports(lt, m) &&
+      (many_rows ? (m >= 9 || lt->C >= 64) : (m >= 8 && lutgemm_k2_long_k(lt, m))))
+    return ANYQ_PATH_K2;
   try {
     // K1t only when one x image fits: its K-sliced form (a grid-wide wait per
     // slice) measured slower than the fallbacks below (gate m = 9: 65 vs 31 us)
