@@ -490,20 +490,20 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
       const int rb = 4 * rt + q;
       const bool live = rb < P.RB;
       // the row's 16 fp16 LUT values
-      float T[16];
+      // this warp builds table entries 4j..4j+3 only: the row's fp16 LUT
+      // entries 8(j/2)..+7 are one 16-B load, the half picked by selects (a
+      // runtime index into a register array would go through local memory)
+      float T[4];
       {
-        uint4 l0 = make_uint4(0, 0, 0, 0), l1 = l0;
-        if (live) {
-          l0 = P.lut[((size_t)rb * 32 + lane) * 2];
-          l1 = P.lut[((size_t)rb * 32 + lane) * 2 + 1];
-        }
-        const uint32_t lw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&lw[i]));
-          T[2 * i] = f.x;
-          T[2 * i + 1] = f.y;
-        }
+        uint4 l = make_uint4(0, 0, 0, 0);
+        if (live) l = P.lut[((size_t)rb * 32 + lane) * 2 + (j >> 1)];
+        const uint32_t w0 = (j & 1) ? l.z : l.x, w1 = (j & 1) ? l.w : l.y;
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&w0));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&w1));
+        T[0] = f0.x;
+        T[1] = f0.y;
+        T[2] = f1.x;
+        T[3] = f1.y;
       }
       for (int sp = sg.s0; sp < sg.s1; ++sp) {
         const int c0 = sp * kK2Cps, nc = min(kK2Cps, C - c0);
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kK2T, 1) k_lutgemm_k2(const __grid_constant__ 
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 tbl[(4 * j + i) * 32 + lane] = __bfloat16_as_ushort(
-                    __float2bfloat16_rn(__fadd_rn(__fmul_rn(ab[h].x, T[4 * j + i]), ab[h].y)));
+                    __float2bfloat16_rn(__fadd_rn(__fmul_rn(ab[h].x, T[i]), ab[h].y)));
             }
           }
           asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
