@@ -736,12 +736,14 @@ int64_t anyq_dev_tensor_cols(const anyq_dev_tensor* t) {
 }
 
 int32_t anyq_dev_gemm_auto_path(const anyq_dev_tensor* t, int64_t m) {
-  // measured crossovers on B200 (profiles/round2_k1t.md): the CUDA-core GEMV
-  // at m = 1 (and m = 2 for fewer than 2 row blocks per SM); K1t (tcgen05
-  // GEMV) for 3 <= m <= 4, and up to m = 16 with at least 2 row blocks per
-  // SM, while its shared-memory plan fits; K2 for 16 <= m <= 128 on tall
-  // tensors; the fused dequant-to-shared-memory mma.sync kernel up to m = 32
-  // (it splits K over every SM, which wins on small N); dequant + cuBLAS above
+  // measured crossovers on B200 (profiles/round2_k1t.md,
+  // profiles/round2_k2_stream_k.md): the CUDA-core GEMV at m = 1 (and m = 2
+  // for fewer than 2 row blocks per SM); K1t (tcgen05 GEMV) for 3 <= m <= 4,
+  // and up to m = 8 with at least 2 row blocks per SM, while its shared-memory
+  // plan fits; K2 up to m = 128 on tall tensors (from m = 9, or m = 5 with
+  // K >= 8192) and on long-K tensors it splits stream-K (from m = 8); the fused
+  // dequant-to-shared-memory mma.sync kernel up to m = 32 (it splits K over
+  // every SM, which wins on small N); dequant + cuBLAS above
   const LutTensor* lt = reinterpret_cast<const LutTensor*>(t);
   const bool many_rows = lt->RB >= 2 * lt->sms;
   // K2's cost is flat in m up to its 64-token tile, so it takes over below
